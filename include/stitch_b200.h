@@ -1,0 +1,272 @@
+/*
+ * stitch_b200.h -- C ABI of the B200-native per-frame stitching path.
+ *
+ * Drop-in boundary for the reference's
+ *   ProcessResult stitch::process_frame(PipelineState&, const std::vector<Frame>&)
+ *   (/root/reference/proj/include/stitch/pipeline.hpp:79-80,
+ *    impl proj/src/pipeline.cpp:259-360).
+ * A context (stitch_b200_ctx) is the device-resident twin of one
+ * PipelineState (pipeline.hpp:47-63): canvas, per-view inverse maps, pairs
+ * {view, bounds, blend weights, 3D-M window}, threshold history, frame
+ * counter.  One context per panorama stream; not thread-shared.
+ *
+ * Plain C types only; no exceptions cross this boundary.  Every entry point
+ * returns STITCH_B200_OK (0) or a positive code mirroring stitch::ErrorCode
+ * (proj/include/stitch/types.hpp:9-27) offset by 1; the message of the last
+ * failure on the calling thread is available from stitch_b200_last_error().
+ */
+#ifndef STITCH_B200_H
+#define STITCH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STITCH_B200_MAX_VIEWS 16
+#define STITCH_B200_MAX_PAIRS 16
+
+/* Return codes: 0 = OK, else 1 + stitch::ErrorCode (types.hpp:9-27),
+ * plus codes >= 100 for device/runtime failures. */
+enum stitch_b200_status {
+  STITCH_B200_OK = 0,
+  STITCH_B200_EmptyRegion = 1,
+  STITCH_B200_EmptyHistogram = 2,
+  STITCH_B200_RankDeficient = 3,
+  STITCH_B200_RegionTooSmall = 4,
+  STITCH_B200_InsufficientMatches = 5,
+  STITCH_B200_NoConsensus = 6,
+  STITCH_B200_ShapeMismatch = 7,
+  STITCH_B200_NoOverlap = 8,
+  STITCH_B200_SingularHomography = 9,
+  STITCH_B200_DegeneratePose = 10,
+  STITCH_B200_EmptyProjection = 11,
+  STITCH_B200_MissingState = 12,
+  STITCH_B200_TooSmall = 13,
+  STITCH_B200_ConfigError = 14,
+  STITCH_B200_ConfigurationError = 15,
+  STITCH_B200_InputMismatch = 16,
+  STITCH_B200_IoError = 17,
+  STITCH_B200_CudaError = 100,
+  STITCH_B200_Unsupported = 101
+};
+
+/* CameraIntrinsics + CameraExtrinsics (geometry.hpp:11-30). */
+typedef struct {
+  double fx, fy, cx, cy;
+  double rotation[9]; /* row-major, world -> camera */
+  double translation[3];
+} stitch_b200_camera;
+
+/* StitchConfig (pipeline.hpp:33-44) restricted to what the per-frame path
+ * consumes.  refine_enabled must be 0: feature refinement is init-only and
+ * out of scope; pass refined maps through
+ * stitch_b200_create() instead. */
+typedef struct {
+  int n_views;
+  int reference;
+  int width[STITCH_B200_MAX_VIEWS];
+  int height[STITCH_B200_MAX_VIEWS];
+  stitch_b200_camera cams[STITCH_B200_MAX_VIEWS];
+  /* BalanceConfig, color_balance.hpp:19-25 */
+  double lambda;
+  double gamma_dark, gamma_bright;
+  int target_black, target_white;
+  /* FlowOptions, flow.hpp:29-34 */
+  int flow_levels, flow_iterations;
+  double smoothness;
+  int window_capacity; /* 1..3 (clamped like TransferWindow) */
+  int fuse_weighting;  /* 0 = own (OwnWeightOnOwnFlow), 1 = cross */
+  int topology;        /* 0 = auto (star <= 3 views, chain beyond), 1 star, 2 chain */
+  int refine_enabled;  /* must be 0 */
+} stitch_b200_config;
+
+/* Fill a config with the reference defaults (pipeline.hpp:23-44,
+ * color_balance.hpp:19-25, flow.hpp:29-34) and refine disabled. */
+void stitch_b200_config_defaults(stitch_b200_config* cfg);
+
+/* POD snapshot of an initialised PipelineState: the exact values the
+ * reference's process_frame reads (pipeline.cpp:259-360). */
+typedef struct {
+  int view;    /* PairState::view */
+  int partner; /* reference view (star) or neighbour (chain extension) */
+  int x0, y0, x1, y1;    /* PairState::bounds (types.hpp:47-62) */
+  const float* theta_i;  /* PairState::weights.theta_i, (y1-y0)*(x1-x0), row-major */
+} stitch_b200_pair;
+
+typedef struct {
+  int canvas_width, canvas_height; /* CanvasGeometry (geometry.hpp:87-91) */
+  double canvas_offset[2];
+  int n_views, reference;
+  int view_width[STITCH_B200_MAX_VIEWS];
+  int view_height[STITCH_B200_MAX_VIEWS];
+  /* warp_maps[v].h.inverse() exactly as pipeline.cpp:40 computes it (raw
+   * Eigen cofactor inverse, not renormalised), row-major. */
+  double inv_maps[STITCH_B200_MAX_VIEWS][9];
+  int n_pairs;
+  stitch_b200_pair pairs[STITCH_B200_MAX_PAIRS];
+  /* StitchConfig fields read per frame */
+  int window_capacity;
+  double lambda, gamma_dark, gamma_bright;
+  int target_black, target_white;
+  int flow_levels, flow_iterations;
+  double smoothness;
+  int fuse_weighting;
+} stitch_b200_init;
+
+/* FrameReport (report.hpp:38-45) without the host-only fields. */
+typedef struct {
+  long long frame_index;
+  int n_pairs;
+  double color_matrices[STITCH_B200_MAX_PAIRS][9]; /* row-major M per pair */
+  int rank_deficient[STITCH_B200_MAX_PAIRS];
+  int threshold_m1[3], threshold_m2[3];
+  int balanced; /* 0 when the panorama histogram was empty */
+  /* Stage::{GeometricWarping, ColorCorrection, LocalWarping, ImageBlending}
+   * (report.hpp:11-17), device milliseconds from CUDA events. */
+  double stage_ms[4];
+} stitch_b200_report;
+
+typedef struct stitch_b200_ctx stitch_b200_ctx;
+
+const char* stitch_b200_last_error(void);
+const char* stitch_b200_version(void);
+
+/* Create a device context from a state snapshot (reference-side
+ * initialize() output).  Copies everything it needs. */
+int stitch_b200_create(const stitch_b200_init* init, int device,
+                       stitch_b200_ctx** out);
+
+/* Standalone initialize (pipeline.cpp:209-257 with refinement off): camera
+ * homographies, canvas, pairs, overlap bounds and blend weights.  The warp
+ * masks are evaluated on the device with the per-frame warp sampler. */
+int stitch_b200_initialize(const stitch_b200_config* cfg, int device,
+                           stitch_b200_ctx** out);
+
+/* Re-upload geometry (re-refinement, pipeline.cpp:395-406): the 3D-M
+ * windows, threshold history and frame counter are kept. */
+int stitch_b200_update_geometry(stitch_b200_ctx* ctx,
+                                const stitch_b200_init* init);
+
+void stitch_b200_destroy(stitch_b200_ctx* ctx);
+
+/* Geometry of a context. */
+int stitch_b200_canvas(const stitch_b200_ctx* ctx, int* width, int* height,
+                       double* offset_x, double* offset_y);
+int stitch_b200_n_pairs(const stitch_b200_ctx* ctx);
+int stitch_b200_get_pair(const stitch_b200_ctx* ctx, int k,
+                         stitch_b200_pair* pair, float* theta_i_out);
+int stitch_b200_view_bbox(const stitch_b200_ctx* ctx, int view, int bbox[4]);
+int stitch_b200_get_inv_map(const stitch_b200_ctx* ctx, int view,
+                            double inv[9]);
+
+/* One frame through the stage order (pipeline.cpp:259-360).
+ * frames[v]: host RGB8 (width*height*3), pinned or pageable.  Outputs:
+ * pano_rgb (canvas w*h*3) and pano_mask (w*h, 0/1) in host memory; either
+ * may be NULL to skip that copy.  report may be NULL.  Synchronous, like the
+ * reference. */
+int stitch_b200_process(stitch_b200_ctx* ctx, const uint8_t* const* frames,
+                        uint8_t* pano_rgb, uint8_t* pano_mask,
+                        stitch_b200_report* report);
+
+/* Device-resident variant: frames[v] are device pointers; outputs stay in
+ * the context (see stitch_b200_device_pano).  Enqueued on the context's
+ * stream; returns without synchronising unless report != NULL. */
+int stitch_b200_process_device(stitch_b200_ctx* ctx,
+                               const uint8_t* const* dev_frames,
+                               stitch_b200_report* report);
+
+/* Device pointers of the context's last panorama (rgb w*h*3, mask w*h). */
+int stitch_b200_device_pano(const stitch_b200_ctx* ctx, uint8_t** rgb,
+                            uint8_t** mask);
+
+/* The CUDA stream (cudaStream_t) the context enqueues on. */
+void* stitch_b200_stream(const stitch_b200_ctx* ctx);
+int stitch_b200_synchronize(stitch_b200_ctx* ctx);
+
+/* Number of kernel launches one processed frame issues. */
+int stitch_b200_launches_per_frame(const stitch_b200_ctx* ctx);
+
+/* Profiling: run one frame's launch plan eagerly (not as a graph) on the
+ * context stream with a CUDA event pair around every kernel launch.
+ * dev_frames as for stitch_b200_process_device.  Writes up to max_ops
+ * (kernel-kind, milliseconds) pairs and returns the number of launches, or
+ * a negative status.  Kinds: 0 crop_warp, 1 pair_stats, 2 pair_solve,
+ * 3 flow_prepare, 4 pyr_down, 5 upsample, 6 hs_iter, 7 canvas, 8 balance,
+ * 9 tone.  Advances the temporal state like a processed frame. */
+int stitch_b200_profile_frame(stitch_b200_ctx* ctx,
+                              const uint8_t* const* dev_frames, int max_ops,
+                              int* kinds, float* ms);
+
+/* Pinned host memory helpers (cudaHostAlloc / cudaFreeHost). */
+void* stitch_b200_host_alloc(size_t bytes);
+void stitch_b200_host_free(void* p);
+/* Device memory helpers for callers without another allocator. */
+void* stitch_b200_device_alloc(int device, size_t bytes);
+void stitch_b200_device_free(void* p);
+int stitch_b200_memcpy_h2d(void* dst, const void* src, size_t bytes);
+int stitch_b200_memcpy_d2h(void* dst, const void* src, size_t bytes);
+
+/* ---- per-stage debug readback of the last processed frame ---- */
+/* Raw warped crops of pair k (side 0 = view, 1 = partner), bounds-sized,
+ * RGB8 + mask, before color correction. */
+int stitch_b200_debug_crop(stitch_b200_ctx* ctx, int k, int side,
+                           int corrected, uint8_t* rgb, uint8_t* mask);
+/* Final level-0 flow of pair k, dir 0 = view->partner, 1 = partner->view,
+ * zeroed at invalid pixels (flow.cpp:178-185). */
+int stitch_b200_debug_flow(stitch_b200_ctx* ctx, int k, int dir, float* u,
+                           float* v);
+/* Pre-balance panorama (after composition). */
+int stitch_b200_debug_prebalance(stitch_b200_ctx* ctx, uint8_t* rgb,
+                                 uint8_t* mask);
+/* Full warped view v over the canvas (evaluated on demand with the same
+ * device sampler, raw, before color correction). */
+int stitch_b200_debug_warp_view(stitch_b200_ctx* ctx, int view,
+                                const uint8_t* host_frame, uint8_t* rgb,
+                                uint8_t* mask);
+
+/* ---- synthetic scenes (SynthScene, proj/include/stitch/synth.hpp) ---- */
+typedef struct {
+  int frame, view;
+  double gains[3];
+} stitch_b200_flicker;
+
+typedef struct {
+  uint64_t seed;
+  int views, frames, width, height;
+  double overlap_fraction;
+  int n_casts;
+  double color_casts[STITCH_B200_MAX_VIEWS][3];
+  int n_flicker;
+  stitch_b200_flicker flicker[16];
+  int object_enabled;
+  double object_depth_fraction, object_half_size;
+  double object_position[2], object_velocity[2];
+  double perturb_focal_scale, perturb_principal_px;
+  /* 0 = auto: the reference yaw rig (synth.cpp:60-152) for <= 3 views, the
+   * strip rig (N-view extension: small toe-in yaw, baseline solved for the
+   * overlap fraction) beyond. 1 = yaw, 2 = strip. */
+  int rig;
+  double strip_yaw; /* radians per view step for the strip rig */
+} stitch_b200_synth_spec;
+
+typedef struct stitch_b200_synth stitch_b200_synth;
+
+void stitch_b200_synth_defaults(stitch_b200_synth_spec* spec);
+int stitch_b200_synth_create(const stitch_b200_synth_spec* spec,
+                             stitch_b200_synth** out);
+void stitch_b200_synth_destroy(stitch_b200_synth* s);
+int stitch_b200_synth_reference(const stitch_b200_synth* s);
+/* Pipeline config carrying the (optionally perturbed) cameras, refine off. */
+int stitch_b200_synth_config(const stitch_b200_synth* s,
+                             stitch_b200_config* cfg);
+/* render_view (synth.cpp:203-231) into width*height*3 bytes. */
+int stitch_b200_synth_render(const stitch_b200_synth* s, int view, int frame,
+                             uint8_t* out, int threads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,965 @@
+// context.cu -- the C ABI (include/stitch_b200.h): device contexts, the
+// per-frame launch plan captured once as a CUDA graph, uploads/downloads,
+// and the standalone initialize() (pipeline.cpp:209-257, refinement off).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "host_geometry.hpp"
+#include "kernels.cuh"
+#include "stitch_b200.h"
+
+using namespace stitch_b200_dev;
+namespace hg_ns = stitch_b200_host;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess)                                                               \
+      return fail(STITCH_B200_CudaError, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+enum OpKind { OP_CROP, OP_STATS, OP_SOLVE, OP_PREP, OP_PYR, OP_UP, OP_HS, OP_CANVAS, OP_BALANCE,
+              OP_TONE, OP_EVENT };
+
+struct Op {
+  OpKind kind;
+  int offset = 0, count = 0;  // task table slice or pair list slice
+  int max_w = 0, max_h = 0, max_px = 0;
+  int event = 0;
+};
+
+}  // namespace
+
+struct Ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  Geometry hg{};           // host mirror of the device geometry
+  Geometry* dg = nullptr;  // device geometry
+  DevState* dst = nullptr;
+  stitch_b200_init init{};  // copy (theta pointers re-pointed at host copies)
+  std::vector<std::vector<float>> theta_host;
+  std::vector<void*> allocs;
+  std::uint8_t* d_frames[kMaxViews] = {};
+  size_t frame_bytes[kMaxViews] = {};
+  uchar4* d_pano = nullptr;
+  std::uint8_t* d_out_rgb = nullptr;
+  std::uint8_t* d_out_mask = nullptr;
+  long long n_px = 0;
+  int max_crop_px = 0;
+  int sweeps = 10;
+  float alpha2 = 225.0f;
+  int n_levels_max = 0;
+  std::vector<Op> plan;
+  HsTask* d_hs = nullptr;
+  UpTask* d_up = nullptr;
+  PyrTask* d_pyr = nullptr;
+  int* d_lists = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int launches = 0;
+  cudaEvent_t ev[6] = {};
+  // pinned ring for device-frame pointer tables
+  const std::uint8_t** h_ptr_ring = nullptr;
+  cudaEvent_t ring_ev[16] = {};
+  int ring_pos = 0;
+  DevReport* h_report = nullptr;
+  bool frames_are_own = true;
+  std::vector<int> pair_levels;
+  float* d_zero = nullptr;
+
+  ~Ctx() {
+    if (stream) cudaStreamSynchronize(stream);
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : ring_ev)
+      if (e) cudaEventDestroy(e);
+    for (void* p : allocs) cudaFree(p);
+    if (h_ptr_ring) cudaFreeHost(h_ptr_ring);
+    if (h_report) cudaFreeHost(h_report);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  template <typename T>
+  cudaError_t alloc(T** p, size_t count) {
+    void* q = nullptr;
+    cudaError_t e = cudaMalloc(&q, std::max<size_t>(count * sizeof(T), 16));
+    if (e != cudaSuccess) return e;
+    allocs.push_back(q);
+    *p = static_cast<T*>(q);
+    return cudaMemset(q, 0, std::max<size_t>(count * sizeof(T), 16));
+  }
+};
+
+struct stitch_b200_ctx {
+  std::unique_ptr<Ctx> c;
+};
+
+namespace {
+
+int validate_init(const stitch_b200_init* in) {
+  if (in->n_views < 2 || in->n_views > kMaxViews)
+    return fail(STITCH_B200_ConfigurationError, "n_views must be in [2, 16]");
+  if (in->reference < 0 || in->reference >= in->n_views)
+    return fail(STITCH_B200_ConfigurationError, "reference view index out of range");
+  if (in->canvas_width <= 0 || in->canvas_height <= 0)
+    return fail(STITCH_B200_ConfigurationError, "empty canvas");
+  if (in->n_pairs < 0 || in->n_pairs > kMaxPairs)
+    return fail(STITCH_B200_ConfigurationError, "too many pairs");
+  for (int v = 0; v < in->n_views; ++v)
+    if (in->view_width[v] <= 0 || in->view_height[v] <= 0)
+      return fail(STITCH_B200_ConfigurationError, "view size must be positive");
+  if (!(in->lambda > 0.0 && in->lambda < 0.5))
+    return fail(STITCH_B200_ConfigError, "balance.lambda must be in (0, 0.5)");
+  if (in->flow_levels < 1 || in->flow_iterations < 1 || !(in->smoothness > 0.0))
+    return fail(STITCH_B200_ConfigError, "flow levels/iterations/smoothness must be positive");
+  for (int k = 0; k < in->n_pairs; ++k) {
+    const stitch_b200_pair& p = in->pairs[k];
+    if (p.view < 0 || p.view >= in->n_views || p.partner < 0 || p.partner >= in->n_views ||
+        p.view == p.partner || p.view == in->reference)
+      return fail(STITCH_B200_ConfigurationError, "bad pair views");
+    if (p.x1 <= p.x0 || p.y1 <= p.y0 || p.x0 < 0 || p.y0 < 0 || p.x1 > in->canvas_width ||
+        p.y1 > in->canvas_height)
+      return fail(STITCH_B200_EmptyRegion, "pair bounds outside the canvas");
+    if (!p.theta_i) return fail(STITCH_B200_MissingState, "pair weights missing");
+  }
+  // a partner must be the reference or a view corrected by an earlier pair
+  for (int k = 0; k < in->n_pairs; ++k) {
+    const int partner = in->pairs[k].partner;
+    if (partner == in->reference) continue;
+    bool found = false;
+    for (int j = 0; j < k; ++j)
+      if (in->pairs[j].view == partner) found = true;
+    if (!found)
+      return fail(STITCH_B200_ConfigurationError,
+                  "pair partner must be the reference or corrected by an earlier pair");
+  }
+  return STITCH_B200_OK;
+}
+
+// Warp validity masks of every view over the full canvas, evaluated on the
+// device with the per-frame sampler's geometry (init only).
+int compute_masks(int device, const Geometry& geom, int n_views,
+                  std::vector<std::vector<std::uint8_t>>& masks) {
+  CUDA_TRY(cudaSetDevice(device));
+  Geometry* d = nullptr;
+  std::uint8_t* dm = nullptr;
+  const size_t n = static_cast<size_t>(geom.canvas_w) * geom.canvas_h;
+  CUDA_TRY(cudaMalloc(&d, sizeof(Geometry)));
+  cudaError_t e = cudaMalloc(&dm, n);
+  if (e != cudaSuccess) {
+    cudaFree(d);
+    return fail(STITCH_B200_CudaError, cudaGetErrorString(e));
+  }
+  e = cudaMemcpy(d, &geom, sizeof(Geometry), cudaMemcpyHostToDevice);
+  masks.assign(n_views, std::vector<std::uint8_t>(n));
+  for (int v = 0; v < n_views && e == cudaSuccess; ++v) {
+    launch_warp_mask(d, v, dm, 0);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpy(masks[v].data(), dm, n, cudaMemcpyDeviceToHost);
+  }
+  cudaFree(d);
+  cudaFree(dm);
+  if (e != cudaSuccess) return fail(STITCH_B200_CudaError, cudaGetErrorString(e));
+  return STITCH_B200_OK;
+}
+
+void fill_views(Geometry& g, const stitch_b200_init* in) {
+  g.canvas_w = in->canvas_width;
+  g.canvas_h = in->canvas_height;
+  g.offx = in->canvas_offset[0];
+  g.offy = in->canvas_offset[1];
+  g.n_views = in->n_views;
+  g.reference = in->reference;
+  for (int v = 0; v < in->n_views; ++v) {
+    g.views[v].width = in->view_width[v];
+    g.views[v].height = in->view_height[v];
+    for (int i = 0; i < 9; ++i) g.views[v].inv[i] = in->inv_maps[v][i];
+  }
+}
+
+int enqueue_op(Ctx* ctx, const Op& op, cudaStream_t s) {
+  const Geometry& g = ctx->hg;
+  switch (op.kind) {
+    case OP_CROP:
+      if (!g.n_pairs) return 0;
+      launch_crop_warp(ctx->dg, g.n_pairs, ctx->max_crop_px, s);
+      return 1;
+    case OP_STATS:
+      launch_pair_stats(ctx->dg, ctx->dst, ctx->d_lists + op.offset, op.count, ctx->max_crop_px, s);
+      return 1;
+    case OP_SOLVE:
+      launch_pair_solve(ctx->dg, ctx->dst, ctx->d_lists + op.offset, op.count, s);
+      return 1;
+    case OP_PREP:
+      if (!g.n_pairs) return 0;
+      launch_flow_prepare(ctx->dg, ctx->dst, g.n_pairs, ctx->max_crop_px, s);
+      return 1;
+    case OP_PYR:
+      launch_pyr_down(ctx->d_pyr + op.offset, op.count, op.max_px, s);
+      return 1;
+    case OP_UP:
+      launch_upsample(ctx->d_up + op.offset, op.count, op.max_px, s);
+      return 1;
+    case OP_HS:
+      launch_hs_iter(ctx->d_hs + op.offset, op.count, op.max_w, op.max_h, ctx->sweeps,
+                     ctx->alpha2, s);
+      return 1;
+    case OP_CANVAS:
+      launch_canvas(ctx->dg, ctx->dst, ctx->d_pano, ctx->n_px, ctx->num_sms, s);
+      return 1;
+    case OP_BALANCE:
+      launch_balance(ctx->dg, ctx->dst, s);
+      return 1;
+    case OP_TONE:
+      launch_tone(ctx->dst, ctx->d_pano, ctx->n_px, ctx->d_out_rgb, ctx->d_out_mask, s);
+      return 1;
+    default:
+      return 0;
+  }
+}
+
+int build_context(const stitch_b200_init* in, int device,
+                  const std::vector<std::vector<std::uint8_t>>* masks_in,
+                  std::unique_ptr<Ctx>& out) {
+  int rc = validate_init(in);
+  if (rc) return rc;
+  auto ctx = std::make_unique<Ctx>();
+  ctx->device = device;
+  CUDA_TRY(cudaSetDevice(device));
+  CUDA_TRY(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
+  CUDA_TRY(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  ctx->init = *in;
+  Geometry& g = ctx->hg;
+  std::memset(&g, 0, sizeof(g));
+  fill_views(g, in);
+  g.n_pairs = in->n_pairs;
+  g.weighting = in->fuse_weighting ? 1 : 0;
+  g.lambda = in->lambda;
+  g.gamma_dark = in->gamma_dark;
+  g.gamma_bright = in->gamma_bright;
+  g.target_black = in->target_black;
+  g.target_white = in->target_white;
+  g.curve_ok = (in->gamma_dark > 0.0 && in->gamma_bright > 0.0 &&
+                in->target_black <= in->target_white)
+                   ? 1
+                   : 0;
+
+  // view footprints (bbox of the warp mask); EmptyProjection if none.
+  std::vector<std::vector<std::uint8_t>> masks_local;
+  const std::vector<std::vector<std::uint8_t>>* masks = masks_in;
+  if (!masks) {
+    rc = compute_masks(device, g, in->n_views, masks_local);
+    if (rc) return rc;
+    masks = &masks_local;
+  }
+  for (int v = 0; v < in->n_views; ++v) {
+    int b[4];
+    if (!hg_ns::mask_bbox((*masks)[v].data(), g.canvas_w, g.canvas_h, b))
+      return fail(STITCH_B200_EmptyProjection, "a view projects to no canvas pixel");
+    for (int i = 0; i < 4; ++i) g.views[v].bbox[i] = b[i];
+  }
+
+  // buffers
+  for (int v = 0; v < in->n_views; ++v) {
+    ctx->frame_bytes[v] = static_cast<size_t>(in->view_width[v]) * in->view_height[v] * 3;
+    CUDA_TRY(ctx->alloc(&ctx->d_frames[v], ctx->frame_bytes[v]));
+    g.frames[v] = ctx->d_frames[v];
+  }
+  ctx->n_px = static_cast<long long>(g.canvas_w) * g.canvas_h;
+  CUDA_TRY(ctx->alloc(&ctx->d_pano, static_cast<size_t>(ctx->n_px) + 4));
+  CUDA_TRY(ctx->alloc(&ctx->d_out_rgb, static_cast<size_t>(ctx->n_px) * 3 + 16));
+  CUDA_TRY(ctx->alloc(&ctx->d_out_mask, static_cast<size_t>(ctx->n_px) + 16));
+
+  ctx->sweeps = std::max(1, in->flow_iterations / 5);  // flow.cpp:79-80
+  ctx->alpha2 = static_cast<float>(in->smoothness * in->smoothness);
+  ctx->theta_host.resize(in->n_pairs);
+  int max_zero = 16;
+  for (int k = 0; k < in->n_pairs; ++k) {
+    const stitch_b200_pair& sp = in->pairs[k];
+    PairDesc& p = g.pairs[k];
+    p.view = sp.view;
+    p.partner = sp.partner;
+    p.x0 = sp.x0;
+    p.y0 = sp.y0;
+    p.w = sp.x1 - sp.x0;
+    p.h = sp.y1 - sp.y0;
+    const int n = p.w * p.h;
+    ctx->max_crop_px = std::max(ctx->max_crop_px, n);
+    max_zero = std::max(max_zero, n);
+    ctx->theta_host[k].assign(sp.theta_i, sp.theta_i + n);
+    ctx->init.pairs[k].theta_i = ctx->theta_host[k].data();
+    float* th;
+    CUDA_TRY(ctx->alloc(&th, n));
+    CUDA_TRY(cudaMemcpy(th, sp.theta_i, sizeof(float) * n, cudaMemcpyHostToDevice));
+    p.theta_i = th;
+    for (int s = 0; s < 2; ++s) {
+      CUDA_TRY(ctx->alloc(&p.crop_raw[s], n));
+      CUDA_TRY(ctx->alloc(&p.crop_cor[s], n));
+    }
+    // dense_flow requires >= 16x16 (flow.cpp:146-148), else zero flow
+    p.flow_ok = (p.w >= 16 && p.h >= 16) ? 1 : 0;
+  }
+  CUDA_TRY(ctx->alloc(&ctx->d_zero, max_zero));
+
+  // pair depth (distance from the reference through partners)
+  std::vector<int> depth(in->n_pairs, 1);
+  int max_depth = 0;
+  for (int k = 0; k < in->n_pairs; ++k) {
+    const int partner = in->pairs[k].partner;
+    if (partner != in->reference)
+      for (int j = 0; j < k; ++j)
+        if (in->pairs[j].view == partner) depth[k] = depth[j] + 1;
+    g.pair_depth[k] = depth[k];
+    max_depth = std::max(max_depth, depth[k]);
+  }
+
+  // ---- flow plan: pyramids (flow.cpp:152-156), per-level tasks ----
+  struct TaskState {
+    int k, dir, L;
+    int dims[kMaxLevels][2];
+    float* U[2];
+    float* V[2];
+    int cur;
+  };
+  std::vector<TaskState> tasks;
+  ctx->pair_levels.assign(in->n_pairs, 0);
+  int Lmax = 0;
+  for (int k = 0; k < in->n_pairs; ++k) {
+    PairDesc& p = g.pairs[k];
+    if (!p.flow_ok) {
+      for (int d = 0; d < 2; ++d) {
+        p.flow_u[d] = ctx->d_zero;
+        p.flow_v[d] = ctx->d_zero;
+      }
+      continue;
+    }
+    int dims[kMaxLevels][2];
+    int L = 1;
+    dims[0][0] = p.w;
+    dims[0][1] = p.h;
+    for (int l = 1; l < in->flow_levels && l < kMaxLevels; ++l) {
+      if (dims[l - 1][0] < 16 || dims[l - 1][1] < 16) break;
+      dims[l][0] = std::max(1, dims[l - 1][0] / 2);
+      dims[l][1] = std::max(1, dims[l - 1][1] / 2);
+      ++L;
+    }
+    ctx->pair_levels[k] = L;
+    Lmax = std::max(Lmax, L);
+    for (int s = 0; s < 2; ++s)
+      for (int l = 0; l < L; ++l) CUDA_TRY(ctx->alloc(&p.pyr[s][l], dims[l][0] * dims[l][1]));
+    for (int d = 0; d < 2; ++d) {
+      TaskState t{};
+      t.k = k;
+      t.dir = d;
+      t.L = L;
+      std::memcpy(t.dims, dims, sizeof(dims));
+      for (int b = 0; b < 2; ++b) {
+        CUDA_TRY(ctx->alloc(&t.U[b], p.w * p.h));
+        CUDA_TRY(ctx->alloc(&t.V[b], p.w * p.h));
+      }
+      t.cur = 0;
+      tasks.push_back(t);
+    }
+  }
+  ctx->n_levels_max = Lmax;
+
+  std::vector<HsTask> hs_table;
+  std::vector<UpTask> up_table;
+  std::vector<PyrTask> pyr_table;
+  std::vector<int> lists;
+  std::vector<Op>& plan = ctx->plan;
+  plan.push_back({OP_EVENT, 0, 0, 0, 0, 0, 0});
+  plan.push_back({OP_CROP});
+  plan.push_back({OP_EVENT, 0, 0, 0, 0, 0, 1});
+  for (int d = 1; d <= max_depth; ++d) {
+    Op op{OP_STATS};
+    op.offset = static_cast<int>(lists.size());
+    for (int k = 0; k < in->n_pairs; ++k)
+      if (depth[k] == d) lists.push_back(k);
+    op.count = static_cast<int>(lists.size()) - op.offset;
+    plan.push_back(op);
+    op.kind = OP_SOLVE;
+    plan.push_back(op);
+  }
+  plan.push_back({OP_PREP});
+  plan.push_back({OP_EVENT, 0, 0, 0, 0, 0, 2});
+  for (int l = 1; l < Lmax; ++l) {
+    Op op{OP_PYR};
+    op.offset = static_cast<int>(pyr_table.size());
+    for (int k = 0; k < in->n_pairs; ++k) {
+      if (ctx->pair_levels[k] <= l) continue;
+      const PairDesc& p = g.pairs[k];
+      // recompute dims
+      int w = p.w, h = p.h;
+      for (int i = 0; i < l - 1; ++i) {
+        w = std::max(1, w / 2);
+        h = std::max(1, h / 2);
+      }
+      const int w2 = std::max(1, w / 2), h2 = std::max(1, h / 2);
+      for (int s = 0; s < 2; ++s) {
+        pyr_table.push_back({p.pyr[s][l - 1], w, h, p.pyr[s][l], w2, h2});
+        op.max_px = std::max(op.max_px, w2 * h2);
+      }
+    }
+    op.count = static_cast<int>(pyr_table.size()) - op.offset;
+    if (op.count) plan.push_back(op);
+  }
+  for (int l = Lmax - 1; l >= 0; --l) {
+    Op up{OP_UP};
+    up.offset = static_cast<int>(up_table.size());
+    for (auto& t : tasks) {
+      if (l >= t.L - 1) continue;  // coarsest level of this task or above
+      const int w = t.dims[l][0], h = t.dims[l][1];
+      const int wi = t.dims[l + 1][0], hi = t.dims[l + 1][1];
+      up_table.push_back({t.U[t.cur], t.V[t.cur], wi, hi, t.U[1 - t.cur], t.V[1 - t.cur], w, h});
+      t.cur ^= 1;
+      up.max_px = std::max(up.max_px, w * h);
+    }
+    up.count = static_cast<int>(up_table.size()) - up.offset;
+    if (up.count) plan.push_back(up);
+    for (int it = 0; it < 5; ++it) {  // 5 warps per level (flow.cpp:78)
+      Op op{OP_HS};
+      op.offset = static_cast<int>(hs_table.size());
+      for (auto& t : tasks) {
+        if (l >= t.L) continue;
+        const PairDesc& p = g.pairs[t.k];
+        const int sa = t.dir == 0 ? 0 : 1, sb = 1 - sa;
+        HsTask h{};
+        h.a = p.pyr[sa][l];
+        h.b = p.pyr[sb][l];
+        h.u_in = t.U[t.cur];
+        h.v_in = t.V[t.cur];
+        h.u_out = t.U[1 - t.cur];
+        h.v_out = t.V[1 - t.cur];
+        h.w = t.dims[l][0];
+        h.h = t.dims[l][1];
+        h.zero_in = (l == t.L - 1 && it == 0) ? 1 : 0;
+        h.zero_invalid = (l == 0 && it == 4) ? 1 : 0;
+        h.mask_a = p.crop_cor[sa];
+        h.mask_b = p.crop_cor[sb];
+        t.cur ^= 1;
+        hs_table.push_back(h);
+        op.max_w = std::max(op.max_w, h.w);
+        op.max_h = std::max(op.max_h, h.h);
+      }
+      op.count = static_cast<int>(hs_table.size()) - op.offset;
+      if (op.count) plan.push_back(op);
+    }
+  }
+  for (auto& t : tasks) {
+    PairDesc& p = g.pairs[t.k];
+    p.flow_u[t.dir] = t.U[t.cur];
+    p.flow_v[t.dir] = t.V[t.cur];
+  }
+  plan.push_back({OP_EVENT, 0, 0, 0, 0, 0, 3});
+  plan.push_back({OP_CANVAS});
+  plan.push_back({OP_EVENT, 0, 0, 0, 0, 0, 4});
+  plan.push_back({OP_BALANCE});
+  plan.push_back({OP_TONE});
+  plan.push_back({OP_EVENT, 0, 0, 0, 0, 0, 5});
+
+  // upload tables + geometry + state
+  CUDA_TRY(ctx->alloc(&ctx->d_hs, hs_table.size() + 1));
+  CUDA_TRY(ctx->alloc(&ctx->d_up, up_table.size() + 1));
+  CUDA_TRY(ctx->alloc(&ctx->d_pyr, pyr_table.size() + 1));
+  CUDA_TRY(ctx->alloc(&ctx->d_lists, lists.size() + 1));
+  if (!hs_table.empty())
+    CUDA_TRY(cudaMemcpy(ctx->d_hs, hs_table.data(), hs_table.size() * sizeof(HsTask),
+                        cudaMemcpyHostToDevice));
+  if (!up_table.empty())
+    CUDA_TRY(cudaMemcpy(ctx->d_up, up_table.data(), up_table.size() * sizeof(UpTask),
+                        cudaMemcpyHostToDevice));
+  if (!pyr_table.empty())
+    CUDA_TRY(cudaMemcpy(ctx->d_pyr, pyr_table.data(), pyr_table.size() * sizeof(PyrTask),
+                        cudaMemcpyHostToDevice));
+  if (!lists.empty())
+    CUDA_TRY(cudaMemcpy(ctx->d_lists, lists.data(), lists.size() * sizeof(int),
+                        cudaMemcpyHostToDevice));
+  CUDA_TRY(ctx->alloc(&ctx->dg, 1));
+  CUDA_TRY(cudaMemcpy(ctx->dg, &g, sizeof(Geometry), cudaMemcpyHostToDevice));
+  CUDA_TRY(ctx->alloc(&ctx->dst, 1));
+  {
+    // window capacity (TransferWindow clamps to 1..3, color_transfer.cpp:8-11)
+    // and identity matrices for every view
+    std::unique_ptr<DevState> hs(new DevState());
+    std::memset(hs.get(), 0, sizeof(DevState));
+    const int cap = std::min(3, std::max(1, in->window_capacity));
+    for (int k = 0; k < kMaxPairs; ++k) hs->windows[k].capacity = cap;
+    for (int v = 0; v < kMaxViews; ++v)
+      for (int i = 0; i < 9; ++i) hs->mview[v][i] = (i % 4 == 0) ? 1.0 : 0.0;
+    for (int c = 0; c < 3; ++c)
+      for (int v = 0; v < 256; ++v) hs->lut[c][v] = static_cast<unsigned char>(v);
+    CUDA_TRY(cudaMemcpy(ctx->dst, hs.get(), sizeof(DevState), cudaMemcpyHostToDevice));
+  }
+  CUDA_TRY(prepare_hs(ctx->sweeps));
+  for (auto& e : ctx->ev) CUDA_TRY(cudaEventCreate(&e));
+  for (auto& e : ctx->ring_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_ptr_ring),
+                         sizeof(void*) * kMaxViews * 16, cudaHostAllocDefault));
+  CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_report), sizeof(DevReport),
+                         cudaHostAllocDefault));
+
+  // ---- capture the per-frame launch sequence once ----
+  cudaStream_t s = ctx->stream;
+  CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  int launches = 0;
+  for (const Op& op : plan) {
+    if (op.kind == OP_EVENT)
+      cudaEventRecordWithFlags(ctx->ev[op.event], s, cudaEventRecordExternal);
+    else
+      launches += enqueue_op(ctx.get(), op, s);
+  }
+  cudaError_t cap_err = cudaStreamEndCapture(s, &ctx->graph);
+  if (cap_err != cudaSuccess)
+    return fail(STITCH_B200_CudaError, std::string("graph capture: ") + cudaGetErrorString(cap_err));
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaGraphInstantiate(&ctx->exec, ctx->graph, 0));
+  ctx->launches = launches;
+  out = std::move(ctx);
+  return STITCH_B200_OK;
+}
+
+int set_frame_pointers(Ctx* ctx, const std::uint8_t* const* ptrs) {
+  const int slot = ctx->ring_pos;
+  ctx->ring_pos = (ctx->ring_pos + 1) % 16;
+  CUDA_TRY(cudaEventSynchronize(ctx->ring_ev[slot]));
+  const std::uint8_t** h = ctx->h_ptr_ring + slot * kMaxViews;
+  for (int v = 0; v < ctx->hg.n_views; ++v) h[v] = ptrs[v];
+  CUDA_TRY(cudaMemcpyAsync(ctx->dg->frames, h, sizeof(void*) * ctx->hg.n_views,
+                           cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(cudaEventRecord(ctx->ring_ev[slot], ctx->stream));
+  return STITCH_B200_OK;
+}
+
+void fill_report(Ctx* ctx, stitch_b200_report* r) {
+  const DevReport& d = *ctx->h_report;
+  std::memset(r, 0, sizeof(*r));
+  r->frame_index = d.frame_index;
+  r->n_pairs = ctx->hg.n_pairs;
+  for (int k = 0; k < ctx->hg.n_pairs; ++k) {
+    for (int i = 0; i < 9; ++i) r->color_matrices[k][i] = d.m[k][i];
+    r->rank_deficient[k] = d.rank_deficient[k];
+  }
+  for (int c = 0; c < 3; ++c) {
+    r->threshold_m1[c] = d.m1[c];
+    r->threshold_m2[c] = d.m2[c];
+  }
+  r->balanced = d.balanced;
+  float t01 = 0, t12 = 0, t23 = 0, t34 = 0, t45 = 0;
+  cudaEventElapsedTime(&t01, ctx->ev[0], ctx->ev[1]);
+  cudaEventElapsedTime(&t12, ctx->ev[1], ctx->ev[2]);
+  cudaEventElapsedTime(&t23, ctx->ev[2], ctx->ev[3]);
+  cudaEventElapsedTime(&t34, ctx->ev[3], ctx->ev[4]);
+  cudaEventElapsedTime(&t45, ctx->ev[4], ctx->ev[5]);
+  r->stage_ms[0] = t01;
+  r->stage_ms[1] = t12 + t45;
+  r->stage_ms[2] = t23;
+  r->stage_ms[3] = t34;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* stitch_b200_last_error(void) { return g_last_error.c_str(); }
+
+const char* stitch_b200_version(void) { return "stitch_b200 0.1 (sm_100a)"; }
+
+void stitch_b200_config_defaults(stitch_b200_config* c) {
+  std::memset(c, 0, sizeof(*c));
+  c->n_views = 2;
+  c->reference = 0;
+  c->lambda = 0.05;
+  c->gamma_dark = 1.5;
+  c->gamma_bright = 1.5;
+  c->target_black = 0;
+  c->target_white = 255;
+  c->flow_levels = 4;
+  c->flow_iterations = 50;
+  c->smoothness = 15.0;
+  c->window_capacity = 3;
+  c->fuse_weighting = 0;
+  c->topology = 0;
+  c->refine_enabled = 0;
+  for (int v = 0; v < STITCH_B200_MAX_VIEWS; ++v) {
+    c->cams[v].fx = c->cams[v].fy = 1.0;
+    c->cams[v].rotation[0] = c->cams[v].rotation[4] = c->cams[v].rotation[8] = 1.0;
+  }
+}
+
+int stitch_b200_create(const stitch_b200_init* init, int device, stitch_b200_ctx** out) {
+  *out = nullptr;
+  std::unique_ptr<Ctx> ctx;
+  int rc = build_context(init, device, nullptr, ctx);
+  if (rc) return rc;
+  *out = new stitch_b200_ctx{std::move(ctx)};
+  return STITCH_B200_OK;
+}
+
+int stitch_b200_initialize(const stitch_b200_config* cfg, int device, stitch_b200_ctx** out) {
+  *out = nullptr;
+  if (cfg->refine_enabled)
+    return fail(STITCH_B200_Unsupported,
+                "feature refinement is init-only and not part of the B200 path; pass refined "
+                "maps through stitch_b200_create");
+  if (cfg->n_views < 2 || cfg->n_views > kMaxViews)
+    return fail(STITCH_B200_ConfigurationError, "n_views must be in [2, 16]");
+  if (cfg->reference < 0 || cfg->reference >= cfg->n_views)
+    return fail(STITCH_B200_ConfigurationError, "reference view index out of range");
+  // camera homographies and pairwise maps (pipeline.cpp:219-229)
+  std::vector<hg_ns::Mat3> cam(cfg->n_views), maps(cfg->n_views);
+  std::vector<std::pair<int, int>> sizes;
+  for (int v = 0; v < cfg->n_views; ++v) {
+    int rc = hg_ns::planar_homography(cfg->cams[v], cam[v]);
+    if (rc) return fail(rc, "camera homography failed (rotation or degenerate pose)");
+  }
+  for (int v = 0; v < cfg->n_views; ++v) {
+    int rc = hg_ns::pairwise_homography(cam[cfg->reference], cam[v], maps[v]);
+    if (rc) return fail(rc, "singular pairwise homography");
+    sizes.emplace_back(cfg->width[v], cfg->height[v]);
+  }
+  const hg_ns::Canvas canvas = hg_ns::compute_canvas(maps, sizes);  // pipeline.cpp:231
+  stitch_b200_init in{};
+  in.canvas_width = canvas.width;
+  in.canvas_height = canvas.height;
+  in.canvas_offset[0] = canvas.offx;
+  in.canvas_offset[1] = canvas.offy;
+  in.n_views = cfg->n_views;
+  in.reference = cfg->reference;
+  for (int v = 0; v < cfg->n_views; ++v) {
+    in.view_width[v] = cfg->width[v];
+    in.view_height[v] = cfg->height[v];
+    hg_ns::Mat3 inv;
+    hg_ns::inverse3(maps[v], inv);  // pipeline.cpp:40
+    for (int i = 0; i < 9; ++i) in.inv_maps[v][i] = inv[i];
+  }
+  in.window_capacity = cfg->window_capacity;
+  in.lambda = cfg->lambda;
+  in.gamma_dark = cfg->gamma_dark;
+  in.gamma_bright = cfg->gamma_bright;
+  in.target_black = cfg->target_black;
+  in.target_white = cfg->target_white;
+  in.flow_levels = cfg->flow_levels;
+  in.flow_iterations = cfg->flow_iterations;
+  in.smoothness = cfg->smoothness;
+  in.fuse_weighting = cfg->fuse_weighting;
+  if (canvas.width <= 0 || canvas.height <= 0 ||
+      static_cast<long long>(canvas.width) * canvas.height > (1ll << 31))
+    return fail(STITCH_B200_ConfigurationError, "canvas size out of range");
+
+  // rebuild_pair_geometry (pipeline.cpp:181-205): warp masks on the device,
+  // overlap bounds and chamfer blend weights on the host (init only).
+  Geometry g{};
+  fill_views(g, &in);
+  std::vector<std::vector<std::uint8_t>> masks;
+  int rc = compute_masks(device, g, cfg->n_views, masks);
+  if (rc) return rc;
+  const auto pairs = hg_ns::build_pairs(cfg->n_views, cfg->reference, cfg->topology);
+  if (static_cast<int>(pairs.size()) > kMaxPairs)
+    return fail(STITCH_B200_ConfigurationError, "too many pairs");
+  std::vector<std::vector<float>> thetas(pairs.size());
+  in.n_pairs = static_cast<int>(pairs.size());
+  for (size_t k = 0; k < pairs.size(); ++k) {
+    int b[4];
+    if (!hg_ns::overlap_bounds(masks[pairs[k].view].data(), masks[pairs[k].partner].data(),
+                               canvas.width, canvas.height, b))
+      return fail(STITCH_B200_ConfigurationError, "adjacent views do not overlap");
+    thetas[k].resize(static_cast<size_t>(b[2] - b[0]) * (b[3] - b[1]));
+    hg_ns::blend_weights(masks[pairs[k].view].data(), masks[pairs[k].partner].data(), canvas.width,
+                         canvas.height, b, thetas[k].data());
+    stitch_b200_pair& p = in.pairs[k];
+    p.view = pairs[k].view;
+    p.partner = pairs[k].partner;
+    p.x0 = b[0];
+    p.y0 = b[1];
+    p.x1 = b[2];
+    p.y1 = b[3];
+    p.theta_i = thetas[k].data();
+  }
+  std::unique_ptr<Ctx> ctx;
+  rc = build_context(&in, device, &masks, ctx);
+  if (rc) return rc;
+  *out = new stitch_b200_ctx{std::move(ctx)};
+  return STITCH_B200_OK;
+}
+
+int stitch_b200_update_geometry(stitch_b200_ctx* h, const stitch_b200_init* init) {
+  Ctx* ctx = h->c.get();
+  if (init->n_pairs != ctx->hg.n_pairs)
+    return fail(STITCH_B200_ConfigurationError, "re-refinement must keep the pair set");
+  std::unique_ptr<Ctx> fresh;
+  int rc = build_context(init, ctx->device, nullptr, fresh);
+  if (rc) return rc;
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  // carry windows, threshold history and the frame counter over
+  // (pipeline.cpp:399-405)
+  CUDA_TRY(cudaMemcpy(&fresh->dst->windows, &ctx->dst->windows, sizeof(DevState::windows),
+                      cudaMemcpyDeviceToDevice));
+  CUDA_TRY(cudaMemcpy(&fresh->dst->balance, &ctx->dst->balance, sizeof(BalanceState),
+                      cudaMemcpyDeviceToDevice));
+  CUDA_TRY(cudaMemcpy(&fresh->dst->frame_counter, &ctx->dst->frame_counter, sizeof(long long),
+                      cudaMemcpyDeviceToDevice));
+  h->c = std::move(fresh);  // the old context is released here
+  return STITCH_B200_OK;
+}
+
+void stitch_b200_destroy(stitch_b200_ctx* h) { delete h; }
+
+int stitch_b200_canvas(const stitch_b200_ctx* hd, int* w, int* h, double* ox, double* oy) {
+  const Ctx* ctx = hd->c.get();
+  if (w) *w = ctx->hg.canvas_w;
+  if (h) *h = ctx->hg.canvas_h;
+  if (ox) *ox = ctx->hg.offx;
+  if (oy) *oy = ctx->hg.offy;
+  return STITCH_B200_OK;
+}
+
+int stitch_b200_n_pairs(const stitch_b200_ctx* h) { return h->c->hg.n_pairs; }
+
+int stitch_b200_get_pair(const stitch_b200_ctx* h, int k, stitch_b200_pair* pair,
+                         float* theta_out) {
+  const Ctx* ctx = h->c.get();
+  if (k < 0 || k >= ctx->hg.n_pairs) return fail(STITCH_B200_ConfigurationError, "bad pair index");
+  *pair = ctx->init.pairs[k];
+  if (theta_out)
+    std::memcpy(theta_out, ctx->theta_host[k].data(), ctx->theta_host[k].size() * sizeof(float));
+  return STITCH_B200_OK;
+}
+
+int stitch_b200_view_bbox(const stitch_b200_ctx* h, int view, int bbox[4]) {
+  const Ctx* ctx = h->c.get();
+  if (view < 0 || view >= ctx->hg.n_views) return fail(STITCH_B200_ConfigurationError, "bad view");
+  for (int i = 0; i < 4; ++i) bbox[i] = ctx->hg.views[view].bbox[i];
+  return STITCH_B200_OK;
+}
+
+int stitch_b200_get_inv_map(const stitch_b200_ctx* h, int view, double inv[9]) {
+  const Ctx* ctx = h->c.get();
+  if (view < 0 || view >= ctx->hg.n_views) return fail(STITCH_B200_ConfigurationError, "bad view");
+  for (int i = 0; i < 9; ++i) inv[i] = ctx->hg.views[view].inv[i];
+  return STITCH_B200_OK;
+}
+
+int stitch_b200_process(stitch_b200_ctx* h, const uint8_t* const* frames, uint8_t* pano_rgb,
+                        uint8_t* pano_mask, stitch_b200_report* report) {
+  Ctx* ctx = h->c.get();
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  for (int v = 0; v < ctx->hg.n_views; ++v) {
+    if (!frames[v]) return fail(STITCH_B200_InputMismatch, "null frame");
+    CUDA_TRY(cudaMemcpyAsync(ctx->d_frames[v], frames[v], ctx->frame_bytes[v],
+                             cudaMemcpyHostToDevice, s));
+  }
+  if (!ctx->frames_are_own) {
+    const std::uint8_t* own[kMaxViews];
+    for (int v = 0; v < ctx->hg.n_views; ++v) own[v] = ctx->d_frames[v];
+    int rc = set_frame_pointers(ctx, own);
+    if (rc) return rc;
+    ctx->frames_are_own = true;
+  }
+  CUDA_TRY(cudaGraphLaunch(ctx->exec, s));
+  if (pano_rgb)
+    CUDA_TRY(cudaMemcpyAsync(pano_rgb, ctx->d_out_rgb, static_cast<size_t>(ctx->n_px) * 3,
+                             cudaMemcpyDeviceToHost, s));
+  if (pano_mask)
+    CUDA_TRY(cudaMemcpyAsync(pano_mask, ctx->d_out_mask, static_cast<size_t>(ctx->n_px),
+                             cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_report, &ctx->dst->report, sizeof(DevReport),
+                           cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  if (report) fill_report(ctx, report);
+  return STITCH_B200_OK;
+}
+
+int stitch_b200_process_device(stitch_b200_ctx* h, const uint8_t* const* dev_frames,
+                               stitch_b200_report* report) {
+  Ctx* ctx = h->c.get();
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  int rc = set_frame_pointers(ctx, dev_frames);
+  if (rc) return rc;
+  ctx->frames_are_own = false;
+  CUDA_TRY(cudaGraphLaunch(ctx->exec, ctx->stream));
+  if (report) {
+    CUDA_TRY(cudaMemcpyAsync(ctx->h_report, &ctx->dst->report, sizeof(DevReport),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    fill_report(ctx, report);
+  }
+  return STITCH_B200_OK;
+}
+
+int stitch_b200_profile_frame(stitch_b200_ctx* h, const uint8_t* const* dev_frames, int max_ops,
+                              int* kinds, float* ms) {
+  Ctx* ctx = h->c.get();
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  int rc = set_frame_pointers(ctx, dev_frames);
+  if (rc) return -rc;
+  ctx->frames_are_own = false;
+  std::vector<cudaEvent_t> evs;
+  std::vector<int> ks;
+  cudaStream_t s = ctx->stream;
+  for (const Op& op : ctx->plan) {
+    if (op.kind == OP_EVENT) continue;
+    cudaEvent_t a, b;
+    CUDA_TRY(cudaEventCreate(&a));
+    CUDA_TRY(cudaEventCreate(&b));
+    CUDA_TRY(cudaEventRecord(a, s));
+    const int n = enqueue_op(ctx, op, s);
+    CUDA_TRY(cudaEventRecord(b, s));
+    if (n == 0) {
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+      continue;
+    }
+    evs.push_back(a);
+    evs.push_back(b);
+    ks.push_back(static_cast<int>(op.kind));
+  }
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  const int n = static_cast<int>(ks.size());
+  for (int i = 0; i < n; ++i) {
+    float t = 0;
+    if (e == cudaSuccess) cudaEventElapsedTime(&t, evs[2 * i], evs[2 * i + 1]);
+    if (i < max_ops) {
+      kinds[i] = ks[i];
+      ms[i] = t;
+    }
+  }
+  for (auto& x : evs) cudaEventDestroy(x);
+  if (e != cudaSuccess) return -fail(STITCH_B200_CudaError, cudaGetErrorString(e));
+  return n;
+}
+
+int stitch_b200_device_pano(const stitch_b200_ctx* h, uint8_t** rgb, uint8_t** mask) {
+  const Ctx* ctx = h->c.get();
+  if (rgb) *rgb = ctx->d_out_rgb;
+  if (mask) *mask = ctx->d_out_mask;
+  return STITCH_B200_OK;
+}
+
+void* stitch_b200_stream(const stitch_b200_ctx* h) { return h->c->stream; }
+
+int stitch_b200_synchronize(stitch_b200_ctx* h) {
+  Ctx* ctx = h->c.get();
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return STITCH_B200_OK;
+}
+
+int stitch_b200_launches_per_frame(const stitch_b200_ctx* h) { return h->c->launches; }
+
+void* stitch_b200_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes, cudaHostAllocDefault) != cudaSuccess) return nullptr;
+  return p;
+}
+
+void stitch_b200_host_free(void* p) { cudaFreeHost(p); }
+
+void* stitch_b200_device_alloc(int device, size_t bytes) {
+  void* p = nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) return nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+  return p;
+}
+
+void stitch_b200_device_free(void* p) { cudaFree(p); }
+
+int stitch_b200_memcpy_h2d(void* dst, const void* src, size_t bytes) {
+  CUDA_TRY(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+  return STITCH_B200_OK;
+}
+
+int stitch_b200_memcpy_d2h(void* dst, const void* src, size_t bytes) {
+  CUDA_TRY(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+  return STITCH_B200_OK;
+}
+
+int stitch_b200_debug_crop(stitch_b200_ctx* h, int k, int side, int corrected, uint8_t* rgb,
+                           uint8_t* mask) {
+  Ctx* ctx = h->c.get();
+  if (k < 0 || k >= ctx->hg.n_pairs || side < 0 || side > 1)
+    return fail(STITCH_B200_ConfigurationError, "bad pair/side");
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  const PairDesc& p = ctx->hg.pairs[k];
+  std::vector<uchar4> buf(static_cast<size_t>(p.w) * p.h);
+  CUDA_TRY(cudaMemcpy(buf.data(), corrected ? p.crop_cor[side] : p.crop_raw[side],
+                      buf.size() * sizeof(uchar4), cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < buf.size(); ++i) {
+    rgb[3 * i + 0] = buf[i].x;
+    rgb[3 * i + 1] = buf[i].y;
+    rgb[3 * i + 2] = buf[i].z;
+    mask[i] = buf[i].w;
+  }
+  return STITCH_B200_OK;
+}
+
+int stitch_b200_debug_flow(stitch_b200_ctx* h, int k, int dir, float* u, float* v) {
+  Ctx* ctx = h->c.get();
+  if (k < 0 || k >= ctx->hg.n_pairs || dir < 0 || dir > 1)
+    return fail(STITCH_B200_ConfigurationError, "bad pair/dir");
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  const PairDesc& p = ctx->hg.pairs[k];
+  const size_t n = static_cast<size_t>(p.w) * p.h;
+  CUDA_TRY(cudaMemcpy(u, p.flow_u[dir], n * sizeof(float), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(v, p.flow_v[dir], n * sizeof(float), cudaMemcpyDeviceToHost));
+  return STITCH_B200_OK;
+}
+
+int stitch_b200_debug_prebalance(stitch_b200_ctx* h, uint8_t* rgb, uint8_t* mask) {
+  Ctx* ctx = h->c.get();
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  std::vector<uchar4> buf(static_cast<size_t>(ctx->n_px));
+  CUDA_TRY(cudaMemcpy(buf.data(), ctx->d_pano, buf.size() * sizeof(uchar4),
+                      cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < buf.size(); ++i) {
+    rgb[3 * i + 0] = buf[i].x;
+    rgb[3 * i + 1] = buf[i].y;
+    rgb[3 * i + 2] = buf[i].z;
+    mask[i] = buf[i].w;
+  }
+  return STITCH_B200_OK;
+}
+
+int stitch_b200_debug_warp_view(stitch_b200_ctx* h, int view, const uint8_t* host_frame,
+                                uint8_t* rgb, uint8_t* mask) {
+  Ctx* ctx = h->c.get();
+  if (view < 0 || view >= ctx->hg.n_views) return fail(STITCH_B200_ConfigurationError, "bad view");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  std::uint8_t *df = nullptr, *dr = nullptr, *dm = nullptr;
+  const size_t n = static_cast<size_t>(ctx->n_px);
+  CUDA_TRY(cudaMalloc(&df, ctx->frame_bytes[view]));
+  CUDA_TRY(cudaMalloc(&dr, n * 3));
+  CUDA_TRY(cudaMalloc(&dm, n));
+  CUDA_TRY(cudaMemcpy(df, host_frame, ctx->frame_bytes[view], cudaMemcpyHostToDevice));
+  launch_warp_view(ctx->dg, view, df, dr, dm, ctx->stream);
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  if (e == cudaSuccess) e = cudaMemcpy(rgb, dr, n * 3, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(mask, dm, n, cudaMemcpyDeviceToHost);
+  cudaFree(df);
+  cudaFree(dr);
+  cudaFree(dm);
+  if (e != cudaSuccess) return fail(STITCH_B200_CudaError, cudaGetErrorString(e));
+  return STITCH_B200_OK;
+}
+
+}  // extern "C"

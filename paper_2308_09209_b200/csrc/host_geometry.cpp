@@ -1,0 +1,259 @@
+// host_geometry.cpp -- init-time geometry (see host_geometry.hpp).
+// Compiled with -ffp-contract=off so the double arithmetic is unfused.
+#include "host_geometry.hpp"
+
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <cstdlib>
+#include <limits>
+
+namespace stitch_b200_host {
+
+void mul3(const Mat3& a, const Mat3& b, Mat3& out) {
+  Mat3 r;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      r[i * 3 + j] = (a[i * 3 + 0] * b[0 * 3 + j] + a[i * 3 + 1] * b[1 * 3 + j]) +
+                     a[i * 3 + 2] * b[2 * 3 + j];
+  out = r;
+}
+
+static inline double cof3(const Mat3& m, int i, int j) {
+  const int i1 = (i + 1) % 3, i2 = (i + 2) % 3;
+  const int j1 = (j + 1) % 3, j2 = (j + 2) % 3;
+  return m[i1 * 3 + j1] * m[i2 * 3 + j2] - m[i1 * 3 + j2] * m[i2 * 3 + j1];
+}
+
+double det3(const Mat3& m) {
+  const double c0 = cof3(m, 0, 0), c1 = cof3(m, 1, 0), c2 = cof3(m, 2, 0);
+  return (c0 * m[0] + c1 * m[3]) + c2 * m[6];
+}
+
+// Eigen compute_inverse<MatrixType, ResultType, 3>::run
+void inverse3(const Mat3& m, Mat3& out) {
+  const double c0 = cof3(m, 0, 0), c1 = cof3(m, 1, 0), c2 = cof3(m, 2, 0);
+  const double det = (c0 * m[0] + c1 * m[3]) + c2 * m[6];
+  const double invdet = 1.0 / det;
+  Mat3 r;
+  r[1 * 3 + 0] = cof3(m, 0, 1) * invdet;
+  r[1 * 3 + 1] = cof3(m, 1, 1) * invdet;
+  r[2 * 3 + 0] = cof3(m, 0, 2) * invdet;
+  r[1 * 3 + 2] = cof3(m, 2, 1) * invdet;
+  r[2 * 3 + 1] = cof3(m, 1, 2) * invdet;
+  r[2 * 3 + 2] = cof3(m, 2, 2) * invdet;
+  r[0] = c0 * invdet;
+  r[1] = c1 * invdet;
+  r[2] = c2 * invdet;
+  out = r;
+}
+
+int homography_from_matrix(const Mat3& m, Mat3& out) {
+  Mat3 h = m;
+  if (std::abs(h[8]) > 1e-12) {
+    const double s = h[8];
+    for (double& x : h) x /= s;
+  }
+  if (std::abs(det3(h)) <= 1e-12) return STITCH_B200_SingularHomography;
+  out = h;
+  return STITCH_B200_OK;
+}
+
+int homography_inverse(const Mat3& h, Mat3& out) {
+  Mat3 inv;
+  inverse3(h, inv);
+  return homography_from_matrix(inv, out);
+}
+
+void homography_apply(const Mat3& h, double x, double y, double& ox, double& oy) {
+  const double q0 = (h[0] * x + h[1] * y) + h[2] * 1.0;
+  const double q1 = (h[3] * x + h[4] * y) + h[5] * 1.0;
+  const double q2 = (h[6] * x + h[7] * y) + h[8] * 1.0;
+  ox = q0 / q2;
+  oy = q1 / q2;
+}
+
+// check_rotation (geometry.cpp:8-14)
+static int check_rotation(const double* r) {
+  Mat3 rm, rt, rrt;
+  for (int i = 0; i < 9; ++i) rm[i] = r[i];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) rt[i * 3 + j] = r[j * 3 + i];
+  mul3(rm, rt, rrt);
+  double s = 0.0;
+  for (int i = 0; i < 9; ++i) {
+    const double d = rrt[i] - ((i % 4 == 0) ? 1.0 : 0.0);
+    s += d * d;
+  }
+  if (std::sqrt(s) >= 1e-6 || det3(rm) < 0.0) return STITCH_B200_ConfigError;
+  return STITCH_B200_OK;
+}
+
+int planar_homography(const stitch_b200_camera& c, Mat3& out) {
+  int e = check_rotation(c.rotation);
+  if (e != STITCH_B200_OK) return e;
+  const Mat3 k = {c.fx, 0, c.cx, 0, c.fy, c.cy, 0, 0, 1};
+  Mat3 cols;
+  for (int i = 0; i < 3; ++i) {
+    cols[i * 3 + 0] = c.rotation[i * 3 + 0];
+    cols[i * 3 + 1] = c.rotation[i * 3 + 1];
+    cols[i * 3 + 2] = c.translation[i];
+  }
+  Mat3 h;
+  mul3(k, cols, h);
+  if (std::abs(det3(h)) <= 1e-12) return STITCH_B200_DegeneratePose;
+  return homography_from_matrix(h, out);
+}
+
+int pairwise_homography(const Mat3& hi, const Mat3& hj, Mat3& out) {
+  Mat3 inv, p;
+  inverse3(hj, inv);
+  mul3(hi, inv, p);
+  return homography_from_matrix(p, out);
+}
+
+Canvas compute_canvas(const std::vector<Mat3>& maps,
+                      const std::vector<std::pair<int, int>>& sizes) {
+  double min_x = std::numeric_limits<double>::max();
+  double min_y = std::numeric_limits<double>::max();
+  double max_x = std::numeric_limits<double>::lowest();
+  double max_y = std::numeric_limits<double>::lowest();
+  for (size_t v = 0; v < maps.size(); ++v) {
+    const double w = sizes[v].first - 1.0, h = sizes[v].second - 1.0;
+    const double cx[4] = {0.0, w, 0.0, w}, cy[4] = {0.0, 0.0, h, h};
+    for (int k = 0; k < 4; ++k) {
+      double X, Y;
+      homography_apply(maps[v], cx[k], cy[k], X, Y);
+      min_x = std::min(min_x, X);
+      min_y = std::min(min_y, Y);
+      max_x = std::max(max_x, X);
+      max_y = std::max(max_y, Y);
+    }
+  }
+  Canvas c;
+  c.offx = std::floor(min_x);
+  c.offy = std::floor(min_y);
+  c.width = static_cast<int>(std::ceil(max_x) - c.offx) + 1;
+  c.height = static_cast<int>(std::ceil(max_y) - c.offy) + 1;
+  return c;
+}
+
+std::vector<PairSpec> build_pairs(int n_views, int reference, int topology) {
+  const int topo = (topology == 1 || topology == 2) ? topology : (n_views <= 3 ? 1 : 2);
+  std::vector<PairSpec> pairs;
+  if (topo == 1) {
+    for (int v = 0; v < n_views; ++v)
+      if (v != reference) pairs.push_back({v, reference});
+    return pairs;
+  }
+  for (int d = 1; d < n_views; ++d)
+    for (int v = 0; v < n_views; ++v)
+      if (std::abs(v - reference) == d)
+        pairs.push_back({v, v < reference ? v + 1 : v - 1});
+  return pairs;
+}
+
+bool overlap_bounds(const std::uint8_t* mi, const std::uint8_t* mj, int w, int h,
+                    int b[4]) {
+  int x0 = w, y0 = h, x1 = 0, y1 = 0;
+  for (int y = 0; y < h; ++y)
+    for (int x = 0; x < w; ++x) {
+      const size_t i = static_cast<size_t>(y) * w + x;
+      if (mi[i] && mj[i]) {
+        x0 = std::min(x0, x);
+        y0 = std::min(y0, y);
+        x1 = std::max(x1, x + 1);
+        y1 = std::max(y1, y + 1);
+      }
+    }
+  if (x1 <= x0 || y1 <= y0) return false;
+  b[0] = x0;
+  b[1] = y0;
+  b[2] = x1;
+  b[3] = y1;
+  return true;
+}
+
+bool mask_bbox(const std::uint8_t* m, int w, int h, int b[4]) {
+  int x0 = w, y0 = h, x1 = 0, y1 = 0;
+  for (int y = 0; y < h; ++y)
+    for (int x = 0; x < w; ++x)
+      if (m[static_cast<size_t>(y) * w + x]) {
+        x0 = std::min(x0, x);
+        y0 = std::min(y0, y);
+        x1 = std::max(x1, x + 1);
+        y1 = std::max(y1, y + 1);
+      }
+  if (x1 <= x0 || y1 <= y0) return false;
+  b[0] = x0;
+  b[1] = y0;
+  b[2] = x1;
+  b[3] = y1;
+  return true;
+}
+
+static constexpr float kFarAway = 1e9f;  // flow.cpp:14
+
+// chamfer_distance (flow.cpp:192-223)
+static void chamfer(const std::vector<std::uint8_t>& zone, int w, int h,
+                    std::vector<float>& d) {
+  d.resize(static_cast<size_t>(w) * h);
+  for (size_t i = 0; i < d.size(); ++i) d[i] = zone[i] ? 0.0f : kFarAway;
+  auto at = [&](int y, int x) -> float& { return d[static_cast<size_t>(y) * w + x]; };
+  for (int y = 0; y < h; ++y)
+    for (int x = 0; x < w; ++x) {
+      float best = at(y, x);
+      if (x > 0) best = std::min(best, at(y, x - 1) + 3.0f);
+      if (y > 0) {
+        best = std::min(best, at(y - 1, x) + 3.0f);
+        if (x > 0) best = std::min(best, at(y - 1, x - 1) + 4.0f);
+        if (x + 1 < w) best = std::min(best, at(y - 1, x + 1) + 4.0f);
+      }
+      at(y, x) = best;
+    }
+  for (int y = h - 1; y >= 0; --y)
+    for (int x = w - 1; x >= 0; --x) {
+      float best = at(y, x);
+      if (x + 1 < w) best = std::min(best, at(y, x + 1) + 3.0f);
+      if (y + 1 < h) {
+        best = std::min(best, at(y + 1, x) + 3.0f);
+        if (x + 1 < w) best = std::min(best, at(y + 1, x + 1) + 4.0f);
+        if (x > 0) best = std::min(best, at(y + 1, x - 1) + 4.0f);
+      }
+      at(y, x) = best;
+    }
+}
+
+void blend_weights(const std::uint8_t* mi, const std::uint8_t* mj, int w, int h,
+                   const int b[4], float* theta_i) {
+  std::vector<std::uint8_t> ei(static_cast<size_t>(w) * h), ej(ei.size());
+  for (size_t i = 0; i < ei.size(); ++i) {
+    ei[i] = mi[i] && !mj[i];
+    ej[i] = mj[i] && !mi[i];
+  }
+  std::vector<float> to_j, to_i;
+  chamfer(ej, w, h, to_j);
+  chamfer(ei, w, h, to_i);
+  const int bw = b[2] - b[0], bh = b[3] - b[1];
+  for (int y = 0; y < bh; ++y)
+    for (int x = 0; x < bw; ++x) {
+      const size_t ci_ = static_cast<size_t>(b[1] + y) * w + b[0] + x;
+      const float cj = to_j[ci_], ci = to_i[ci_];
+      const float di = cj >= kFarAway ? kFarAway : std::max(0.0f, cj / 3.0f - 1.0f);
+      const float dj = ci >= kFarAway ? kFarAway : std::max(0.0f, ci / 3.0f - 1.0f);
+      float ti;
+      if (di >= kFarAway && dj >= kFarAway)
+        ti = 0.5f;
+      else if (di >= kFarAway)
+        ti = 1.0f;
+      else if (dj >= kFarAway)
+        ti = 0.0f;
+      else if (di + dj <= 0.0f)
+        ti = 0.5f;
+      else
+        ti = di / (di + dj);
+      theta_i[static_cast<size_t>(y) * bw + x] = ti;
+    }
+}
+
+}  // namespace stitch_b200_host

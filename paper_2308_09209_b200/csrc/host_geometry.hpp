@@ -1,0 +1,55 @@
+// host_geometry.hpp -- init-time geometry on the host (runs once per
+// context, not per frame).  Restates the reference's init path
+// (/root/reference/proj/src/geometry.cpp:8-171, pipeline.cpp:209-257,
+// flow.cpp:192-280) in plain C++; 3x3 products use a fixed left-to-right
+// summation order and the 3x3 inverse follows Eigen's cofactor formula
+// (Eigen/src/LU/InverseImpl.h), which pipeline.cpp:40 relies on.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <vector>
+
+#include "stitch_b200.h"
+
+namespace stitch_b200_host {
+
+using Mat3 = std::array<double, 9>;  // row-major
+
+void mul3(const Mat3& a, const Mat3& b, Mat3& out);
+double det3(const Mat3& m);
+void inverse3(const Mat3& m, Mat3& out);  // raw Eigen cofactor inverse
+// Homography::from_matrix (geometry.cpp:16-26); returns status.
+int homography_from_matrix(const Mat3& m, Mat3& out);
+// Homography::inverse (geometry.cpp:29-31): normalised inverse.
+int homography_inverse(const Mat3& h, Mat3& out);
+// Homography::apply (geometry.cpp:33-36)
+void homography_apply(const Mat3& h, double x, double y, double& ox, double& oy);
+// planar_homography (geometry.cpp:38-51)
+int planar_homography(const stitch_b200_camera& c, Mat3& out);
+// pairwise_homography (geometry.cpp:53-56)
+int pairwise_homography(const Mat3& hi, const Mat3& hj, Mat3& out);
+
+struct Canvas {
+  int width = 0, height = 0;
+  double offx = 0, offy = 0;
+};
+// compute_canvas (geometry.cpp:147-171)
+Canvas compute_canvas(const std::vector<Mat3>& maps, const std::vector<std::pair<int, int>>& sizes);
+
+struct PairSpec {
+  int view = 0, partner = 0;
+};
+// Star pairs (pipeline.cpp:233-239) or the N-view chain extension.
+std::vector<PairSpec> build_pairs(int n_views, int reference, int topology);
+
+// Overlap bbox of two canvas masks (geometry.cpp:85-117); false if empty.
+bool overlap_bounds(const std::uint8_t* mi, const std::uint8_t* mj, int w, int h,
+                    int bounds[4]);
+// bbox of one mask; false if empty.
+bool mask_bbox(const std::uint8_t* m, int w, int h, int bbox[4]);
+// blend_weights (flow.cpp:227-280), theta_i over bounds.
+void blend_weights(const std::uint8_t* mi, const std::uint8_t* mj, int w, int h,
+                   const int bounds[4], float* theta_i);
+
+}  // namespace stitch_b200_host

@@ -1,0 +1,161 @@
+// kernels.cuh -- descriptor tables shared by the host context and the
+// sm_100a kernels of the per-frame stitching path.
+//
+// HBM layout of one context (one panorama stream):
+//   frames[v]      RGB8 interleaved, W*H*3 bytes (inputs; reused every frame)
+//   crop_raw[k][s] uchar4 (r,g,b,valid) over pair k's bounds, s=0 view, 1 partner
+//   crop_cor[k][s] same after the per-view 3x3 colour matrix
+//   pyr[k][s][l]   float luma pyramid of crop_cor
+//   flow[k][d]     float u/v ping-pong planes (level-0 sized, reused per level)
+//   pano           uchar4 per canvas pixel (pre-balance), flat row-major
+//   out_rgb/mask   balanced panorama in the reference's Frame layout
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "stitch_b200.h"
+
+namespace stitch_b200_dev {
+
+constexpr int kMaxViews = STITCH_B200_MAX_VIEWS;
+constexpr int kMaxPairs = STITCH_B200_MAX_PAIRS;
+constexpr int kMaxLevels = 16;
+constexpr int kMaxTasks = 2 * kMaxPairs;
+
+struct ViewDesc {
+  int width, height;
+  int bbox[4];  // x0,y0,x1,y1 of the view's valid canvas footprint
+  double inv[9];
+};
+
+struct PairDesc {
+  int view, partner;
+  int x0, y0, w, h;  // bounds
+  int flow_ok;       // 0: crop below 16x16 -> zero flow (pipeline.cpp:317-320)
+  const float* theta_i;
+  uchar4* crop_raw[2];
+  uchar4* crop_cor[2];
+  float* pyr[2][kMaxLevels];
+  const float* flow_u[2];  // final level-0 flow, dir 0: view->partner
+  const float* flow_v[2];
+};
+
+// Per-pair integer moments of one frame (k_pair_stats -> k_pair_solve).
+struct PairStats {
+  unsigned int hs[3][256];   // source (view) histogram
+  unsigned int hr[3][256];   // reference (partner) histogram
+  unsigned long long s[6][256];  // S_{a|b}[v] = sum_{x_b = v} x_a, (a,b) a!=b
+  unsigned long long n;
+};
+
+// 3D-M window entry: exact integer moments of one frame
+// (TransferWindow::Entry, color_transfer.hpp:43-46, reduced to X^T X, X^T Y).
+struct WindowEntry {
+  unsigned long long xtx[9];
+  unsigned long long xty[9];
+  unsigned long long n;
+};
+
+struct PairWindow {
+  WindowEntry e[3];  // newest first
+  int size;
+  int capacity;
+};
+
+struct DevReport {
+  long long frame_index;
+  double m[kMaxPairs][9];
+  int rank_deficient[kMaxPairs];
+  int m1[3], m2[3];
+  int balanced;
+};
+
+struct BalanceState {
+  int n;  // history entries (<= 3), newest last
+  int m1[3][3], m2[3][3];
+};
+
+struct Geometry {
+  const std::uint8_t* frames[kMaxViews];  // device RGB8 inputs (per frame)
+  int canvas_w, canvas_h;
+  double offx, offy;
+  int n_views, reference, n_pairs;
+  int weighting;  // 0 own, 1 cross
+  ViewDesc views[kMaxViews];
+  PairDesc pairs[kMaxPairs];
+  int pair_depth[kMaxPairs];
+  // balance config
+  double lambda, gamma_dark, gamma_bright;
+  int target_black, target_white;
+  int curve_ok;
+};
+
+struct HsTask {
+  const float* a;  // luma of the first image at this level
+  const float* b;  // luma of the second image
+  const float* u_in;
+  const float* v_in;
+  float* u_out;
+  float* v_out;
+  int w, h;
+  int zero_in;       // coarsest level, first warp: flow starts at zero
+  int zero_invalid;  // final write: zero where either crop is invalid
+  const uchar4* mask_a;
+  const uchar4* mask_b;
+};
+
+struct UpTask {
+  const float* u_in;
+  const float* v_in;
+  int w_in, h_in;
+  float* u_out;
+  float* v_out;
+  int w, h;
+};
+
+struct PyrTask {
+  const float* src;
+  int sw, sh;
+  float* dst;
+  int w, h;
+};
+
+// mutable per-context device state
+struct DevState {
+  PairStats stats[kMaxPairs];
+  PairWindow windows[kMaxPairs];
+  double mview[kMaxViews][9];  // colour matrix applied to each view
+  unsigned int pano_hist[3][256];
+  BalanceState balance;
+  unsigned char lut[3][256];
+  DevReport report;
+  long long frame_counter;
+};
+
+// ---- launchers (kernels.cu) ----
+void launch_crop_warp(const Geometry* g, int n_pairs, int max_crop_px, cudaStream_t s);
+void launch_pair_stats(const Geometry* g, DevState* st, const int* pair_list, int n,
+                       int max_crop_px, cudaStream_t s);
+void launch_pair_solve(const Geometry* g, DevState* st, const int* pair_list, int n,
+                       cudaStream_t s);
+void launch_flow_prepare(const Geometry* g, DevState* st, int n_pairs, int max_crop_px,
+                         cudaStream_t s);
+void launch_pyr_down(const PyrTask* tasks, int n, int max_px, cudaStream_t s);
+void launch_upsample(const UpTask* tasks, int n, int max_px, cudaStream_t s);
+size_t hs_smem_bytes(int sweeps);
+cudaError_t prepare_hs(int sweeps);
+void launch_hs_iter(const HsTask* tasks, int n, int max_w, int max_h, int sweeps,
+                    float alpha2, cudaStream_t s);
+void launch_canvas(const Geometry* g, DevState* st, uchar4* pano, long long n_px,
+                   int num_sms, cudaStream_t s);
+void launch_balance(const Geometry* g, DevState* st, cudaStream_t s);
+void launch_tone(const DevState* st, const uchar4* pano, long long n_px,
+                 std::uint8_t* out_rgb, std::uint8_t* out_mask, cudaStream_t s);
+void launch_warp_view(const Geometry* g, int view, const std::uint8_t* frame,
+                      std::uint8_t* rgb, std::uint8_t* mask, cudaStream_t s);
+void launch_warp_mask(const Geometry* g, int view, std::uint8_t* mask, cudaStream_t s);
+
+}  // namespace stitch_b200_dev

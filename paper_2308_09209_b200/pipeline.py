@@ -1,0 +1,507 @@
+"""Python mirror of the reference's pipeline API over the B200 C ABI.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/stitch/pipeline.hpp:17-92 (StitchConfig,
+PipelineState, initialize, process_frame, run_sequence),
+report.hpp:11-58 (Stage, FrameReport, RunReport) and types.hpp:9-44
+(ErrorCode, StitchError).  Every frame goes through libstitch_b200.so; there
+is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import time
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional, Sequence
+
+import numpy as np
+
+from . import _abi
+
+
+class ErrorCode(enum.IntEnum):
+    """stitch::ErrorCode (types.hpp:9-27)."""
+    EmptyRegion = 0
+    EmptyHistogram = 1
+    RankDeficient = 2
+    RegionTooSmall = 3
+    InsufficientMatches = 4
+    NoConsensus = 5
+    ShapeMismatch = 6
+    NoOverlap = 7
+    SingularHomography = 8
+    DegeneratePose = 9
+    EmptyProjection = 10
+    MissingState = 11
+    TooSmall = 12
+    ConfigError = 13
+    ConfigurationError = 14
+    InputMismatch = 15
+    IoError = 16
+
+
+class StitchError(RuntimeError):
+    """stitch::StitchError (types.hpp:33-44); `code` is an ErrorCode, or None
+    for device/runtime failures (status >= 100)."""
+
+    def __init__(self, status: int, message: str):
+        super().__init__(message)
+        self.status = status
+        self.code = ErrorCode(status - 1) if 1 <= status <= 17 else None
+
+
+def _lib():
+    return _abi.load()
+
+
+def check(status: int) -> None:
+    if status != 0:
+        msg = _lib().stitch_b200_last_error().decode(errors="replace")
+        raise StitchError(status, msg or f"stitch_b200 status {status}")
+
+
+# ---------------------------------------------------------------------------
+# Frames and config (frame.hpp:17-57, geometry.hpp:11-30, pipeline.hpp:17-44)
+# ---------------------------------------------------------------------------
+@dataclass
+class Frame:
+    """RGB8 raster (H, W, 3) with an optional 0/1 mask (H, W); None = all valid."""
+    data: np.ndarray
+    mask: Optional[np.ndarray] = None
+
+    @property
+    def width(self) -> int:
+        return int(self.data.shape[1])
+
+    @property
+    def height(self) -> int:
+        return int(self.data.shape[0])
+
+    def has_mask(self) -> bool:
+        return self.mask is not None
+
+
+@dataclass
+class CameraIntrinsics:
+    fx: float = 1.0
+    fy: float = 1.0
+    cx: float = 0.0
+    cy: float = 0.0
+
+
+@dataclass
+class CameraExtrinsics:
+    rotation: np.ndarray = field(default_factory=lambda: np.eye(3))
+    translation: np.ndarray = field(default_factory=lambda: np.zeros(3))
+
+
+@dataclass
+class ViewSetup:
+    intrinsics: CameraIntrinsics = field(default_factory=CameraIntrinsics)
+    extrinsics: CameraExtrinsics = field(default_factory=CameraExtrinsics)
+    dir: str = ""
+
+
+@dataclass
+class BalanceConfig:  # color_balance.hpp:19-25
+    lambda_: float = 0.05
+    gamma_dark: float = 1.5
+    gamma_bright: float = 1.5
+    target_black: int = 0
+    target_white: int = 255
+
+
+@dataclass
+class FlowOptions:  # flow.hpp:29-34
+    levels: int = 4
+    iterations: int = 50
+    smoothness: float = 15.0
+    threads: int = 1
+
+
+@dataclass
+class RefineOptions:  # pipeline.hpp:23-31
+    # Feature refinement is init-only and outside the B200 path; the mirror
+    # defaults it off (the reference defaults it on).
+    enabled: bool = False
+    margin: float = 0.15
+    ransac_iters: int = 500
+    inlier_px: float = 2.0
+    detect_threshold: float = 2e-4
+    match_ratio: float = 0.8
+    rerefine_every: int = 0
+
+
+@dataclass
+class StitchConfig:  # pipeline.hpp:33-44
+    views: List[ViewSetup] = field(default_factory=list)
+    reference: int = 0
+    balance: BalanceConfig = field(default_factory=BalanceConfig)
+    flow: FlowOptions = field(default_factory=FlowOptions)
+    refine: RefineOptions = field(default_factory=RefineOptions)
+    threads: int = 1
+    seed: int = 0
+    window_capacity: int = 3
+    fuse_weighting: str = "own"  # "own" | "cross"
+    scene_id: str = "scene"
+    topology: str = "auto"  # extension: "auto" | "star" | "chain"
+    device: int = 0
+
+
+def _config_to_c(cfg: StitchConfig, sizes: Sequence[tuple]) -> _abi.Config:
+    c = _abi.Config()
+    _lib().stitch_b200_config_defaults(C.byref(c))
+    c.n_views = len(cfg.views)
+    c.reference = cfg.reference
+    for v, (setup, (w, h)) in enumerate(zip(cfg.views, sizes)):
+        c.width[v] = int(w)
+        c.height[v] = int(h)
+        cam = c.cams[v]
+        cam.fx, cam.fy = setup.intrinsics.fx, setup.intrinsics.fy
+        cam.cx, cam.cy = setup.intrinsics.cx, setup.intrinsics.cy
+        r = np.asarray(setup.extrinsics.rotation, dtype=np.float64).reshape(9)
+        t = np.asarray(setup.extrinsics.translation, dtype=np.float64).reshape(3)
+        for i in range(9):
+            cam.rotation[i] = float(r[i])
+        for i in range(3):
+            cam.translation[i] = float(t[i])
+    c.lambda_ = cfg.balance.lambda_
+    c.gamma_dark = cfg.balance.gamma_dark
+    c.gamma_bright = cfg.balance.gamma_bright
+    c.target_black = cfg.balance.target_black
+    c.target_white = cfg.balance.target_white
+    c.flow_levels = cfg.flow.levels
+    c.flow_iterations = cfg.flow.iterations
+    c.smoothness = cfg.flow.smoothness
+    c.window_capacity = cfg.window_capacity
+    c.fuse_weighting = 1 if cfg.fuse_weighting == "cross" else 0
+    c.topology = {"auto": 0, "star": 1, "chain": 2}[cfg.topology]
+    c.refine_enabled = 1 if cfg.refine.enabled else 0
+    return c
+
+
+def _config_from_c(c: _abi.Config) -> StitchConfig:
+    cfg = StitchConfig(reference=c.reference)
+    for v in range(c.n_views):
+        cam = c.cams[v]
+        cfg.views.append(ViewSetup(
+            CameraIntrinsics(cam.fx, cam.fy, cam.cx, cam.cy),
+            CameraExtrinsics(np.array(cam.rotation[:], dtype=np.float64).reshape(3, 3),
+                             np.array(cam.translation[:], dtype=np.float64))))
+    return cfg
+
+
+# ---------------------------------------------------------------------------
+# Report (report.hpp:11-58)
+# ---------------------------------------------------------------------------
+STAGE_NAMES = ("Geometric Warping", "Color Correction", "Local Warping", "Image Blending")
+
+
+@dataclass
+class FrameReport:
+    frame_index: int = 0
+    times: List[float] = field(default_factory=lambda: [0.0] * 4)  # seconds per Stage
+    color_matrices: List[np.ndarray] = field(default_factory=list)
+    rank_deficient: List[bool] = field(default_factory=list)
+    threshold_m1: List[int] = field(default_factory=lambda: [0, 0, 0])
+    threshold_m2: List[int] = field(default_factory=lambda: [0, 0, 0])
+    balanced: bool = False
+
+
+@dataclass
+class RunReport:
+    scene_id: str = ""
+    threads: int = 1
+    frames: int = 0
+    totals: List[float] = field(default_factory=lambda: [0.0] * 4)
+    wall_seconds: float = 0.0
+    per_frame: List[FrameReport] = field(default_factory=list)
+    refine_warning: bool = False
+
+    def fps(self) -> float:
+        return self.frames / self.wall_seconds if self.wall_seconds > 0 else 0.0
+
+
+def _report_from_c(r: _abi.Report) -> FrameReport:
+    out = FrameReport(frame_index=int(r.frame_index))
+    out.times = [r.stage_ms[i] * 1e-3 for i in range(4)]
+    for k in range(r.n_pairs):
+        out.color_matrices.append(np.array(r.color_matrices[k][:], dtype=np.float64).reshape(3, 3))
+        out.rank_deficient.append(bool(r.rank_deficient[k]))
+    out.threshold_m1 = list(r.threshold_m1)
+    out.threshold_m2 = list(r.threshold_m2)
+    out.balanced = bool(r.balanced)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Device context == PipelineState (pipeline.hpp:47-63)
+# ---------------------------------------------------------------------------
+@dataclass
+class PairState:
+    view: int
+    partner: int
+    bounds: tuple  # (x0, y0, x1, y1)
+    theta_i: np.ndarray
+
+
+class PipelineState:
+    """Owns one stitch_b200_ctx: the device-resident pipeline state of one
+    panorama stream (canvas, maps, pairs, 3D-M windows, threshold history)."""
+
+    def __init__(self, handle: C.c_void_p, config: Optional[StitchConfig] = None):
+        self._h = handle
+        self.config = config
+        lib = _lib()
+        w, h = C.c_int(), C.c_int()
+        ox, oy = C.c_double(), C.c_double()
+        check(lib.stitch_b200_canvas(self._h, C.byref(w), C.byref(h), C.byref(ox), C.byref(oy)))
+        self.canvas = (w.value, h.value, ox.value, oy.value)
+        self.pairs: List[PairState] = []
+        for k in range(lib.stitch_b200_n_pairs(self._h)):
+            p = _abi.Pair()
+            check(lib.stitch_b200_get_pair(self._h, k, C.byref(p), None))
+            th = np.empty((p.y1 - p.y0, p.x1 - p.x0), dtype=np.float32)
+            check(lib.stitch_b200_get_pair(self._h, k, C.byref(p), th.ctypes.data_as(C.c_void_p)))
+            self.pairs.append(PairState(p.view, p.partner, (p.x0, p.y0, p.x1, p.y1), th))
+        self.n_views = len(config.views) if config else None
+        self.frame_counter = 0
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    @property
+    def canvas_width(self) -> int:
+        return self.canvas[0]
+
+    @property
+    def canvas_height(self) -> int:
+        return self.canvas[1]
+
+    def view_bbox(self, view: int) -> tuple:
+        b = (C.c_int * 4)()
+        check(_lib().stitch_b200_view_bbox(self._h, view, b))
+        return tuple(b)
+
+    def inv_map(self, view: int) -> np.ndarray:
+        m = (C.c_double * 9)()
+        check(_lib().stitch_b200_get_inv_map(self._h, view, m))
+        return np.array(m[:], dtype=np.float64).reshape(3, 3)
+
+    def launches_per_frame(self) -> int:
+        return _lib().stitch_b200_launches_per_frame(self._h)
+
+    def close(self) -> None:
+        if self._h:
+            _lib().stitch_b200_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class ProcessResult:  # pipeline.hpp:65-68
+    panorama: Frame
+    report: FrameReport
+
+
+def initialize(config: StitchConfig, first_frames: Sequence[Frame]) -> PipelineState:
+    """pipeline.hpp:73-74 (refinement must be off; see RefineOptions)."""
+    if len(first_frames) != len(config.views):
+        raise StitchError(ErrorCode.ConfigurationError + 1,
+                          "frame count does not match configured views")
+    sizes = [(f.width, f.height) for f in first_frames]
+    c = _config_to_c(config, sizes)
+    h = C.c_void_p()
+    check(_lib().stitch_b200_initialize(C.byref(c), config.device, C.byref(h)))
+    return PipelineState(h, config)
+
+
+def create_from_init(init: _abi.Init, device: int = 0,
+                     config: Optional[StitchConfig] = None) -> PipelineState:
+    """Drop-in path: a state snapshot produced elsewhere (e.g. the reference's
+    own initialize() with feature refinement) -> device context."""
+    h = C.c_void_p()
+    check(_lib().stitch_b200_create(C.byref(init), device, C.byref(h)))
+    return PipelineState(h, config)
+
+
+def _frame_ptrs(frames: Sequence[Frame], n: int):
+    if len(frames) != n:
+        raise StitchError(ErrorCode.ConfigurationError + 1,
+                          "frame count does not match configured views")
+    arrs = [np.ascontiguousarray(f.data, dtype=np.uint8) for f in frames]
+    ptrs = (C.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+    return arrs, ptrs
+
+
+def process_frame(state: PipelineState, frames: Sequence[Frame]) -> ProcessResult:
+    """pipeline.hpp:79-80: one frame through warp -> 3D-M colour -> flow ->
+    blend -> balance, on the GPU."""
+    n = len(state.config.views) if state.config else len(frames)
+    arrs, ptrs = _frame_ptrs(frames, n)
+    for f, a in zip(frames, arrs):
+        if a.ndim != 3 or a.shape[2] != 3:
+            raise StitchError(ErrorCode.InputMismatch + 1, "frames must be (H, W, 3) uint8")
+    w, h = state.canvas_width, state.canvas_height
+    rgb = np.empty((h, w, 3), dtype=np.uint8)
+    mask = np.empty((h, w), dtype=np.uint8)
+    rep = _abi.Report()
+    check(_lib().stitch_b200_process(state.handle, ptrs, rgb.ctypes.data_as(C.c_void_p),
+                                     mask.ctypes.data_as(C.c_void_p), C.byref(rep)))
+    state.frame_counter += 1
+    return ProcessResult(Frame(rgb, mask), _report_from_c(rep))
+
+
+@dataclass
+class RunResult:
+    panoramas: List[Frame]
+    report: RunReport
+
+
+def run_sequence(config: StitchConfig, views: Sequence[Sequence[Frame]],
+                 sink: Optional[Callable[[int, Frame], None]] = None) -> RunResult:
+    """pipeline.hpp:90-92 / pipeline.cpp:362-420 (re-refinement unsupported)."""
+    if len(views) != len(config.views):
+        raise StitchError(ErrorCode.ConfigurationError + 1,
+                          "stream count does not match configured views")
+    frames = len(views[0])
+    if any(len(s) != frames for s in views):
+        raise StitchError(ErrorCode.ConfigurationError + 1, "streams must have equal length")
+    if frames == 0:
+        raise StitchError(ErrorCode.ConfigurationError + 1, "empty input streams")
+    t0 = time.perf_counter()
+    state = initialize(config, [s[0] for s in views])
+    result = RunResult([], RunReport(scene_id=config.scene_id, threads=config.threads,
+                                     frames=frames))
+    try:
+        for t in range(frames):
+            pr = process_frame(state, [s[t] for s in views])
+            for i in range(4):
+                result.report.totals[i] += pr.report.times[i]
+            result.report.per_frame.append(pr.report)
+            if sink:
+                sink(t, pr.panorama)
+            else:
+                result.panoramas.append(pr.panorama)
+    finally:
+        state.close()
+    result.report.wall_seconds = time.perf_counter() - t0
+    return result
+
+
+# ---------------------------------------------------------------------------
+# Synthetic scenes (synth.hpp:17-87)
+# ---------------------------------------------------------------------------
+@dataclass
+class FlickerEvent:
+    frame: int = 0
+    view: int = 0
+    gains: tuple = (1.0, 1.0, 1.0)
+
+
+@dataclass
+class ParallaxObject:
+    enabled: bool = False
+    depth_fraction: float = 0.15
+    half_size: float = 40.0
+    position: tuple = (0.0, 0.0)
+    velocity: tuple = (0.0, 0.0)
+
+
+@dataclass
+class SynthSpec:
+    seed: int = 1
+    views: int = 2
+    frames: int = 5
+    width: int = 320
+    height: int = 240
+    overlap_fraction: float = 0.3
+    color_casts: List[tuple] = field(default_factory=list)
+    flicker: List[FlickerEvent] = field(default_factory=list)
+    object: ParallaxObject = field(default_factory=ParallaxObject)
+    perturb_focal_scale: float = 1.0
+    perturb_principal_px: float = 0.0
+    rig: str = "auto"  # "auto" | "yaw" (reference) | "strip" (N-view extension)
+    strip_yaw: float = 0.05
+
+    def to_c(self) -> _abi.SynthSpec:
+        s = _abi.SynthSpec()
+        _lib().stitch_b200_synth_defaults(C.byref(s))
+        s.seed = self.seed
+        s.views = self.views
+        s.frames = self.frames
+        s.width = self.width
+        s.height = self.height
+        s.overlap_fraction = self.overlap_fraction
+        s.n_casts = len(self.color_casts)
+        for v, g in enumerate(self.color_casts):
+            for c in range(3):
+                s.color_casts[v][c] = float(g[c])
+        s.n_flicker = len(self.flicker)
+        for i, f in enumerate(self.flicker):
+            s.flicker[i].frame = f.frame
+            s.flicker[i].view = f.view
+            for c in range(3):
+                s.flicker[i].gains[c] = float(f.gains[c])
+        s.object_enabled = 1 if self.object.enabled else 0
+        s.object_depth_fraction = self.object.depth_fraction
+        s.object_half_size = self.object.half_size
+        s.object_position[0], s.object_position[1] = self.object.position
+        s.object_velocity[0], s.object_velocity[1] = self.object.velocity
+        s.perturb_focal_scale = self.perturb_focal_scale
+        s.perturb_principal_px = self.perturb_principal_px
+        s.rig = {"auto": 0, "yaw": 1, "strip": 2}[self.rig]
+        s.strip_yaw = self.strip_yaw
+        return s
+
+
+class SynthScene:
+    """synth.hpp:49-87: procedural plane scene + cameras + renderer."""
+
+    def __init__(self, spec: SynthSpec):
+        self.spec = spec
+        self._c = spec.to_c()
+        self._h = C.c_void_p()
+        check(_lib().stitch_b200_synth_create(C.byref(self._c), C.byref(self._h)))
+
+    def reference_view(self) -> int:
+        return _lib().stitch_b200_synth_reference(self._h)
+
+    def config_c(self) -> _abi.Config:
+        c = _abi.Config()
+        check(_lib().stitch_b200_synth_config(self._h, C.byref(c)))
+        return c
+
+    def config(self) -> StitchConfig:
+        cfg = _config_from_c(self.config_c())
+        cfg.seed = self.spec.seed
+        cfg.scene_id = f"synth-{self.spec.seed}"
+        return cfg
+
+    def render_view(self, view: int, frame: int, threads: int = 0) -> Frame:
+        out = np.empty((self.spec.height, self.spec.width, 3), dtype=np.uint8)
+        check(_lib().stitch_b200_synth_render(self._h, view, frame,
+                                              out.ctypes.data_as(C.c_void_p), threads))
+        return Frame(out, None)
+
+    def render_streams(self, frames: Optional[int] = None, threads: int = 0) -> List[List[Frame]]:
+        n = self.spec.frames if frames is None else frames
+        return [[self.render_view(v, t, threads) for t in range(n)] for v in range(self.spec.views)]
+
+    def close(self):
+        if self._h:
+            _lib().stitch_b200_synth_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,90 @@
+"""CPU checks of the drop-in boundary: the C-ABI library loads, exports every
+function include/stitch_b200.h declares, and the ctypes structs match the
+header layout.  No compute calls (no GPU here)."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_2308_09209_b200 import _abi
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "stitch_b200.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(stitch_b200_\w+)\s*\(", src)))
+
+
+def test_library_loads_and_exports_every_declared_symbol():
+    lib = _abi.load()
+    names = declared_functions()
+    assert len(names) >= 30
+    for n in names:
+        assert hasattr(lib, n), n
+    # and the ctypes table covers the header
+    assert sorted(n for n, _, _ in _abi.SYMBOLS) == names
+
+
+def test_exported_dynamic_symbols():
+    out = subprocess.run(["nm", "-D", "--defined-only", _abi.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r" T (stitch_b200_\w+)", out))
+    assert set(declared_functions()) <= exported
+
+
+def test_struct_layouts_match_header():
+    # compile a tiny C program against the header and compare sizeof/offsetof
+    prog = r"""
+#include <stdio.h>
+#include <stddef.h>
+#include "stitch_b200.h"
+int main(void){
+ printf("%zu %zu %zu %zu %zu %zu %zu\n", sizeof(stitch_b200_camera), sizeof(stitch_b200_config),
+   sizeof(stitch_b200_pair), sizeof(stitch_b200_init), sizeof(stitch_b200_report),
+   sizeof(stitch_b200_synth_spec), offsetof(stitch_b200_init, pairs));
+ return 0; }
+"""
+    tmp = "/tmp/stitch_b200_layout"
+    with open(tmp + ".c", "w") as f:
+        f.write(prog)
+    subprocess.run(["/usr/bin/gcc", "-I", os.path.join(ROOT, "include"), tmp + ".c", "-o", tmp],
+                   check=True)
+    got = [int(x) for x in subprocess.run([tmp], capture_output=True, text=True,
+                                          check=True).stdout.split()]
+    want = [C.sizeof(_abi.Camera), C.sizeof(_abi.Config), C.sizeof(_abi.Pair),
+            C.sizeof(_abi.Init), C.sizeof(_abi.Report), C.sizeof(_abi.SynthSpec),
+            _abi.Init.pairs.offset]
+    assert got == want
+
+
+def test_config_defaults_match_reference():
+    lib = _abi.load()
+    c = _abi.Config()
+    lib.stitch_b200_config_defaults(C.byref(c))
+    # BalanceConfig (color_balance.hpp:19-25), FlowOptions (flow.hpp:29-34),
+    # window 3 / fuse "own" (pipeline.hpp:39-42)
+    assert (c.lambda_, c.gamma_dark, c.gamma_bright) == (0.05, 1.5, 1.5)
+    assert (c.target_black, c.target_white) == (0, 255)
+    assert (c.flow_levels, c.flow_iterations, c.smoothness) == (4, 50, 15.0)
+    assert (c.window_capacity, c.fuse_weighting, c.refine_enabled) == (3, 0, 0)
+
+
+def test_last_error_is_a_string():
+    lib = _abi.load()
+    assert isinstance(lib.stitch_b200_last_error(), bytes)
+    assert b"sm_100a" in lib.stitch_b200_version()
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    _abi._lib_saved = _abi._lib
+    try:
+        _abi._lib = None
+        with pytest.raises(ImportError):
+            _abi.load(str(tmp_path / "nope.so"))
+    finally:
+        _abi._lib = _abi._lib_saved

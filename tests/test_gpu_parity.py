@@ -1,0 +1,275 @@
+"""GPU parity: the B200 path (through the C ABI) against the CPU oracle on
+identical synthetic inputs.
+
+Contract (BASELINE.json north_star): warp/flow fields within 1e-3 px, colour
+matrices within 1e-4 relative, final 8-bit panoramas within +-1 LSB with an
+identical mask.  The implementation is designed to be bit-exact (FP64 warp,
+integer-exact colour moments, FP32 flow with --fmad=false), so these tests
+assert the tolerance AND report the max-abs-diff; the bit-exact expectation
+is asserted separately where the arithmetic is integer/byte work.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2308_09209_b200 as pb
+from paper_2308_09209_b200 import _abi
+from tests.helpers import frames_at, maxdiff, oracle_config, product_config, scene
+
+pytestmark = pytest.mark.gpu
+
+M_RTOL = 1e-4
+FLOW_TOL = 1e-3
+
+
+def _lib():
+    return _abi.load()
+
+
+def make_pair(sc, frames0=None, **kw):
+    cfg = product_config(sc, **kw)
+    first = frames0 or frames_at(sc, 0)
+    state = pb.initialize(cfg, first)
+    ost = O.OracleState(oracle_config(sc, **kw))
+    return state, ost
+
+
+def debug_flow(state, k, d, shape):
+    u = np.zeros(shape, np.float32)
+    v = np.zeros(shape, np.float32)
+    pb.pipeline.check(_lib().stitch_b200_debug_flow(state.handle, k, d,
+                                                    u.ctypes.data_as(C.c_void_p),
+                                                    v.ctypes.data_as(C.c_void_p)))
+    return u, v
+
+
+def debug_warp(state, view, frame):
+    w, h = state.canvas_width, state.canvas_height
+    rgb = np.zeros((h, w, 3), np.uint8)
+    mask = np.zeros((h, w), np.uint8)
+    src = np.ascontiguousarray(frame.data)
+    pb.pipeline.check(_lib().stitch_b200_debug_warp_view(state.handle, view,
+                                                         src.ctypes.data_as(C.c_void_p),
+                                                         rgb.ctypes.data_as(C.c_void_p),
+                                                         mask.ctypes.data_as(C.c_void_p)))
+    return rgb, mask
+
+
+def check_geometry(state, ost, n_views):
+    assert state.canvas == ost.canvas
+    assert len(state.pairs) == ost.n_pairs()
+    for v in range(n_views):
+        _, inv = ost.maps(v)
+        np.testing.assert_array_equal(state.inv_map(v), inv)
+        assert state.view_bbox(v) == ost.view_bbox(v)
+    for k, p in enumerate(state.pairs):
+        view, partner, bounds = ost.pair(k)
+        assert (p.view, p.partner, p.bounds) == (view, partner, bounds)
+        np.testing.assert_array_equal(p.theta_i, ost.pair_weights(k))
+
+
+def check_frame(state, ost, frames, t, *, exact=True):
+    res = pb.process_frame(state, frames)
+    odata, omask, orep = ost.process([f.data for f in frames])
+    rep = res.report
+    # colour matrices (1e-4 relative; bit-exact expected)
+    for k in range(len(state.pairs)):
+        m_ref = np.array(orep.m[k][:]).reshape(3, 3)
+        m = rep.color_matrices[k]
+        np.testing.assert_allclose(m, m_ref, rtol=M_RTOL, atol=1e-12)
+        if exact:
+            np.testing.assert_array_equal(m, m_ref)
+        assert rep.rank_deficient[k] == bool(orep.rank_deficient[k])
+    # flows (1e-3 px; bit-exact expected)
+    for k, p in enumerate(state.pairs):
+        shape = (p.bounds[3] - p.bounds[1], p.bounds[2] - p.bounds[0])
+        for d in range(2):
+            u, v = debug_flow(state, k, d, shape)
+            ou, ov = ost.last_flow(k, d)
+            assert np.abs(u - ou).max() <= FLOW_TOL, (t, k, d, np.abs(u - ou).max())
+            assert np.abs(v - ov).max() <= FLOW_TOL
+            if exact:
+                np.testing.assert_array_equal(u, ou)
+                np.testing.assert_array_equal(v, ov)
+    # balancing thresholds
+    assert rep.balanced == bool(orep.balanced)
+    assert rep.threshold_m1 == list(orep.threshold_m1)
+    assert rep.threshold_m2 == list(orep.threshold_m2)
+    assert rep.frame_index == orep.frame_index
+    # panorama: identical mask, +-1 LSB (bit-exact expected)
+    np.testing.assert_array_equal(res.panorama.mask, omask)
+    d = maxdiff(res.panorama.data, odata)
+    assert d <= 1, f"frame {t}: max abs diff {d}"
+    if exact:
+        assert d == 0, f"frame {t}: max abs diff {d}"
+    return res
+
+
+@pytest.mark.parametrize("views", [2, 3])
+def test_init_geometry_matches_oracle(views):
+    sc = scene(views=views, width=200, height=150)
+    state, ost = make_pair(sc)
+    check_geometry(state, ost, views)
+
+
+def test_warp_views_bit_exact():
+    sc = scene(views=3, width=160, height=120)
+    state, ost = make_pair(sc)
+    frames = frames_at(sc, 0)
+    ost.process([f.data for f in frames])
+    for v in range(3):
+        rgb, mask = debug_warp(state, v, frames[v])
+        orgb, omask = ost.last_warped(v)
+        np.testing.assert_array_equal(mask, omask)
+        np.testing.assert_array_equal(rgb, orgb)
+
+
+def test_c1_config_parity_all_stages():
+    """BASELINE config 1: 2 x 640x480, one overlap, fixed homography; casts,
+    a flicker event and a moving parallax object; several frames so the
+    3-frame windows fill and roll."""
+    sc = scene(views=2, width=640, height=480, frames=6, casts=[(1, 1, 1), (0.85, 1.0, 1.1)],
+               flicker=[pb.FlickerEvent(frame=3, view=1, gains=(1.2, 1.1, 0.9))])
+    state, ost = make_pair(sc)
+    check_geometry(state, ost, 2)
+    for t in range(6):
+        check_frame(state, ost, frames_at(sc, t), t)
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(window=1), dict(weighting=1), dict(window=2),
+                                dict(levels=2, iterations=20)])
+def test_three_view_parity(kw):
+    sc = scene(views=3, width=200, height=150, frames=4, casts=[(0.9, 1, 1), (1, 1, 1),
+                                                                (1, 0.95, 1.1)])
+    state, ost = make_pair(sc, **kw)
+    check_geometry(state, ost, 3)
+    for t in range(4):
+        check_frame(state, ost, frames_at(sc, t), t)
+
+
+def test_four_view_chain_parity():
+    """N-view extension (chain topology, strip rig): parity vs the extended
+    oracle (unpinned by the reference, which caps views at 3)."""
+    sc = scene(views=4, width=200, height=150, frames=3, focal_scale=1.03,
+               casts=[(0.9, 1, 1), (1, 1, 1), (1, 0.95, 1.1), (1.1, 1, 0.9)])
+    state, ost = make_pair(sc)
+    check_geometry(state, ost, 4)
+    for t in range(3):
+        check_frame(state, ost, frames_at(sc, t), t)
+
+
+def test_tiny_overlap_degrades_to_zero_flow():
+    # overlap narrower than 16 px -> dense_flow throws TooSmall -> zero flow
+    sc = scene(views=2, width=160, height=120, overlap=0.07)
+    state, ost = make_pair(sc)
+    p = state.pairs[0]
+    assert p.bounds[2] - p.bounds[0] < 16 or p.bounds[3] - p.bounds[1] < 16
+    for t in range(2):
+        check_frame(state, ost, frames_at(sc, t), t)
+
+
+def test_flat_overlap_rank_deficient_identity():
+    # a constant scene makes X^T X rank one -> RankDeficient -> identity M
+    sc = scene(views=2, width=120, height=90, obj=False)
+    frames = [pb.Frame(np.full_like(f.data, 77)) for f in frames_at(sc, 0)]
+    state, ost = make_pair(sc, frames0=frames)
+    res = check_frame(state, ost, frames, 0)
+    assert res.report.rank_deficient == [True]
+    np.testing.assert_array_equal(res.report.color_matrices[0], np.eye(3))
+
+
+def test_run_sequence_and_determinism():
+    sc = scene(views=2, width=160, height=120, frames=3)
+    cfg = product_config(sc)
+    streams = sc.render_streams()
+    a = pb.run_sequence(cfg, streams)
+    b = pb.run_sequence(cfg, streams)
+    assert a.report.frames == 3 and len(a.panoramas) == 3
+    for x, y in zip(a.panoramas, b.panoramas):
+        np.testing.assert_array_equal(x.data, y.data)
+        np.testing.assert_array_equal(x.mask, y.mask)
+    assert all(t >= 0 for t in a.report.totals)
+
+
+def test_errors_fail_loudly():
+    sc = scene(views=2, width=120, height=90)
+    cfg = product_config(sc)
+    cfg.refine.enabled = True
+    with pytest.raises(pb.StitchError):
+        pb.initialize(cfg, frames_at(sc, 0))
+    cfg = product_config(sc, lam=0.7)
+    with pytest.raises(pb.StitchError) as e:
+        pb.initialize(cfg, frames_at(sc, 0))
+    assert e.value.code == pb.ErrorCode.ConfigError
+    cfg = product_config(sc)
+    state = pb.initialize(cfg, frames_at(sc, 0))
+    with pytest.raises(pb.StitchError):
+        pb.process_frame(state, frames_at(sc, 0)[:1])
+
+
+def test_update_geometry_keeps_temporal_state():
+    """Re-refinement (pipeline.cpp:395-406) keeps windows, history, counter."""
+    sc = scene(views=2, width=160, height=120, frames=4, casts=[(1, 1, 1), (0.8, 1, 1.1)])
+    state, ost = make_pair(sc)
+    for t in range(2):
+        check_frame(state, ost, frames_at(sc, t), t)
+    # re-upload the same geometry through the drop-in snapshot path
+    init = _abi.Init()
+    w, h, ox, oy = state.canvas
+    init.canvas_width, init.canvas_height = w, h
+    init.canvas_offset[0], init.canvas_offset[1] = ox, oy
+    init.n_views, init.reference = 2, sc.reference_view()
+    keep = []
+    for v in range(2):
+        init.view_width[v], init.view_height[v] = 160, 120
+        inv = state.inv_map(v).reshape(9)
+        for i in range(9):
+            init.inv_maps[v][i] = inv[i]
+    init.n_pairs = len(state.pairs)
+    for k, p in enumerate(state.pairs):
+        th = np.ascontiguousarray(p.theta_i, np.float32)
+        keep.append(th)
+        init.pairs[k].view, init.pairs[k].partner = p.view, p.partner
+        init.pairs[k].x0, init.pairs[k].y0, init.pairs[k].x1, init.pairs[k].y1 = p.bounds
+        init.pairs[k].theta_i = th.ctypes.data_as(C.POINTER(C.c_float))
+    init.window_capacity = 3
+    init.lambda_, init.gamma_dark, init.gamma_bright = 0.05, 1.5, 1.5
+    init.target_black, init.target_white = 0, 255
+    init.flow_levels, init.flow_iterations, init.smoothness = 4, 50, 15.0
+    init.fuse_weighting = 0
+    pb.pipeline.check(_lib().stitch_b200_update_geometry(state.handle, C.byref(init)))
+    for t in range(2, 4):
+        check_frame(state, ost, frames_at(sc, t), t)
+
+
+def test_create_from_snapshot_matches_initialize():
+    sc = scene(views=2, width=160, height=120, frames=2)
+    state, ost = make_pair(sc)
+    init = _abi.Init()
+    w, h, ox, oy = state.canvas
+    init.canvas_width, init.canvas_height = w, h
+    init.canvas_offset[0], init.canvas_offset[1] = ox, oy
+    init.n_views, init.reference = 2, sc.reference_view()
+    for v in range(2):
+        init.view_width[v], init.view_height[v] = 160, 120
+        inv = state.inv_map(v).reshape(9)
+        for i in range(9):
+            init.inv_maps[v][i] = inv[i]
+    init.n_pairs = 1
+    p = state.pairs[0]
+    th = np.ascontiguousarray(p.theta_i, np.float32)
+    init.pairs[0].view, init.pairs[0].partner = p.view, p.partner
+    init.pairs[0].x0, init.pairs[0].y0, init.pairs[0].x1, init.pairs[0].y1 = p.bounds
+    init.pairs[0].theta_i = th.ctypes.data_as(C.POINTER(C.c_float))
+    init.window_capacity = 3
+    init.lambda_, init.gamma_dark, init.gamma_bright = 0.05, 1.5, 1.5
+    init.target_black, init.target_white = 0, 255
+    init.flow_levels, init.flow_iterations, init.smoothness = 4, 50, 15.0
+    snap = pb.create_from_init(init, 0, product_config(sc))
+    for t in range(2):
+        fr = frames_at(sc, t)
+        a = pb.process_frame(state, fr)
+        b = pb.process_frame(snap, fr)
+        np.testing.assert_array_equal(a.panorama.data, b.panorama.data)
