@@ -161,8 +161,8 @@ def test_four_view_chain_parity():
 
 
 def test_tiny_overlap_degrades_to_zero_flow():
-    # overlap narrower than 16 px -> dense_flow throws TooSmall -> zero flow
-    sc = scene(views=2, width=160, height=120, overlap=0.07)
+    # overlap shorter than 16 rows -> dense_flow throws TooSmall -> zero flow
+    sc = scene(views=2, width=160, height=14, obj=False)
     state, ost = make_pair(sc)
     p = state.pairs[0]
     assert p.bounds[2] - p.bounds[0] < 16 or p.bounds[3] - p.bounds[1] < 16
