@@ -1,0 +1,426 @@
+// canvas_kernels.cu -- geometric warping (overlap crops), the canvas pass
+// (warp + colour matrix + flow fusion + composition + histogram + global
+// balance LUT) and the tone/output pass.
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+
+#include "device_math.cuh"
+#include "kernels.cuh"
+
+namespace stitch_b200_dev {
+
+// ---------------------------------------------------------------------------
+// Geometric warping of the overlap crops: crop_frame(warp_frame(...), bounds)
+// (pipeline.cpp:310-311) evaluated directly on the bounds.
+// grid: (x blocks, 2*n_pairs)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_crop_warp(const Geometry* __restrict__ g) {
+  const int k = blockIdx.y >> 1;
+  const int side = blockIdx.y & 1;
+  const PairDesc& p = g->pairs[k];
+  const int n = p.w * p.h;
+  const int view = side ? p.partner : p.view;
+  const ViewDesc& v = g->views[view];
+  const std::uint8_t* frame = g->frames[view];
+  uchar4* out = p.crop_raw[side];
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += gridDim.x * blockDim.x) {
+    const int dy = idx / p.w;
+    const int dx = idx - dy * p.w;
+    const double X = static_cast<double>(p.x0 + dx) + g->offx;
+    const double Y = static_cast<double>(p.y0 + dy) + g->offy;
+    out[idx] = warp_sample(v, frame, X, Y);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Canvas pass: for every canvas pixel, the warped reference view, then the
+// compose_panorama fold over pairs (pipeline.cpp:326-333, flow.cpp:324-357)
+// with the colour-corrected warped view (apply_matrix_rows, pipeline.cpp:296)
+// and, inside each overlap, the flow-displaced fusion of flow_fuse
+// (flow.cpp:282-322) evaluated on demand.  Inside a pair's bounds the raw
+// warped samples already computed for the overlap crops are reused
+// (bit-identical: same sampler).  Also the balance histogram of the composed
+// panorama (compute_histogram, histogram.cpp:5-18); the last CTA turns it
+// into the tone LUT (global balancing, pipeline.cpp:336-355).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool fused_pixel(const Geometry* __restrict__ g, const PairDesc& p,
+                                            int dx, int dy, uchar4& out) {
+  const int i = dy * p.w + dx;
+  const float ti = p.theta_i[i];
+  const float tj = 1.0f - ti;  // BlendWeights::theta_j (flow.cpp:276)
+  const float wi = g->weighting == 0 ? ti : tj;
+  const float wj = g->weighting == 0 ? tj : ti;
+  float ri, gi, bi, rj, gj, bj;
+  const bool vi = sample_crop(p.crop_cor[0], p.w, p.h,
+                              static_cast<double>(static_cast<float>(dx) + wi * p.flow_u[0][i]),
+                              static_cast<double>(static_cast<float>(dy) + wi * p.flow_v[0][i]),
+                              ri, gi, bi);
+  const bool vj = sample_crop(p.crop_cor[1], p.w, p.h,
+                              static_cast<double>(static_cast<float>(dx) + wj * p.flow_u[1][i]),
+                              static_cast<double>(static_cast<float>(dy) + wj * p.flow_v[1][i]),
+                              rj, gj, bj);
+  if (!vi && !vj) return false;
+  float r, gg, b;
+  if (vi && vj) {
+    r = ti * ri + tj * rj;
+    gg = ti * gi + tj * gj;
+    b = ti * bi + tj * bj;
+  } else if (vi) {
+    r = ri;
+    gg = gi;
+    b = bi;
+  } else {
+    r = rj;
+    gg = gj;
+    b = bj;
+  }
+  out = make_uchar4(quantize_f(r), quantize_f(gg), quantize_f(b), 1);
+  return true;
+}
+
+// Global balancing on the last CTA: find_thresholds (color_balance.cpp:8-38),
+// history push (pipeline.cpp:340-345), smooth_thresholds
+// (color_balance.cpp:40-63), build_curve (color_balance.cpp:65-104).
+__device__ void balance_lut(const Geometry* __restrict__ g, DevState* __restrict__ st) {
+  __shared__ int sm1[3], sm2[3], first1[3], first2[3];
+  __shared__ unsigned long long wtot[8];
+  __shared__ int ok;
+  const int v = threadIdx.x;
+  unsigned int hist[3];
+  for (int c = 0; c < 3; ++c) {
+    hist[c] = st->pano_hist[c][v];
+    st->pano_hist[c][v] = 0;
+  }
+  if (v < 3) {
+    first1[v] = 256;
+    first2[v] = 256;
+  }
+  // inclusive prefix per channel (block scan of 256 bins)
+  unsigned long long run[3];
+  for (int c = 0; c < 3; ++c) {
+    unsigned long long x = hist[c];
+    const int lane = v & 31, wid = v >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wtot[wid] = x;
+    __syncthreads();
+    unsigned long long add = 0;
+    for (int i = 0; i < wid; ++i) add += wtot[i];
+    __syncthreads();
+    run[c] = x + add;
+  }
+  __shared__ unsigned long long s_total;
+  if (v == 255) s_total = run[0];
+  __syncthreads();
+  const unsigned long long tot = s_total;
+  if (tot != 0) {
+    const double dtot = static_cast<double>(tot);
+    for (int c = 0; c < 3; ++c) {
+      const double cdf = static_cast<double>(run[c]) / dtot;
+      if (cdf >= g->lambda) atomicMin(&first1[c], v);
+      if (cdf >= 1.0 - g->lambda) atomicMin(&first2[c], v);
+    }
+  }
+  __syncthreads();
+  if (v == 0) {
+    ok = 0;
+    st->report.frame_index = st->frame_counter;
+    if (tot != 0) {
+      BalanceState& bs = st->balance;
+      if (bs.n == 3) {
+        for (int i = 0; i < 2; ++i)
+          for (int c = 0; c < 3; ++c) {
+            bs.m1[i][c] = bs.m1[i + 1][c];
+            bs.m2[i][c] = bs.m2[i + 1][c];
+          }
+        bs.n = 2;
+      }
+      for (int c = 0; c < 3; ++c) {
+        // m1 defaults to 255 and is only taken at or before m2 (the
+        // reference loop breaks at m2, color_balance.cpp:25-35)
+        const int m2 = first2[c] < 256 ? first2[c] : 255;
+        const int m1 = first1[c] <= m2 ? first1[c] : 255;
+        bs.m1[bs.n][c] = m1;
+        bs.m2[bs.n][c] = m2;
+      }
+      bs.n++;
+      const int nh = bs.n;
+      for (int c = 0; c < 3; ++c) {
+        double s1 = 0.0, s2 = 0.0;
+        for (int i = 0; i < nh; ++i) {
+          s1 += bs.m1[i][c];
+          s2 += bs.m2[i][c];
+        }
+        int a = static_cast<int>(llround(s1 / static_cast<double>(nh)));
+        int b = static_cast<int>(llround(s2 / static_cast<double>(nh)));
+        if (a > b) {
+          const int tmp = a;
+          a = b;
+          b = tmp;
+        }
+        sm1[c] = a;
+        sm2[c] = b;
+      }
+      ok = g->curve_ok;
+    }
+    st->report.balanced = ok;
+    for (int c = 0; c < 3; ++c) {
+      st->report.m1[c] = ok ? sm1[c] : 0;
+      st->report.m2[c] = ok ? sm2[c] : 0;
+    }
+    st->frame_counter++;
+  }
+  __syncthreads();
+  for (int c = 0; c < 3; ++c) {
+    unsigned char out = static_cast<unsigned char>(v);
+    if (ok) {
+      const int m1 = sm1[c], m2 = sm2[c];
+      const double tb = g->target_black, tw = g->target_white;
+      const double x = static_cast<double>(v);
+      double val;
+      if (m1 >= m2) {
+        val = tb + (tw - tb) * (x / 255.0);
+      } else {
+        const double lm1 = tb + (tw - tb) * (static_cast<double>(m1) / 255.0);
+        const double lm2 = tb + (tw - tb) * (static_cast<double>(m2) / 255.0);
+        if (x <= m1) {
+          val = (m1 == 0) ? tb : tb + (lm1 - tb) * pow(x / m1, g->gamma_dark);
+        } else if (x >= m2) {
+          val = (m2 == 255) ? tw : lm2 + (tw - lm2) * pow((x - m2) / (255.0 - m2), g->gamma_bright);
+        } else {
+          val = lm1 + (lm2 - lm1) * (x - m1) / (m2 - m1);
+        }
+      }
+      out = quantize_d(val);
+    }
+    st->lut[c][v] = out;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_canvas(const Geometry* __restrict__ g,
+                                                DevState* __restrict__ st,
+                                                uchar4* __restrict__ pano, long long n_px) {
+  __shared__ unsigned int hist[3][256];
+  __shared__ bool last;
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    hist[0][i] = 0;
+    hist[1][i] = 0;
+    hist[2][i] = 0;
+  }
+  __syncthreads();
+  const int cw = g->canvas_w;
+  const int ref = g->reference;
+  const ViewDesc& vr = g->views[ref];
+  const int np = g->n_pairs;
+  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < n_px;
+       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int y = static_cast<int>(idx / cw);
+    const int x = static_cast<int>(idx - static_cast<long long>(y) * cw);
+    const double X = static_cast<double>(x) + g->offx;
+    const double Y = static_cast<double>(y) + g->offy;
+    uchar4 pv = make_uchar4(0, 0, 0, 0);
+    if (x >= vr.bbox[0] && x < vr.bbox[2] && y >= vr.bbox[1] && y < vr.bbox[3]) {
+      // reuse a star pair's crop of the reference view when inside its bounds
+      int kc = -1;
+      for (int k = 0; k < np; ++k) {
+        const PairDesc& p = g->pairs[k];
+        if (p.partner == ref && x >= p.x0 && x < p.x0 + p.w && y >= p.y0 && y < p.y0 + p.h) {
+          kc = k;
+          break;
+        }
+      }
+      if (kc >= 0) {
+        const PairDesc& p = g->pairs[kc];
+        pv = p.crop_raw[1][(y - p.y0) * p.w + (x - p.x0)];
+      } else {
+        pv = warp_sample(vr, g->frames[ref], X, Y);
+      }
+    }
+    for (int k = 0; k < np; ++k) {
+      const PairDesc& p = g->pairs[k];
+      const ViewDesc& vv = g->views[p.view];
+      if (x < vv.bbox[0] || x >= vv.bbox[2] || y < vv.bbox[1] || y >= vv.bbox[3]) continue;
+      const int dx = x - p.x0, dy = y - p.y0;
+      const bool inb = dx >= 0 && dy >= 0 && dx < p.w && dy < p.h;
+      const uchar4 q = inb ? p.crop_raw[0][dy * p.w + dx] : warp_sample(vv, g->frames[p.view], X, Y);
+      if (!q.w) continue;
+      if (pv.w) {
+        if (inb) {
+          uchar4 f;
+          if (fused_pixel(g, p, dx, dy, f)) pv = f;
+        }
+      } else {
+        pv = apply_matrix(st->mview[p.view], q);
+      }
+    }
+    pano[idx] = pv;
+    if (pv.w) {
+      atomicAdd(&hist[0][pv.x], 1u);
+      atomicAdd(&hist[1][pv.y], 1u);
+      atomicAdd(&hist[2][pv.z], 1u);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x)
+    for (int c = 0; c < 3; ++c)
+      if (hist[c][i]) atomicAdd(&st->pano_hist[c][i], hist[c][i]);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&st->canvas_done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x == 0) st->canvas_done = 0;
+  balance_lut(g, st);
+}
+
+// apply_tone_rows (pipeline.cpp:84-96) + conversion to the reference's Frame
+// layout (RGB8 interleaved + 0/1 mask).  4 pixels per thread: one 16-byte
+// uchar4x4 load, three 4-byte RGB stores, one 4-byte mask store.
+__global__ void __launch_bounds__(256) k_tone(const DevState* __restrict__ st,
+                                              const uchar4* __restrict__ pano, long long n_px,
+                                              std::uint8_t* __restrict__ out_rgb,
+                                              std::uint8_t* __restrict__ out_mask) {
+  __shared__ unsigned char lut[3][256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    lut[0][i] = st->lut[0][i];
+    lut[1][i] = st->lut[1][i];
+    lut[2][i] = st->lut[2][i];
+  }
+  __syncthreads();
+  const long long n4 = n_px / 4;
+  const uint4* p4 = reinterpret_cast<const uint4*>(pano);
+  unsigned int* rgb4 = reinterpret_cast<unsigned int*>(out_rgb);
+  unsigned int* m4 = reinterpret_cast<unsigned int*>(out_mask);
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const uint4 q = p4[i];
+    const unsigned int px[4] = {q.x, q.y, q.z, q.w};
+    unsigned char o[12];
+    unsigned int mask = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const unsigned int v = px[j];
+      const unsigned char r = v & 0xff, gg = (v >> 8) & 0xff, b = (v >> 16) & 0xff;
+      const unsigned char valid = (v >> 24) & 0xff;
+      o[3 * j + 0] = valid ? lut[0][r] : r;
+      o[3 * j + 1] = valid ? lut[1][gg] : gg;
+      o[3 * j + 2] = valid ? lut[2][b] : b;
+      mask |= static_cast<unsigned int>(valid ? 1 : 0) << (8 * j);
+    }
+    rgb4[3 * i + 0] = o[0] | (o[1] << 8) | (o[2] << 16) | (static_cast<unsigned int>(o[3]) << 24);
+    rgb4[3 * i + 1] = o[4] | (o[5] << 8) | (o[6] << 16) | (static_cast<unsigned int>(o[7]) << 24);
+    rgb4[3 * i + 2] = o[8] | (o[9] << 8) | (o[10] << 16) | (static_cast<unsigned int>(o[11]) << 24);
+    m4[i] = mask;
+  }
+  // tail
+  if (blockIdx.x == 0) {
+    for (long long i = n4 * 4 + threadIdx.x; i < n_px; i += blockDim.x) {
+      const uchar4 v = pano[i];
+      out_rgb[3 * i + 0] = v.w ? lut[0][v.x] : v.x;
+      out_rgb[3 * i + 1] = v.w ? lut[1][v.y] : v.y;
+      out_rgb[3 * i + 2] = v.w ? lut[2][v.z] : v.z;
+      out_mask[i] = v.w ? 1 : 0;
+    }
+  }
+}
+
+// Full-canvas warp of one view (init masks and debug readback).
+__global__ void __launch_bounds__(256) k_warp_view(const Geometry* __restrict__ g, int view,
+                                                   const std::uint8_t* __restrict__ frame,
+                                                   std::uint8_t* __restrict__ rgb,
+                                                   std::uint8_t* __restrict__ mask) {
+  const ViewDesc& v = g->views[view];
+  const long long n = static_cast<long long>(g->canvas_w) * g->canvas_h;
+  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < n;
+       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int y = static_cast<int>(idx / g->canvas_w);
+    const int x = static_cast<int>(idx - static_cast<long long>(y) * g->canvas_w);
+    const uchar4 o = warp_sample(v, frame, static_cast<double>(x) + g->offx,
+                                 static_cast<double>(y) + g->offy);
+    if (rgb) {
+      rgb[3 * idx + 0] = o.x;
+      rgb[3 * idx + 1] = o.y;
+      rgb[3 * idx + 2] = o.z;
+    }
+    mask[idx] = o.w;
+  }
+}
+
+// Geometry-only validity of the warp (the input frames are unmasked, so the
+// mask does not depend on pixel values): sample_bilinear is valid iff a
+// neighbour with positive weight lies inside the frame.
+__global__ void __launch_bounds__(256) k_warp_mask(const Geometry* __restrict__ g, int view,
+                                                   std::uint8_t* __restrict__ mask) {
+  const ViewDesc& v = g->views[view];
+  const long long n = static_cast<long long>(g->canvas_w) * g->canvas_h;
+  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < n;
+       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int y = static_cast<int>(idx / g->canvas_w);
+    const int x = static_cast<int>(idx - static_cast<long long>(y) * g->canvas_w);
+    const double X = static_cast<double>(x) + g->offx;
+    const double Y = static_cast<double>(y) + g->offy;
+    const double* m = v.inv;
+    const double sx0 = (m[0] * X + m[1] * Y) + m[2];
+    const double sy0 = (m[3] * X + m[4] * Y) + m[5];
+    const double sz0 = (m[6] * X + m[7] * Y) + m[8];
+    unsigned char ok = 0;
+    if (!(fabs(sz0) < 1e-12)) {
+      const double sx = sx0 / sz0, sy = sy0 / sz0;
+      const double fx0 = floor(sx), fy0 = floor(sy);
+      const int x0 = static_cast<int>(fx0), y0 = static_cast<int>(fy0);
+      const double ax = sx - fx0, ay = sy - fy0;
+      for (int j = 0; j < 2 && !ok; ++j)
+        for (int i = 0; i < 2 && !ok; ++i) {
+          const double w = (i ? ax : 1.0 - ax) * (j ? ay : 1.0 - ay);
+          const unsigned xx = static_cast<unsigned>(x0) + i, yy = static_cast<unsigned>(y0) + j;
+          if (w > 0.0 && xx < static_cast<unsigned>(v.width) && yy < static_cast<unsigned>(v.height))
+            ok = 1;
+        }
+    }
+    mask[idx] = ok;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+static inline int blocks_for(long long n, int per = 256, int cap = 65535) {
+  long long b = (n + per - 1) / per;
+  if (b < 1) b = 1;
+  if (b > cap) b = cap;
+  return static_cast<int>(b);
+}
+
+void launch_crop_warp(const Geometry* g, int n_pairs, int max_crop_px, cudaStream_t s) {
+  dim3 grid(blocks_for(max_crop_px), 2 * n_pairs);
+  k_crop_warp<<<grid, 256, 0, s>>>(g);
+}
+
+void launch_canvas(const Geometry* g, DevState* st, uchar4* pano, long long n_px, int num_sms,
+                   cudaStream_t s) {
+  const int blocks = static_cast<int>(
+      std::min<long long>(static_cast<long long>(num_sms) * 8, (n_px + 255) / 256));
+  k_canvas<<<blocks < 1 ? 1 : blocks, 256, 0, s>>>(g, st, pano, n_px);
+}
+
+void launch_tone(const DevState* st, const uchar4* pano, long long n_px, std::uint8_t* out_rgb,
+                 std::uint8_t* out_mask, cudaStream_t s) {
+  k_tone<<<blocks_for(n_px / 4 + 1, 256, 148 * 16), 256, 0, s>>>(st, pano, n_px, out_rgb,
+                                                                  out_mask);
+}
+
+void launch_warp_view(const Geometry* g, int view, const std::uint8_t* frame, std::uint8_t* rgb,
+                      std::uint8_t* mask, cudaStream_t s) {
+  k_warp_view<<<148 * 8, 256, 0, s>>>(g, view, frame, rgb, mask);
+}
+
+void launch_warp_mask(const Geometry* g, int view, std::uint8_t* mask, cudaStream_t s) {
+  k_warp_mask<<<148 * 8, 256, 0, s>>>(g, view, mask);
+}
+
+}  // namespace stitch_b200_dev

@@ -1,0 +1,244 @@
+// color_kernels.cu -- 3D-M spatio-temporal colour transfer (transfer_step,
+// /root/reference/proj/src/color_transfer.cpp:133-191, as driven by
+// process_frame, pipeline.cpp:279-300), one launch per pair depth.
+//
+// Single HBM pass over the jointly valid overlap pixels reduced to integer
+// tables (source/reference histograms and the conditional sums
+// S_{a|b}[v] = sum_{x_b = v} x_a), from which the specification LUT and the
+// exact moments X^T X and X^T Y of the LUT-revised rows follow:
+//   X^T X[a][a] = sum_v v^2 h_a[v],        X^T X[a][b] = sum_v v S_{a|b}[v]
+//   X^T Y[a][a] = sum_v v LUT_a[v] h_a[v], X^T Y[a][b] = sum_v LUT_b[v] S_{a|b}[v]
+// All entries are integers < 2^53, so the window sum (ring of <= 3 frames)
+// is bit-identical to the reference's stacked-row normal equations.  The
+// last CTA of each pair (grid-wide counter) performs the solve.
+#include <cuda_runtime.h>
+
+#include "device_math.cuh"
+#include "kernels.cuh"
+
+namespace stitch_b200_dev {
+
+__device__ __forceinline__ int sidx(int a, int b) { return a * 2 + (b > a ? b - 1 : b); }
+
+// Block-wide inclusive scan of 256 values (one per thread), u64.
+__device__ __forceinline__ unsigned long long block_scan256(unsigned long long x,
+                                                            unsigned long long* warp_tot) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[wid] = x;
+  __syncthreads();
+  unsigned long long add = 0;
+  for (int i = 0; i < wid; ++i) add += warp_tot[i];
+  __syncthreads();
+  return x + add;
+}
+
+__device__ __forceinline__ unsigned long long block_sum256(unsigned long long x,
+                                                           unsigned long long* warp_tot) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+  if (lane == 0) warp_tot[wid] = x;
+  __syncthreads();
+  unsigned long long t = 0;
+  for (int i = 0; i < 8; ++i) t += warp_tot[i];
+  __syncthreads();
+  return t;
+}
+
+// The per-pair solve, executed by the pair's last CTA (256 threads):
+// histogram_specification (color_transfer.cpp:28-55), revised-row moments,
+// TransferWindow push (color_transfer.cpp:16-21), solve_color_matrix with
+// the rank guard (color_transfer.cpp:73-99), and the degrade rules of
+// process_frame (pipeline.cpp:282-293).
+__device__ void pair_solve(const PairDesc& p, int k, DevState* __restrict__ st) {
+  __shared__ unsigned char lut[3][256];
+  __shared__ unsigned long long cref[3][256];
+  __shared__ unsigned long long wtot[8];
+  __shared__ unsigned long long mom[18];
+  PairStats& in = st->stats[k];
+  const int v = threadIdx.x;  // level owned by this thread
+  const unsigned long long n = in.n;
+  unsigned int hs[3], hr[3];
+  unsigned long long ss[6];
+  for (int c = 0; c < 3; ++c) {
+    hs[c] = in.hs[c][v];
+    hr[c] = in.hr[c][v];
+    in.hs[c][v] = 0;  // reset the accumulators for the next frame
+    in.hr[c][v] = 0;
+  }
+  for (int c = 0; c < 6; ++c) {
+    ss[c] = in.s[c][v];
+    in.s[c][v] = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) in.n = 0;
+  if (n == 0) {
+    // EmptyRegion from transfer_step: identity M, window untouched
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < 9; ++i) {
+        const double e = (i % 4 == 0) ? 1.0 : 0.0;
+        st->mview[p.view][i] = e;
+        st->report.m[k][i] = e;
+      }
+      st->report.rank_deficient[k] = 1;
+    }
+    return;
+  }
+  // LUT[c][v] = smallest u in [0, 255) with cum_ref[u] >= cum_src[v], else
+  // 255 -- the reference's monotone scan (both histograms count the same n
+  // jointly valid pixels, so its cross-multiplied compare reduces to this).
+  unsigned long long csrc[3];
+  for (int c = 0; c < 3; ++c) {
+    cref[c][v] = block_scan256(hr[c], wtot);
+    csrc[c] = block_scan256(hs[c], wtot);
+  }
+  __syncthreads();
+  for (int c = 0; c < 3; ++c) {
+    int lo = 0, hi = 255;  // search in [0, 255)
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (cref[c][mid] < csrc[c])
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    lut[c][v] = static_cast<unsigned char>(lo);
+  }
+  __syncthreads();
+  // exact integer moments
+  const unsigned long long vv = static_cast<unsigned long long>(v);
+  for (int q = 0; q < 18; ++q) {
+    const int which = q / 9, a = (q % 9) / 3, b = q % 3;
+    unsigned long long x;
+    if (which == 0)
+      x = (a == b) ? vv * vv * hs[a] : vv * ss[sidx(a, b)];
+    else
+      x = (a == b) ? vv * lut[a][v] * hs[a] : static_cast<unsigned long long>(lut[b][v]) * ss[sidx(a, b)];
+    const unsigned long long tot = block_sum256(x, wtot);
+    if (threadIdx.x == 0) mom[q] = tot;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  PairWindow& w = st->windows[k];
+  const int size = w.size < w.capacity ? w.size + 1 : w.capacity;
+  for (int i = size - 1; i > 0; --i) w.e[i] = w.e[i - 1];
+  for (int i = 0; i < 9; ++i) {
+    w.e[0].xtx[i] = mom[i];
+    w.e[0].xty[i] = mom[9 + i];
+  }
+  w.e[0].n = n;
+  w.size = size;
+  unsigned long long sx[9] = {0}, sy[9] = {0}, total = 0;
+  for (int e = 0; e < size; ++e) {
+    for (int i = 0; i < 9; ++i) {
+      sx[i] += w.e[e].xtx[i];
+      sy[i] += w.e[e].xty[i];
+    }
+    total += w.e[e].n;
+  }
+  double normal[9], xty[9], m[9], sv[3];
+  for (int i = 0; i < 9; ++i) {
+    normal[i] = static_cast<double>(sx[i]);
+    xty[i] = static_cast<double>(sy[i]);
+  }
+  sym3_eigen(normal, sv);
+  int degraded = 0;
+  if (total < 3 || sv[2] < 1e-8 * sv[0]) {
+    for (int i = 0; i < 9; ++i) m[i] = (i % 4 == 0) ? 1.0 : 0.0;  // RankDeficient
+    degraded = 1;
+  } else {
+    ldlt_solve3(normal, xty, m);
+  }
+  for (int i = 0; i < 9; ++i) {
+    st->mview[p.view][i] = m[i];
+    st->report.m[k][i] = m[i];
+  }
+  st->report.rank_deficient[k] = degraded;
+}
+
+// grid: (blocks per pair, pairs of this depth); 256 threads.
+__global__ void __launch_bounds__(256) k_pair_color(const Geometry* __restrict__ g,
+                                                    DevState* __restrict__ st,
+                                                    const int* __restrict__ list) {
+  __shared__ unsigned int hs[3][256];
+  __shared__ unsigned int hr[3][256];
+  __shared__ unsigned int ss[6][256];
+  __shared__ unsigned int cnt;
+  __shared__ bool last;
+  const int k = list[blockIdx.y];
+  const PairDesc& p = g->pairs[k];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    for (int c = 0; c < 3; ++c) {
+      hs[c][i] = 0;
+      hr[c][i] = 0;
+    }
+    for (int c = 0; c < 6; ++c) ss[c][i] = 0;
+  }
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  // the partner is already corrected when it is not the reference (chain)
+  const bool correct_partner = p.partner != g->reference;
+  const double* mp = st->mview[p.partner];
+  const int n = p.w * p.h;
+  unsigned int local = 0;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += gridDim.x * blockDim.x) {
+    const uchar4 a = p.crop_raw[0][idx];
+    uchar4 b = p.crop_raw[1][idx];
+    if (!a.w || !b.w) continue;
+    if (correct_partner) b = apply_matrix(mp, b);
+    const unsigned int xa[3] = {a.x, a.y, a.z};
+    atomicAdd(&hs[0][a.x], 1u);
+    atomicAdd(&hs[1][a.y], 1u);
+    atomicAdd(&hs[2][a.z], 1u);
+    atomicAdd(&hr[0][b.x], 1u);
+    atomicAdd(&hr[1][b.y], 1u);
+    atomicAdd(&hr[2][b.z], 1u);
+#pragma unroll
+    for (int ca = 0; ca < 3; ++ca)
+#pragma unroll
+      for (int cb = 0; cb < 3; ++cb)
+        if (ca != cb) atomicAdd(&ss[sidx(ca, cb)][xa[cb]], xa[ca]);
+    ++local;
+  }
+  atomicAdd(&cnt, local);
+  __syncthreads();
+  PairStats& out = st->stats[k];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    for (int c = 0; c < 3; ++c) {
+      if (hs[c][i]) atomicAdd(&out.hs[c][i], hs[c][i]);
+      if (hr[c][i]) atomicAdd(&out.hr[c][i], hr[c][i]);
+    }
+    for (int c = 0; c < 6; ++c)
+      if (ss[c][i]) atomicAdd(&out.s[c][i], static_cast<unsigned long long>(ss[c][i]));
+  }
+  if (threadIdx.x == 0 && cnt) atomicAdd(&out.n, static_cast<unsigned long long>(cnt));
+  // last CTA of this pair performs the solve
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&st->pair_done[k], 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x == 0) st->pair_done[k] = 0;
+  pair_solve(p, k, st);
+}
+
+static inline int blocks_for(long long n, int per, int cap) {
+  long long b = (n + per - 1) / per;
+  if (b < 1) b = 1;
+  if (b > cap) b = cap;
+  return static_cast<int>(b);
+}
+
+void launch_pair_color(const Geometry* g, DevState* st, const int* list, int n, int max_crop_px,
+                       cudaStream_t s) {
+  dim3 grid(blocks_for(max_crop_px, 256 * 16, 512), n);
+  k_pair_color<<<grid, 256, 0, s>>>(g, st, list);
+}
+
+}  // namespace stitch_b200_dev

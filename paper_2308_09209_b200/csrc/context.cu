@@ -203,10 +203,7 @@ int enqueue_op(Ctx* ctx, const Op& op, cudaStream_t s) {
       launch_crop_warp(ctx->dg, g.n_pairs, ctx->max_crop_px, s);
       return 1;
     case OP_STATS:
-      launch_pair_stats(ctx->dg, ctx->dst, ctx->d_lists + op.offset, op.count, ctx->max_crop_px, s);
-      return 1;
-    case OP_SOLVE:
-      launch_pair_solve(ctx->dg, ctx->dst, ctx->d_lists + op.offset, op.count, s);
+      launch_pair_color(ctx->dg, ctx->dst, ctx->d_lists + op.offset, op.count, ctx->max_crop_px, s);
       return 1;
     case OP_PREP:
       if (!g.n_pairs) return 0;
@@ -224,9 +221,6 @@ int enqueue_op(Ctx* ctx, const Op& op, cudaStream_t s) {
       return 1;
     case OP_CANVAS:
       launch_canvas(ctx->dg, ctx->dst, ctx->d_pano, ctx->n_px, ctx->num_sms, s);
-      return 1;
-    case OP_BALANCE:
-      launch_balance(ctx->dg, ctx->dst, s);
       return 1;
     case OP_TONE:
       launch_tone(ctx->dst, ctx->d_pano, ctx->n_px, ctx->d_out_rgb, ctx->d_out_mask, s);
@@ -396,8 +390,6 @@ int build_context(const stitch_b200_init* in, int device,
       if (depth[k] == d) lists.push_back(k);
     op.count = static_cast<int>(lists.size()) - op.offset;
     plan.push_back(op);
-    op.kind = OP_SOLVE;
-    plan.push_back(op);
   }
   plan.push_back({OP_PREP});
   plan.push_back({OP_EVENT, 0, 0, 0, 0, 0, 2});
@@ -423,18 +415,6 @@ int build_context(const stitch_b200_init* in, int device,
     if (op.count) plan.push_back(op);
   }
   for (int l = Lmax - 1; l >= 0; --l) {
-    Op up{OP_UP};
-    up.offset = static_cast<int>(up_table.size());
-    for (auto& t : tasks) {
-      if (l >= t.L - 1) continue;  // coarsest level of this task or above
-      const int w = t.dims[l][0], h = t.dims[l][1];
-      const int wi = t.dims[l + 1][0], hi = t.dims[l + 1][1];
-      up_table.push_back({t.U[t.cur], t.V[t.cur], wi, hi, t.U[1 - t.cur], t.V[1 - t.cur], w, h});
-      t.cur ^= 1;
-      up.max_px = std::max(up.max_px, w * h);
-    }
-    up.count = static_cast<int>(up_table.size()) - up.offset;
-    if (up.count) plan.push_back(up);
     for (int it = 0; it < 5; ++it) {  // 5 warps per level (flow.cpp:78)
       Op op{OP_HS};
       op.offset = static_cast<int>(hs_table.size());
@@ -452,6 +432,10 @@ int build_context(const stitch_b200_init* in, int device,
         h.w = t.dims[l][0];
         h.h = t.dims[l][1];
         h.zero_in = (l == t.L - 1 && it == 0) ? 1 : 0;
+        // finer level, first warp: upsample the coarser flow on load
+        h.up_in = (l < t.L - 1 && it == 0) ? 1 : 0;
+        h.wc = h.up_in ? t.dims[l + 1][0] : 0;
+        h.hc = h.up_in ? t.dims[l + 1][1] : 0;
         h.zero_invalid = (l == 0 && it == 4) ? 1 : 0;
         h.mask_a = p.crop_cor[sa];
         h.mask_b = p.crop_cor[sb];
@@ -472,7 +456,6 @@ int build_context(const stitch_b200_init* in, int device,
   plan.push_back({OP_EVENT, 0, 0, 0, 0, 0, 3});
   plan.push_back({OP_CANVAS});
   plan.push_back({OP_EVENT, 0, 0, 0, 0, 0, 4});
-  plan.push_back({OP_BALANCE});
   plan.push_back({OP_TONE});
   plan.push_back({OP_EVENT, 0, 0, 0, 0, 0, 5});
 

@@ -105,6 +105,10 @@ struct HsTask {
   int zero_invalid;  // final write: zero where either crop is invalid
   const uchar4* mask_a;
   const uchar4* mask_b;
+  // first warp of a finer level: u_in/v_in are the coarser level's flow
+  // (wc x hc) and are upsampled on load (resize_bilinear, flow.cpp:163-167)
+  int up_in;
+  int wc, hc;
 };
 
 struct UpTask {
@@ -133,14 +137,14 @@ struct DevState {
   unsigned char lut[3][256];
   DevReport report;
   long long frame_counter;
+  unsigned int pair_done[kMaxPairs];  // CTA completion counters (last-CTA solve)
+  unsigned int canvas_done;
 };
 
 // ---- launchers (kernels.cu) ----
 void launch_crop_warp(const Geometry* g, int n_pairs, int max_crop_px, cudaStream_t s);
-void launch_pair_stats(const Geometry* g, DevState* st, const int* pair_list, int n,
+void launch_pair_color(const Geometry* g, DevState* st, const int* pair_list, int n,
                        int max_crop_px, cudaStream_t s);
-void launch_pair_solve(const Geometry* g, DevState* st, const int* pair_list, int n,
-                       cudaStream_t s);
 void launch_flow_prepare(const Geometry* g, DevState* st, int n_pairs, int max_crop_px,
                          cudaStream_t s);
 void launch_pyr_down(const PyrTask* tasks, int n, int max_px, cudaStream_t s);
@@ -151,7 +155,6 @@ void launch_hs_iter(const HsTask* tasks, int n, int max_w, int max_h, int sweeps
                     float alpha2, cudaStream_t s);
 void launch_canvas(const Geometry* g, DevState* st, uchar4* pano, long long n_px,
                    int num_sms, cudaStream_t s);
-void launch_balance(const Geometry* g, DevState* st, cudaStream_t s);
 void launch_tone(const DevState* st, const uchar4* pano, long long n_px,
                  std::uint8_t* out_rgb, std::uint8_t* out_mask, cudaStream_t s);
 void launch_warp_view(const Geometry* g, int view, const std::uint8_t* frame,

@@ -273,3 +273,26 @@ def test_create_from_snapshot_matches_initialize():
         a = pb.process_frame(state, fr)
         b = pb.process_frame(snap, fr)
         np.testing.assert_array_equal(a.panorama.data, b.panorama.data)
+
+
+@pytest.mark.parametrize("env", [{"STITCH_B200_HS_FORCE_EXACT": "1"},
+                                 {"STITCH_B200_HS_VARIANT": "1"},
+                                 {"STITCH_B200_HS_VARIANT": "2"},
+                                 {"STITCH_B200_HS_VARIANT": "3"},
+                                 {"STITCH_B200_HS_VARIANT": "4"},
+                                 {"STITCH_B200_HS_VARIANT": "4",
+                                  "STITCH_B200_HS_FORCE_EXACT": "1"}])
+def test_flow_kernel_variants_bit_exact(env):
+    """The register-blocked Jacobi kernel's region variants and its exact
+    IEEE-division fallback path (forced) all reproduce the oracle's flows;
+    run in a subprocess because the switches are read once per process."""
+    import os
+    import subprocess
+    import sys
+
+    code = ("import tests.test_gpu_parity as T; T.test_c1_config_parity_all_stages(); "
+            "T.test_three_view_parity({})")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, **env},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
