@@ -114,8 +114,8 @@ SYMBOLS = [
     ("stitch_b200_synth_render", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int]),
 ]
 
-OP_KIND_NAMES = ["crop_warp", "pair_color", "pair_solve", "flow_prepare", "pyr_down", "upsample",
-                 "hs_iter", "canvas_balance", "balance", "tone"]
+OP_KIND_NAMES = ["crop_warp", "pair_color", "pair_solve", "flow_prepare", "pyr_down", "hs_linearize",
+                 "hs_sweeps", "canvas_balance", "balance", "tone"]
 
 _lib = None
 

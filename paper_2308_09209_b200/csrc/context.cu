@@ -33,14 +33,15 @@ int fail(int code, const std::string& msg) {
       return fail(STITCH_B200_CudaError, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
   } while (0)
 
-enum OpKind { OP_CROP, OP_STATS, OP_SOLVE, OP_PREP, OP_PYR, OP_UP, OP_HS, OP_CANVAS, OP_BALANCE,
-              OP_TONE, OP_EVENT };
+enum OpKind { OP_CROP, OP_STATS, OP_SOLVE, OP_PREP, OP_PYR, OP_HSPREP, OP_HS, OP_CANVAS,
+              OP_BALANCE, OP_TONE, OP_EVENT };
 
 struct Op {
   OpKind kind;
   int offset = 0, count = 0;  // task table slice or pair list slice
   int max_w = 0, max_h = 0, max_px = 0;
   int event = 0;
+  int sweeps = 0;  // OP_HS: Jacobi sweeps of this launch (segment length)
 };
 
 }  // namespace
@@ -67,7 +68,7 @@ struct Ctx {
   int n_levels_max = 0;
   std::vector<Op> plan;
   HsTask* d_hs = nullptr;
-  UpTask* d_up = nullptr;
+  PrepTask* d_hp = nullptr;
   PyrTask* d_pyr = nullptr;
   int* d_lists = nullptr;
   cudaGraph_t graph = nullptr;
@@ -212,12 +213,11 @@ int enqueue_op(Ctx* ctx, const Op& op, cudaStream_t s) {
     case OP_PYR:
       launch_pyr_down(ctx->d_pyr + op.offset, op.count, op.max_px, s);
       return 1;
-    case OP_UP:
-      launch_upsample(ctx->d_up + op.offset, op.count, op.max_px, s);
+    case OP_HSPREP:
+      launch_hs_prepare(ctx->d_hp + op.offset, op.count, op.max_w, op.max_h, ctx->alpha2, s);
       return 1;
     case OP_HS:
-      launch_hs_iter(ctx->d_hs + op.offset, op.count, op.max_w, op.max_h, ctx->sweeps,
-                     ctx->alpha2, s);
+      launch_hs_iter(ctx->d_hs + op.offset, op.count, op.max_w, op.max_h, op.sweeps, s);
       return 1;
     case OP_CANVAS:
       launch_canvas(ctx->dg, ctx->dst, ctx->d_pano, ctx->n_px, ctx->num_sms, s);
@@ -331,6 +331,7 @@ int build_context(const stitch_b200_init* in, int device,
     int dims[kMaxLevels][2];
     float* U[2];
     float* V[2];
+    float* K[4];  // gx, gy, c, denom planes of the current warp iteration
     int cur;
   };
   std::vector<TaskState> tasks;
@@ -369,6 +370,7 @@ int build_context(const stitch_b200_init* in, int device,
         CUDA_TRY(ctx->alloc(&t.U[b], p.w * p.h));
         CUDA_TRY(ctx->alloc(&t.V[b], p.w * p.h));
       }
+      for (int b = 0; b < 4; ++b) CUDA_TRY(ctx->alloc(&t.K[b], p.w * p.h));
       t.cur = 0;
       tasks.push_back(t);
     }
@@ -376,7 +378,7 @@ int build_context(const stitch_b200_init* in, int device,
   ctx->n_levels_max = Lmax;
 
   std::vector<HsTask> hs_table;
-  std::vector<UpTask> up_table;
+  std::vector<PrepTask> hp_table;
   std::vector<PyrTask> pyr_table;
   std::vector<int> lists;
   std::vector<Op>& plan = ctx->plan;
@@ -414,38 +416,74 @@ int build_context(const stitch_b200_init* in, int device,
     op.count = static_cast<int>(pyr_table.size()) - op.offset;
     if (op.count) plan.push_back(op);
   }
+  // Each warp iteration (5 per level, flow.cpp:78) is one linearisation
+  // launch (constants planes) followed by its `sweeps` Jacobi sweeps as
+  // nseg launches (segments), ping-ponging two flow buffers per task.
+  const int nseg = hs_segments(ctx->sweeps);
+  std::vector<int> seg_len(nseg, ctx->sweeps / nseg);
+  for (int j = 0; j < ctx->sweeps % nseg; ++j) seg_len[j]++;
   for (int l = Lmax - 1; l >= 0; --l) {
-    for (int it = 0; it < 5; ++it) {  // 5 warps per level (flow.cpp:78)
-      Op op{OP_HS};
-      op.offset = static_cast<int>(hs_table.size());
+    for (int it = 0; it < 5; ++it) {
+      Op pop{OP_HSPREP};
+      pop.offset = static_cast<int>(hp_table.size());
       for (auto& t : tasks) {
         if (l >= t.L) continue;
         const PairDesc& p = g.pairs[t.k];
         const int sa = t.dir == 0 ? 0 : 1, sb = 1 - sa;
-        HsTask h{};
-        h.a = p.pyr[sa][l];
-        h.b = p.pyr[sb][l];
-        h.u_in = t.U[t.cur];
-        h.v_in = t.V[t.cur];
-        h.u_out = t.U[1 - t.cur];
-        h.v_out = t.V[1 - t.cur];
-        h.w = t.dims[l][0];
-        h.h = t.dims[l][1];
-        h.zero_in = (l == t.L - 1 && it == 0) ? 1 : 0;
-        // finer level, first warp: upsample the coarser flow on load
-        h.up_in = (l < t.L - 1 && it == 0) ? 1 : 0;
-        h.wc = h.up_in ? t.dims[l + 1][0] : 0;
-        h.hc = h.up_in ? t.dims[l + 1][1] : 0;
-        h.zero_invalid = (l == 0 && it == 4) ? 1 : 0;
-        h.mask_a = p.crop_cor[sa];
-        h.mask_b = p.crop_cor[sb];
-        t.cur ^= 1;
-        hs_table.push_back(h);
-        op.max_w = std::max(op.max_w, h.w);
-        op.max_h = std::max(op.max_h, h.h);
+        PrepTask q{};
+        q.a = p.pyr[sa][l];
+        q.b = p.pyr[sb][l];
+        // u0: zero at the coarsest level's first warp, the coarser flow
+        // upsampled at a finer level's first warp, else the previous warp's
+        q.mode = (l == t.L - 1 && it == 0) ? 0 : (it == 0 ? 2 : 1);
+        q.u_in = t.U[t.cur];
+        q.v_in = t.V[t.cur];
+        q.wc = q.mode == 2 ? t.dims[l + 1][0] : 0;
+        q.hc = q.mode == 2 ? t.dims[l + 1][1] : 0;
+        q.w = t.dims[l][0];
+        q.h = t.dims[l][1];
+        for (int b = 0; b < 4; ++b) (&q.kgx)[b] = t.K[b];
+        if (q.mode != 1) {
+          q.u0_out = t.U[1 - t.cur];
+          q.v0_out = t.V[1 - t.cur];
+          t.cur ^= 1;
+        }
+        hp_table.push_back(q);
+        pop.max_w = std::max(pop.max_w, q.w);
+        pop.max_h = std::max(pop.max_h, q.h);
       }
-      op.count = static_cast<int>(hs_table.size()) - op.offset;
-      if (op.count) plan.push_back(op);
+      pop.count = static_cast<int>(hp_table.size()) - pop.offset;
+      if (pop.count) plan.push_back(pop);
+      for (int j = 0; j < nseg; ++j) {
+        Op op{OP_HS};
+        op.sweeps = seg_len[j];
+        op.offset = static_cast<int>(hs_table.size());
+        for (auto& t : tasks) {
+          if (l >= t.L) continue;
+          const PairDesc& p = g.pairs[t.k];
+          const int sa = t.dir == 0 ? 0 : 1, sb = 1 - sa;
+          HsTask h{};
+          h.kgx = t.K[0];
+          h.kgy = t.K[1];
+          h.kcc = t.K[2];
+          h.kdn = t.K[3];
+          h.u_in = t.U[t.cur];
+          h.v_in = t.V[t.cur];
+          h.u_out = t.U[1 - t.cur];
+          h.v_out = t.V[1 - t.cur];
+          h.w = t.dims[l][0];
+          h.h = t.dims[l][1];
+          h.zero_invalid = (l == 0 && it == 4 && j == nseg - 1) ? 1 : 0;
+          h.mask_a = p.crop_cor[sa];
+          h.mask_b = p.crop_cor[sb];
+          t.cur ^= 1;
+          hs_table.push_back(h);
+          op.max_w = std::max(op.max_w, h.w);
+          op.max_h = std::max(op.max_h, h.h);
+        }
+        op.count = static_cast<int>(hs_table.size()) - op.offset;
+        if (op.count) plan.push_back(op);
+      }
     }
   }
   for (auto& t : tasks) {
@@ -461,14 +499,14 @@ int build_context(const stitch_b200_init* in, int device,
 
   // upload tables + geometry + state
   CUDA_TRY(ctx->alloc(&ctx->d_hs, hs_table.size() + 1));
-  CUDA_TRY(ctx->alloc(&ctx->d_up, up_table.size() + 1));
+  CUDA_TRY(ctx->alloc(&ctx->d_hp, hp_table.size() + 1));
   CUDA_TRY(ctx->alloc(&ctx->d_pyr, pyr_table.size() + 1));
   CUDA_TRY(ctx->alloc(&ctx->d_lists, lists.size() + 1));
   if (!hs_table.empty())
     CUDA_TRY(cudaMemcpy(ctx->d_hs, hs_table.data(), hs_table.size() * sizeof(HsTask),
                         cudaMemcpyHostToDevice));
-  if (!up_table.empty())
-    CUDA_TRY(cudaMemcpy(ctx->d_up, up_table.data(), up_table.size() * sizeof(UpTask),
+  if (!hp_table.empty())
+    CUDA_TRY(cudaMemcpy(ctx->d_hp, hp_table.data(), hp_table.size() * sizeof(PrepTask),
                         cudaMemcpyHostToDevice));
   if (!pyr_table.empty())
     CUDA_TRY(cudaMemcpy(ctx->d_pyr, pyr_table.data(), pyr_table.size() * sizeof(PyrTask),
@@ -493,6 +531,7 @@ int build_context(const stitch_b200_init* in, int device,
     CUDA_TRY(cudaMemcpy(ctx->dst, hs.get(), sizeof(DevState), cudaMemcpyHostToDevice));
   }
   CUDA_TRY(prepare_hs(ctx->sweeps));
+  for (int j = 1; j <= ctx->sweeps; ++j) CUDA_TRY(prepare_hs(j));
   for (auto& e : ctx->ev) CUDA_TRY(cudaEventCreate(&e));
   for (auto& e : ctx->ring_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_ptr_ring),

@@ -93,31 +93,41 @@ struct Geometry {
   int curve_ok;
 };
 
-struct HsTask {
+// Linearisation of one warp iteration (refine_level, flow.cpp:84-108) for
+// one (pair, direction) task at one level: u0 (zero / previous flow /
+// coarser flow upsampled, flow.cpp:163-167) -> warped image bw -> the
+// per-pixel Jacobi constants gx, gy, c = it - gx*u0 - gy*v0 and
+// denom = alpha2 + gx*gx + gy*gy, written as planes.
+struct PrepTask {
   const float* a;  // luma of the first image at this level
   const float* b;  // luma of the second image
+  int mode;        // 0: u0 = 0, 1: u0 = (u_in, v_in), 2: upsample (u_in, v_in) from wc x hc
   const float* u_in;
+  const float* v_in;
+  int wc, hc;
+  int w, h;
+  float* u0_out;  // modes 0 and 2: u0 materialised here (the sweeps' start state)
+  float* v0_out;
+  float* kgx;
+  float* kgy;
+  float* kcc;
+  float* kdn;
+};
+
+// One segment of Jacobi sweeps (flow.cpp:109-134) on constant planes.
+struct HsTask {
+  const float* kgx;
+  const float* kgy;
+  const float* kcc;
+  const float* kdn;
+  const float* u_in;  // state at the start of the segment
   const float* v_in;
   float* u_out;
   float* v_out;
   int w, h;
-  int zero_in;       // coarsest level, first warp: flow starts at zero
   int zero_invalid;  // final write: zero where either crop is invalid
   const uchar4* mask_a;
   const uchar4* mask_b;
-  // first warp of a finer level: u_in/v_in are the coarser level's flow
-  // (wc x hc) and are upsampled on load (resize_bilinear, flow.cpp:163-167)
-  int up_in;
-  int wc, hc;
-};
-
-struct UpTask {
-  const float* u_in;
-  const float* v_in;
-  int w_in, h_in;
-  float* u_out;
-  float* v_out;
-  int w, h;
 };
 
 struct PyrTask {
@@ -148,11 +158,14 @@ void launch_pair_color(const Geometry* g, DevState* st, const int* pair_list, in
 void launch_flow_prepare(const Geometry* g, DevState* st, int n_pairs, int max_crop_px,
                          cudaStream_t s);
 void launch_pyr_down(const PyrTask* tasks, int n, int max_px, cudaStream_t s);
-void launch_upsample(const UpTask* tasks, int n, int max_px, cudaStream_t s);
 size_t hs_smem_bytes(int sweeps);
+// how many launches (sweep segments) one warp iteration of `sweeps` uses
+int hs_segments(int sweeps);
 cudaError_t prepare_hs(int sweeps);
+void launch_hs_prepare(const PrepTask* tasks, int n, int max_w, int max_h, float alpha2,
+                       cudaStream_t s);
 void launch_hs_iter(const HsTask* tasks, int n, int max_w, int max_h, int sweeps,
-                    float alpha2, cudaStream_t s);
+                    cudaStream_t s);
 void launch_canvas(const Geometry* g, DevState* st, uchar4* pano, long long n_px,
                    int num_sms, cudaStream_t s);
 void launch_tone(const DevState* st, const uchar4* pano, long long n_px,

@@ -276,16 +276,19 @@ def test_create_from_snapshot_matches_initialize():
 
 
 @pytest.mark.parametrize("env", [{"STITCH_B200_HS_FORCE_EXACT": "1"},
+                                 {"STITCH_B200_HS_VARIANT": "0"},
                                  {"STITCH_B200_HS_VARIANT": "1"},
-                                 {"STITCH_B200_HS_VARIANT": "2"},
-                                 {"STITCH_B200_HS_VARIANT": "3"},
-                                 {"STITCH_B200_HS_VARIANT": "4"},
-                                 {"STITCH_B200_HS_VARIANT": "4",
-                                  "STITCH_B200_HS_FORCE_EXACT": "1"}])
+                                 {"STITCH_B200_HS_VARIANT": "5"},
+                                 {"STITCH_B200_HS_VARIANT": "5",
+                                  "STITCH_B200_HS_FORCE_EXACT": "1"},
+                                 {"STITCH_B200_HS_SEGS": "1"},
+                                 {"STITCH_B200_HS_SEGS": "3"},
+                                 {"STITCH_B200_HS_SEGS": "10", "STITCH_B200_HS_VARIANT": "5"}])
 def test_flow_kernel_variants_bit_exact(env):
-    """The register-blocked Jacobi kernel's region variants and its exact
-    IEEE-division fallback path (forced) all reproduce the oracle's flows;
-    run in a subprocess because the switches are read once per process."""
+    """The register-blocked Jacobi kernel's region variants, sweep
+    segmentations and its exact IEEE-division fallback path (forced) all
+    reproduce the oracle's flows; run in a subprocess because the switches
+    are read once per process."""
     import os
     import subprocess
     import sys
