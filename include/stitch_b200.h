@@ -193,9 +193,9 @@ int stitch_b200_launches_per_frame(const stitch_b200_ctx* ctx);
  * context stream with a CUDA event pair around every kernel launch.
  * dev_frames as for stitch_b200_process_device.  Writes up to max_ops
  * (kernel-kind, milliseconds) pairs and returns the number of launches, or
- * a negative status.  Kinds: 0 crop_warp, 1 pair_color (stats + solve),
- * 3 flow_prepare, 4 pyr_down, 5 hs_linearize, 6 hs_sweeps,
- * 7 canvas_balance, 9 tone.  Advances the temporal state like a processed frame. */
+ * a negative status.  Kinds: 0 expand_rgba, 1 crop_warp, 2 pair_color
+ * (stats + solve), 4 flow_prepare, 5 pyr_down, 6 hs_linearize, 7 hs_sweeps,
+ * 8 canvas_balance, 10 tone.  Advances the temporal state like a processed frame. */
 int stitch_b200_profile_frame(stitch_b200_ctx* ctx,
                               const uint8_t* const* dev_frames, int max_ops,
                               int* kinds, float* ms);

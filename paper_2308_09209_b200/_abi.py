@@ -114,7 +114,7 @@ SYMBOLS = [
     ("stitch_b200_synth_render", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int]),
 ]
 
-OP_KIND_NAMES = ["crop_warp", "pair_color", "pair_solve", "flow_prepare", "pyr_down", "hs_linearize",
+OP_KIND_NAMES = ["expand_rgba", "crop_warp", "pair_color", "pair_solve", "flow_prepare", "pyr_down", "hs_linearize",
                  "hs_sweeps", "canvas_balance", "balance", "tone"]
 
 _lib = None

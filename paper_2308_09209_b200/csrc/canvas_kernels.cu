@@ -3,6 +3,7 @@
 // balance LUT) and the tone/output pass.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "device_math.cuh"
@@ -11,26 +12,67 @@
 namespace stitch_b200_dev {
 
 // ---------------------------------------------------------------------------
+// RGB8 -> RGBA8 expansion of the camera frames (one 32-bit load per
+// bilinear neighbour downstream).  4 pixels per thread: three aligned 32-bit
+// loads, one 16-byte store.  grid: (x blocks, views)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void expand_span(const std::uint8_t* __restrict__ src,
+                                            uchar4* __restrict__ dst, long long n) {
+  const long long n4 = n / 4;
+  const unsigned int* s4 = reinterpret_cast<const unsigned int*>(src);
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const unsigned int w0 = __ldg(s4 + 3 * i), w1 = __ldg(s4 + 3 * i + 1),
+                       w2 = __ldg(s4 + 3 * i + 2);
+    uint4 o;
+    o.x = w0 & 0x00ffffffu;
+    o.y = (w0 >> 24) | ((w1 & 0x0000ffffu) << 8);
+    o.z = (w1 >> 16) | ((w2 & 0x000000ffu) << 16);
+    o.w = w2 >> 8;
+    d4[i] = o;
+  }
+  if (blockIdx.x == 0)
+    for (long long i = n4 * 4 + threadIdx.x; i < n; i += blockDim.x)
+      dst[i] = make_uchar4(src[3 * i], src[3 * i + 1], src[3 * i + 2], 0);
+}
+
+__global__ void __launch_bounds__(256) k_expand(const Geometry* __restrict__ g) {
+  const int v = blockIdx.y;
+  const ViewDesc& vd = g->views[v];
+  expand_span(g->frames[v], g->rgba[v], static_cast<long long>(vd.width) * vd.height);
+}
+
+__global__ void __launch_bounds__(256) k_expand_one(const std::uint8_t* __restrict__ src,
+                                                    uchar4* __restrict__ dst, long long n) {
+  expand_span(src, dst, n);
+}
+
+// ---------------------------------------------------------------------------
 // Geometric warping of the overlap crops: crop_frame(warp_frame(...), bounds)
 // (pipeline.cpp:310-311) evaluated directly on the bounds.
-// grid: (x blocks, 2*n_pairs)
+// grid: (ceil(max_w/64), ceil(max_h/4), 2*n_pairs), block (64, 4)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_crop_warp(const Geometry* __restrict__ g) {
-  const int k = blockIdx.y >> 1;
-  const int side = blockIdx.y & 1;
-  const PairDesc& p = g->pairs[k];
-  const int n = p.w * p.h;
+__device__ __forceinline__ uchar4 warp_cv(const CanvasView& v, double X, double Y) {
+  ViewDesc d;
+  d.width = v.w;
+  d.height = v.h;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) d.inv[i] = v.inv[i];
+  return warp_sample(d, v.rgba, X, Y);
+}
+
+__global__ void __launch_bounds__(256) k_crop_warp(const __grid_constant__ CanvasParams P) {
+  const int k = blockIdx.z >> 1;
+  const int side = blockIdx.z & 1;
+  const CanvasPair& p = P.pairs[k];
+  const int dx = blockIdx.x * 64 + threadIdx.x;
+  const int dy = blockIdx.y * 4 + threadIdx.y;
+  if (dx >= p.w || dy >= p.h) return;
   const int view = side ? p.partner : p.view;
-  const ViewDesc& v = g->views[view];
-  const std::uint8_t* frame = g->frames[view];
-  uchar4* out = p.crop_raw[side];
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += gridDim.x * blockDim.x) {
-    const int dy = idx / p.w;
-    const int dx = idx - dy * p.w;
-    const double X = static_cast<double>(p.x0 + dx) + g->offx;
-    const double Y = static_cast<double>(p.y0 + dy) + g->offy;
-    out[idx] = warp_sample(v, frame, X, Y);
-  }
+  const double X = static_cast<double>(p.x0 + dx) + P.offx;
+  const double Y = static_cast<double>(p.y0 + dy) + P.offy;
+  p.crop_raw[side][dy * p.w + dx] = warp_cv(P.views[view], X, Y);
 }
 
 // ---------------------------------------------------------------------------
@@ -44,21 +86,21 @@ __global__ void __launch_bounds__(256) k_crop_warp(const Geometry* __restrict__ 
 // panorama (compute_histogram, histogram.cpp:5-18); the last CTA turns it
 // into the tone LUT (global balancing, pipeline.cpp:336-355).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ bool fused_pixel(const Geometry* __restrict__ g, const PairDesc& p,
-                                            int dx, int dy, uchar4& out) {
+__device__ __forceinline__ bool fused_pixel(const CanvasParams& P, const CanvasPair& p, int dx,
+                                            int dy, uchar4& out) {
   const int i = dy * p.w + dx;
-  const float ti = p.theta_i[i];
+  const float ti = p.theta[i];
   const float tj = 1.0f - ti;  // BlendWeights::theta_j (flow.cpp:276)
-  const float wi = g->weighting == 0 ? ti : tj;
-  const float wj = g->weighting == 0 ? tj : ti;
+  const float wi = P.weighting == 0 ? ti : tj;
+  const float wj = P.weighting == 0 ? tj : ti;
   float ri, gi, bi, rj, gj, bj;
   const bool vi = sample_crop(p.crop_cor[0], p.w, p.h,
-                              static_cast<double>(static_cast<float>(dx) + wi * p.flow_u[0][i]),
-                              static_cast<double>(static_cast<float>(dy) + wi * p.flow_v[0][i]),
+                              static_cast<double>(static_cast<float>(dx) + wi * p.fu[0][i]),
+                              static_cast<double>(static_cast<float>(dy) + wi * p.fv[0][i]),
                               ri, gi, bi);
   const bool vj = sample_crop(p.crop_cor[1], p.w, p.h,
-                              static_cast<double>(static_cast<float>(dx) + wj * p.flow_u[1][i]),
-                              static_cast<double>(static_cast<float>(dy) + wj * p.flow_v[1][i]),
+                              static_cast<double>(static_cast<float>(dx) + wj * p.fu[1][i]),
+                              static_cast<double>(static_cast<float>(dy) + wj * p.fv[1][i]),
                               rj, gj, bj);
   if (!vi && !vj) return false;
   float r, gg, b;
@@ -201,60 +243,67 @@ __device__ void balance_lut(const Geometry* __restrict__ g, DevState* __restrict
   }
 }
 
-__global__ void __launch_bounds__(256) k_canvas(const Geometry* __restrict__ g,
-                                                DevState* __restrict__ st,
-                                                uchar4* __restrict__ pano, long long n_px) {
+__global__ void __launch_bounds__(256, 3) k_canvas(const __grid_constant__ CanvasParams P,
+                                                   const Geometry* __restrict__ g,
+                                                   DevState* __restrict__ st,
+                                                   uchar4* __restrict__ pano) {
   __shared__ unsigned int hist[3][256];
+  __shared__ double mview[kMaxViews][9];
   __shared__ bool last;
   for (int i = threadIdx.x; i < 256; i += blockDim.x) {
     hist[0][i] = 0;
     hist[1][i] = 0;
     hist[2][i] = 0;
   }
+  for (int i = threadIdx.x; i < kMaxViews * 9; i += blockDim.x) mview[i / 9][i % 9] = st->mview[i / 9][i % 9];
   __syncthreads();
-  const int cw = g->canvas_w;
-  const int ref = g->reference;
-  const ViewDesc& vr = g->views[ref];
-  const int np = g->n_pairs;
-  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < n_px;
-       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int y = static_cast<int>(idx / cw);
-    const int x = static_cast<int>(idx - static_cast<long long>(y) * cw);
-    const double X = static_cast<double>(x) + g->offx;
-    const double Y = static_cast<double>(y) + g->offy;
+  const int cw = P.cw, ch = P.ch;
+  const int ref = P.ref;
+  const CanvasView& vr = P.views[ref];
+  const int np = P.np;
+  const int tiles_x = (cw + 63) / 64;
+  const int ntiles = tiles_x * ((ch + 3) / 4);
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int ty = tile / tiles_x;
+    const int x = (tile - ty * tiles_x) * 64 + threadIdx.x % 64;
+    const int y = ty * 4 + threadIdx.x / 64;
+    if (x >= cw || y >= ch) continue;
+    const long long idx = static_cast<long long>(y) * cw + x;
+    const double X = static_cast<double>(x) + P.offx;
+    const double Y = static_cast<double>(y) + P.offy;
     uchar4 pv = make_uchar4(0, 0, 0, 0);
     if (x >= vr.bbox[0] && x < vr.bbox[2] && y >= vr.bbox[1] && y < vr.bbox[3]) {
       // reuse a star pair's crop of the reference view when inside its bounds
       int kc = -1;
       for (int k = 0; k < np; ++k) {
-        const PairDesc& p = g->pairs[k];
+        const CanvasPair& p = P.pairs[k];
         if (p.partner == ref && x >= p.x0 && x < p.x0 + p.w && y >= p.y0 && y < p.y0 + p.h) {
           kc = k;
           break;
         }
       }
       if (kc >= 0) {
-        const PairDesc& p = g->pairs[kc];
+        const CanvasPair& p = P.pairs[kc];
         pv = p.crop_raw[1][(y - p.y0) * p.w + (x - p.x0)];
       } else {
-        pv = warp_sample(vr, g->frames[ref], X, Y);
+        pv = warp_cv(vr, X, Y);
       }
     }
     for (int k = 0; k < np; ++k) {
-      const PairDesc& p = g->pairs[k];
-      const ViewDesc& vv = g->views[p.view];
+      const CanvasPair& p = P.pairs[k];
+      const CanvasView& vv = P.views[p.view];
       if (x < vv.bbox[0] || x >= vv.bbox[2] || y < vv.bbox[1] || y >= vv.bbox[3]) continue;
       const int dx = x - p.x0, dy = y - p.y0;
       const bool inb = dx >= 0 && dy >= 0 && dx < p.w && dy < p.h;
-      const uchar4 q = inb ? p.crop_raw[0][dy * p.w + dx] : warp_sample(vv, g->frames[p.view], X, Y);
+      const uchar4 q = inb ? p.crop_raw[0][dy * p.w + dx] : warp_cv(vv, X, Y);
       if (!q.w) continue;
       if (pv.w) {
         if (inb) {
           uchar4 f;
-          if (fused_pixel(g, p, dx, dy, f)) pv = f;
+          if (fused_pixel(P, p, dx, dy, f)) pv = f;
         }
       } else {
-        pv = apply_matrix(st->mview[p.view], q);
+        pv = apply_matrix(mview[p.view], q);
       }
     }
     pano[idx] = pv;
@@ -331,7 +380,7 @@ __global__ void __launch_bounds__(256) k_tone(const DevState* __restrict__ st,
 
 // Full-canvas warp of one view (init masks and debug readback).
 __global__ void __launch_bounds__(256) k_warp_view(const Geometry* __restrict__ g, int view,
-                                                   const std::uint8_t* __restrict__ frame,
+                                                   const uchar4* __restrict__ frame,
                                                    std::uint8_t* __restrict__ rgb,
                                                    std::uint8_t* __restrict__ mask) {
   const ViewDesc& v = g->views[view];
@@ -396,16 +445,25 @@ static inline int blocks_for(long long n, int per = 256, int cap = 65535) {
   return static_cast<int>(b);
 }
 
-void launch_crop_warp(const Geometry* g, int n_pairs, int max_crop_px, cudaStream_t s) {
-  dim3 grid(blocks_for(max_crop_px), 2 * n_pairs);
-  k_crop_warp<<<grid, 256, 0, s>>>(g);
+void launch_expand(const Geometry* g, int n_views, long long max_px, cudaStream_t s) {
+  dim3 grid(blocks_for(max_px / 4 + 1, 256, 148 * 4), n_views);
+  k_expand<<<grid, 256, 0, s>>>(g);
 }
 
-void launch_canvas(const Geometry* g, DevState* st, uchar4* pano, long long n_px, int num_sms,
-                   cudaStream_t s) {
-  const int blocks = static_cast<int>(
-      std::min<long long>(static_cast<long long>(num_sms) * 8, (n_px + 255) / 256));
-  k_canvas<<<blocks < 1 ? 1 : blocks, 256, 0, s>>>(g, st, pano, n_px);
+void launch_expand_one(const std::uint8_t* rgb, uchar4* rgba, long long n_px, cudaStream_t s) {
+  k_expand_one<<<blocks_for(n_px / 4 + 1, 256, 148 * 4), 256, 0, s>>>(rgb, rgba, n_px);
+}
+
+void launch_crop_warp(const CanvasParams& P, int max_w, int max_h, cudaStream_t s) {
+  dim3 grid((max_w + 63) / 64, (max_h + 3) / 4, 2 * P.np);
+  k_crop_warp<<<grid, dim3(64, 4), 0, s>>>(P);
+}
+
+void launch_canvas(const CanvasParams& P, const Geometry* g, DevState* st, uchar4* pano,
+                   int num_sms, cudaStream_t s) {
+  const long long tiles = static_cast<long long>((P.cw + 63) / 64) * ((P.ch + 3) / 4);
+  const int blocks = static_cast<int>(std::min<long long>(static_cast<long long>(num_sms) * 4, tiles));
+  k_canvas<<<blocks < 1 ? 1 : blocks, 256, 0, s>>>(P, g, st, pano);
 }
 
 void launch_tone(const DevState* st, const uchar4* pano, long long n_px, std::uint8_t* out_rgb,
@@ -414,7 +472,7 @@ void launch_tone(const DevState* st, const uchar4* pano, long long n_px, std::ui
                                                                   out_mask);
 }
 
-void launch_warp_view(const Geometry* g, int view, const std::uint8_t* frame, std::uint8_t* rgb,
+void launch_warp_view(const Geometry* g, int view, const uchar4* frame, std::uint8_t* rgb,
                       std::uint8_t* mask, cudaStream_t s) {
   k_warp_view<<<148 * 8, 256, 0, s>>>(g, view, frame, rgb, mask);
 }

@@ -33,7 +33,7 @@ int fail(int code, const std::string& msg) {
       return fail(STITCH_B200_CudaError, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
   } while (0)
 
-enum OpKind { OP_CROP, OP_STATS, OP_SOLVE, OP_PREP, OP_PYR, OP_HSPREP, OP_HS, OP_CANVAS,
+enum OpKind { OP_EXPAND, OP_CROP, OP_STATS, OP_SOLVE, OP_PREP, OP_PYR, OP_HSPREP, OP_HS, OP_CANVAS,
               OP_BALANCE, OP_TONE, OP_EVENT };
 
 struct Op {
@@ -63,6 +63,8 @@ struct Ctx {
   std::uint8_t* d_out_mask = nullptr;
   long long n_px = 0;
   int max_crop_px = 0;
+  int max_crop_w = 0, max_crop_h = 0;
+  long long max_view_px = 0;
   int sweeps = 10;
   float alpha2 = 225.0f;
   int n_levels_max = 0;
@@ -83,6 +85,7 @@ struct Ctx {
   bool frames_are_own = true;
   std::vector<int> pair_levels;
   float* d_zero = nullptr;
+  CanvasParams cparams{};
 
   ~Ctx() {
     if (stream) cudaStreamSynchronize(stream);
@@ -199,9 +202,12 @@ void fill_views(Geometry& g, const stitch_b200_init* in) {
 int enqueue_op(Ctx* ctx, const Op& op, cudaStream_t s) {
   const Geometry& g = ctx->hg;
   switch (op.kind) {
+    case OP_EXPAND:
+      launch_expand(ctx->dg, g.n_views, ctx->max_view_px, s);
+      return 1;
     case OP_CROP:
       if (!g.n_pairs) return 0;
-      launch_crop_warp(ctx->dg, g.n_pairs, ctx->max_crop_px, s);
+      launch_crop_warp(ctx->cparams, ctx->max_crop_w, ctx->max_crop_h, s);
       return 1;
     case OP_STATS:
       launch_pair_color(ctx->dg, ctx->dst, ctx->d_lists + op.offset, op.count, ctx->max_crop_px, s);
@@ -220,7 +226,7 @@ int enqueue_op(Ctx* ctx, const Op& op, cudaStream_t s) {
       launch_hs_iter(ctx->d_hs + op.offset, op.count, op.max_w, op.max_h, op.sweeps, s);
       return 1;
     case OP_CANVAS:
-      launch_canvas(ctx->dg, ctx->dst, ctx->d_pano, ctx->n_px, ctx->num_sms, s);
+      launch_canvas(ctx->cparams, ctx->dg, ctx->dst, ctx->d_pano, ctx->num_sms, s);
       return 1;
     case OP_TONE:
       launch_tone(ctx->dst, ctx->d_pano, ctx->n_px, ctx->d_out_rgb, ctx->d_out_mask, s);
@@ -276,6 +282,9 @@ int build_context(const stitch_b200_init* in, int device,
     ctx->frame_bytes[v] = static_cast<size_t>(in->view_width[v]) * in->view_height[v] * 3;
     CUDA_TRY(ctx->alloc(&ctx->d_frames[v], ctx->frame_bytes[v]));
     g.frames[v] = ctx->d_frames[v];
+    const long long vpx = static_cast<long long>(in->view_width[v]) * in->view_height[v];
+    CUDA_TRY(ctx->alloc(&g.rgba[v], vpx));
+    ctx->max_view_px = std::max(ctx->max_view_px, vpx);
   }
   ctx->n_px = static_cast<long long>(g.canvas_w) * g.canvas_h;
   CUDA_TRY(ctx->alloc(&ctx->d_pano, static_cast<size_t>(ctx->n_px) + 4));
@@ -297,6 +306,8 @@ int build_context(const stitch_b200_init* in, int device,
     p.h = sp.y1 - sp.y0;
     const int n = p.w * p.h;
     ctx->max_crop_px = std::max(ctx->max_crop_px, n);
+    ctx->max_crop_w = std::max(ctx->max_crop_w, p.w);
+    ctx->max_crop_h = std::max(ctx->max_crop_h, p.h);
     max_zero = std::max(max_zero, n);
     ctx->theta_host[k].assign(sp.theta_i, sp.theta_i + n);
     ctx->init.pairs[k].theta_i = ctx->theta_host[k].data();
@@ -383,6 +394,7 @@ int build_context(const stitch_b200_init* in, int device,
   std::vector<int> lists;
   std::vector<Op>& plan = ctx->plan;
   plan.push_back({OP_EVENT, 0, 0, 0, 0, 0, 0});
+  plan.push_back({OP_EXPAND});
   plan.push_back({OP_CROP});
   plan.push_back({OP_EVENT, 0, 0, 0, 0, 0, 1});
   for (int d = 1; d <= max_depth; ++d) {
@@ -514,6 +526,40 @@ int build_context(const stitch_b200_init* in, int device,
   if (!lists.empty())
     CUDA_TRY(cudaMemcpy(ctx->d_lists, lists.data(), lists.size() * sizeof(int),
                         cudaMemcpyHostToDevice));
+  {
+    CanvasParams& P = ctx->cparams;
+    P.cw = g.canvas_w;
+    P.ch = g.canvas_h;
+    P.ref = g.reference;
+    P.np = g.n_pairs;
+    P.weighting = g.weighting;
+    P.offx = g.offx;
+    P.offy = g.offy;
+    for (int v = 0; v < g.n_views; ++v) {
+      for (int i = 0; i < 9; ++i) P.views[v].inv[i] = g.views[v].inv[i];
+      P.views[v].rgba = g.rgba[v];
+      P.views[v].w = g.views[v].width;
+      P.views[v].h = g.views[v].height;
+      for (int i = 0; i < 4; ++i) P.views[v].bbox[i] = g.views[v].bbox[i];
+    }
+    for (int k = 0; k < g.n_pairs; ++k) {
+      const PairDesc& p = g.pairs[k];
+      CanvasPair& q = P.pairs[k];
+      q.view = p.view;
+      q.partner = p.partner;
+      q.x0 = p.x0;
+      q.y0 = p.y0;
+      q.w = p.w;
+      q.h = p.h;
+      q.theta = p.theta_i;
+      for (int s2 = 0; s2 < 2; ++s2) {
+        q.crop_raw[s2] = p.crop_raw[s2];
+        q.crop_cor[s2] = p.crop_cor[s2];
+        q.fu[s2] = p.flow_u[s2];
+        q.fv[s2] = p.flow_v[s2];
+      }
+    }
+  }
   CUDA_TRY(ctx->alloc(&ctx->dg, 1));
   CUDA_TRY(cudaMemcpy(ctx->dg, &g, sizeof(Geometry), cudaMemcpyHostToDevice));
   CUDA_TRY(ctx->alloc(&ctx->dst, 1));
@@ -968,16 +1014,21 @@ int stitch_b200_debug_warp_view(stitch_b200_ctx* h, int view, const uint8_t* hos
   CUDA_TRY(cudaSetDevice(ctx->device));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   std::uint8_t *df = nullptr, *dr = nullptr, *dm = nullptr;
+  uchar4* dq = nullptr;
   const size_t n = static_cast<size_t>(ctx->n_px);
+  const long long vpx = static_cast<long long>(ctx->hg.views[view].width) * ctx->hg.views[view].height;
   CUDA_TRY(cudaMalloc(&df, ctx->frame_bytes[view]));
+  CUDA_TRY(cudaMalloc(&dq, vpx * sizeof(uchar4)));
   CUDA_TRY(cudaMalloc(&dr, n * 3));
   CUDA_TRY(cudaMalloc(&dm, n));
   CUDA_TRY(cudaMemcpy(df, host_frame, ctx->frame_bytes[view], cudaMemcpyHostToDevice));
-  launch_warp_view(ctx->dg, view, df, dr, dm, ctx->stream);
+  launch_expand_one(df, dq, vpx, ctx->stream);
+  launch_warp_view(ctx->dg, view, dq, dr, dm, ctx->stream);
   cudaError_t e = cudaStreamSynchronize(ctx->stream);
   if (e == cudaSuccess) e = cudaMemcpy(rgb, dr, n * 3, cudaMemcpyDeviceToHost);
   if (e == cudaSuccess) e = cudaMemcpy(mask, dm, n, cudaMemcpyDeviceToHost);
   cudaFree(df);
+  cudaFree(dq);
   cudaFree(dr);
   cudaFree(dm);
   if (e != cudaSuccess) return fail(STITCH_B200_CudaError, cudaGetErrorString(e));

@@ -80,6 +80,7 @@ struct BalanceState {
 
 struct Geometry {
   const std::uint8_t* frames[kMaxViews];  // device RGB8 inputs (per frame)
+  uchar4* rgba[kMaxViews];                // the inputs expanded to RGBA8
   int canvas_w, canvas_h;
   double offx, offy;
   int n_views, reference, n_pairs;
@@ -115,6 +116,32 @@ struct PrepTask {
 };
 
 // One segment of Jacobi sweeps (flow.cpp:109-134) on constant planes.
+// Compact, launch-constant descriptors of the canvas and crop-warp passes,
+// passed by value (__grid_constant__ kernel parameter, read through the
+// constant bank with warp-uniform indices).
+struct CanvasView {
+  double inv[9];
+  const uchar4* rgba;
+  int w, h;
+  int bbox[4];
+};
+
+struct CanvasPair {
+  int view, partner, x0, y0, w, h;
+  const float* theta;
+  uchar4* crop_raw[2];
+  const uchar4* crop_cor[2];
+  const float* fu[2];
+  const float* fv[2];
+};
+
+struct CanvasParams {
+  int cw, ch, ref, np, weighting;
+  double offx, offy;
+  CanvasView views[kMaxViews];
+  CanvasPair pairs[kMaxPairs];
+};
+
 struct HsTask {
   const float* kgx;
   const float* kgy;
@@ -152,7 +179,8 @@ struct DevState {
 };
 
 // ---- launchers (kernels.cu) ----
-void launch_crop_warp(const Geometry* g, int n_pairs, int max_crop_px, cudaStream_t s);
+void launch_expand(const Geometry* g, int n_views, long long max_px, cudaStream_t s);
+void launch_crop_warp(const CanvasParams& P, int max_w, int max_h, cudaStream_t s);
 void launch_pair_color(const Geometry* g, DevState* st, const int* pair_list, int n,
                        int max_crop_px, cudaStream_t s);
 void launch_flow_prepare(const Geometry* g, DevState* st, int n_pairs, int max_crop_px,
@@ -166,12 +194,13 @@ void launch_hs_prepare(const PrepTask* tasks, int n, int max_w, int max_h, float
                        cudaStream_t s);
 void launch_hs_iter(const HsTask* tasks, int n, int max_w, int max_h, int sweeps,
                     cudaStream_t s);
-void launch_canvas(const Geometry* g, DevState* st, uchar4* pano, long long n_px,
+void launch_canvas(const CanvasParams& P, const Geometry* g, DevState* st, uchar4* pano,
                    int num_sms, cudaStream_t s);
 void launch_tone(const DevState* st, const uchar4* pano, long long n_px,
                  std::uint8_t* out_rgb, std::uint8_t* out_mask, cudaStream_t s);
-void launch_warp_view(const Geometry* g, int view, const std::uint8_t* frame,
-                      std::uint8_t* rgb, std::uint8_t* mask, cudaStream_t s);
+void launch_warp_view(const Geometry* g, int view, const uchar4* frame, std::uint8_t* rgb,
+                      std::uint8_t* mask, cudaStream_t s);
+void launch_expand_one(const std::uint8_t* rgb, uchar4* rgba, long long n_px, cudaStream_t s);
 void launch_warp_mask(const Geometry* g, int view, std::uint8_t* mask, cudaStream_t s);
 
 }  // namespace stitch_b200_dev
