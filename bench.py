@@ -49,6 +49,8 @@ WORKLOADS = {
     "c4": dict(views=8, width=3840, height=2160, focal_scale=1.03,
                desc="8 cameras 3840x2160 RGB single panorama stream"),
 }
+# BASELINE.json configs[4]: 64 independent 4x1080p streams sharded over the
+# GPUs -> `--config c2 --total-streams 64`
 
 
 def build_scene(wl, seed):
@@ -140,43 +142,50 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # per-kernel algorithmic bytes / flops
 # ---------------------------------------------------------------------------
-def kernel_model(state, wl):
+def pair_levels(p, levels=4):
+    w, h = p.bounds[2] - p.bounds[0], p.bounds[3] - p.bounds[1]
+    if w < 16 or h < 16:
+        return []
+    dims = [(w, h)]
+    for _ in range(1, levels):
+        if dims[-1][0] < 16 or dims[-1][1] < 16:
+            break
+        dims.append((max(1, dims[-1][0] // 2), max(1, dims[-1][1] // 2)))
+    return dims
+
+
+def kernel_model(state, wl, sweeps=10, warps=5):
     """Algorithmic HBM bytes (and FP32 flops for the flow) per frame, per
-    kernel family."""
+    kernel family (DESIGN.md section 4)."""
     pairs = state.pairs
     o = [(p.bounds[2] - p.bounds[0]) * (p.bounds[3] - p.bounds[1]) for p in pairs]
     P = state.canvas_width * state.canvas_height
-    inputs = wl["views"] * wl["width"] * wl["height"] * 3
-    # flow pyramid pixel counts per task (2 directions per pair)
-    lv_px = []
-    for p in pairs:
-        w, h = p.bounds[2] - p.bounds[0], p.bounds[3] - p.bounds[1]
-        if w < 16 or h < 16:
-            continue
-        levels = [(w, h)]
-        for _ in range(1, 4):
-            if levels[-1][0] < 16 or levels[-1][1] < 16:
-                break
-            levels.append((max(1, levels[-1][0] // 2), max(1, levels[-1][1] // 2)))
-        lv_px.append(sum(a * b for a, b in levels))
-    flow_px = 2 * sum(lv_px)  # both directions
-    sweeps = 10
-    model = {
-        # reads 3 B of source per warped pixel (both sides of each crop), writes uchar4
-        "crop_warp": dict(bytes=sum(2 * (3 + 4) * n for n in o)),
-        # reads two uchar4 crops
-        "pair_stats": dict(bytes=sum(8 * n for n in o)),
-        # reads raw crops, writes corrected crops + luma
+    in_px = wl["views"] * wl["width"] * wl["height"]
+    lv = [pair_levels(p) for p in pairs]
+    flow_px = 2 * sum(a * b for dims in lv for a, b in dims)  # both directions, all levels
+    coarse_px = 2 * sum(a * b for dims in lv for a, b in dims[:-1])  # finer levels (upsampled u0)
+    segs = int(os.environ.get("STITCH_B200_HS_SEGS", "2"))
+    return {
+        # RGB8 read, RGBA8 write
+        "expand_rgba": dict(bytes=7 * in_px),
+        # each crop pixel: one RGBA source pixel read (4 B), uchar4 write; both sides
+        "crop_warp": dict(bytes=sum(2 * (4 + 4) * n for n in o)),
+        # two uchar4 crops read
+        "pair_color": dict(bytes=sum(8 * n for n in o)),
+        # raw crops read, corrected crops + luma written
         "flow_prepare": dict(bytes=sum(2 * (4 + 4 + 4) * n for n in o)),
-        # per warp iteration: read u,v,a,b; write u,v (24 B/px); 5 iterations per level
-        "hs_iter": dict(bytes=5 * 24 * flow_px,
-                        flops=5 * flow_px * (sweeps * 18 + 40)),
-        # inputs once, pano uchar4 write, overlap crops + flows + weights
-        "canvas": dict(bytes=inputs + 4 * P + sum((8 + 16 + 4) * n for n in o)),
+        # per warp iteration and pixel: u0 (8) + a (4) + b (4) read, 4 constant planes
+        # (16) written; + u0 materialised (8) on each level's first warp
+        "hs_linearize": dict(bytes=warps * 32 * flow_px + 8 * flow_px),
+        # per segment and pixel: state (8) + constants (16) read, state (8) written
+        "hs_sweeps": dict(bytes=warps * segs * 32 * flow_px,
+                          flops=warps * sweeps * 17 * flow_px),
+        # RGBA inputs once (4 B/px), pano uchar4 write, overlap crops + flows + weights
+        "canvas_balance": dict(bytes=4 * in_px + 4 * P + sum((8 + 16 + 4) * n for n in o)),
         # uchar4 pano read, RGB + mask write
         "tone": dict(bytes=8 * P),
+        "_coarse_px": coarse_px,
     }
-    return model
 
 
 def load_peaks():
@@ -196,11 +205,16 @@ def run_b200(args, rank, world, local_rank):
     import torch
 
     import paper_2308_09209_b200 as pb
-    from paper_2308_09209_b200 import _abi
+    from paper_2308_09209_b200 import _abi, sharding
 
     lib = _abi.load()
     torch.cuda.set_device(local_rank)
+    dev = f"cuda:{local_rank}"
     wl = WORKLOADS[args.config]
+    # streams: one per GPU (weak scaling) unless a fixed stream count is set
+    total_streams = args.total_streams if args.total_streams else world * args.streams_per_gpu
+    my_streams = sharding.stream_assignment(total_streams, world, rank)
+    ns = len(my_streams)
     sc = build_scene(wl, seed=1 + rank)
     cfg = sc.config()
     cfg.device = local_rank
@@ -209,6 +223,7 @@ def run_b200(args, rank, world, local_rank):
     threads = max(1, cpu_cores() // max(1, world))
     frame_bytes = wl["width"] * wl["height"] * 3
     # pre-render F frame sets, stage them in pinned host memory and in HBM
+    # (shared read-only by this rank's streams)
     host_sets, dev_sets = [], []
     for t in range(F):
         hs, ds = [], []
@@ -223,81 +238,88 @@ def run_b200(args, rank, world, local_rank):
         host_sets.append((C.c_void_p * nv)(*hs))
         dev_sets.append((C.c_void_p * nv)(*ds))
     first = [pb.Frame(np.zeros((wl["height"], wl["width"], 3), np.uint8)) for _ in range(nv)]
-    state = pb.initialize(cfg, first)
-    h = state.handle
+    states = [pb.initialize(cfg, first) for _ in range(ns)]
+    state = states[0]
+    hs_ = [st.handle for st in states]
     P = state.canvas_width * state.canvas_height
     out_rgb = lib.stitch_b200_host_alloc(P * 3)
     out_mask = lib.stitch_b200_host_alloc(P)
-    stream = torch.cuda.ExternalStream(lib.stitch_b200_stream(h), device=local_rank)
+    cstreams = [torch.cuda.ExternalStream(lib.stitch_b200_stream(h), device=local_rank)
+                for h in hs_]
+    main = torch.cuda.current_stream()
     launches = state.launches_per_frame()
 
     def barrier():
         if world > 1:
             torch.distributed.barrier()
 
-    def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local_rank}")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        return float(t.item())
+    def step_all(i):
+        for j, h in enumerate(hs_):
+            pb.pipeline.check(lib.stitch_b200_process_device(h, dev_sets[(i + j) % F], None))
 
     clocks = ClockSampler(local_rank)
     clocks.start()
     # ---- warm-up ----
     for i in range(args.warmup):
-        pb.pipeline.check(lib.stitch_b200_process_device(h, dev_sets[i % F], None))
-    pb.pipeline.check(lib.stitch_b200_synchronize(h))
-    # ---- timed: device-resident inputs ----
+        step_all(i)
+    torch.cuda.synchronize()
+    # ---- timed: device-resident inputs; all streams of this rank ----
     barrier()
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     clocks.active = True
-    e0.record(stream)
+    e0.record(main)
+    for cs in cstreams:
+        cs.wait_event(e0)
     for i in range(args.steps):
-        pb.pipeline.check(lib.stitch_b200_process_device(h, dev_sets[i % F], None))
-    e1.record(stream)
+        step_all(i)
+    for cs in cstreams:
+        ev = torch.cuda.Event()
+        ev.record(cs)
+        main.wait_event(ev)
+    e1.record(main)
     torch.cuda.synchronize()
     clocks.active = False
     barrier()
-    elapsed_ms = e0.elapsed_time(e1)
-    max_ms = max_over_ranks(elapsed_ms)
-    ms_per_step = max_ms / args.steps
-    value = world * args.steps / (max_ms / 1e3)
+    elapsed_s = e0.elapsed_time(e1) / 1e3
+    max_s = sharding.max_over_ranks(elapsed_s, dev)
+    frames_total = sharding.sum_over_ranks(ns * args.steps, dev)
+    value = frames_total / max_s
+    ms_per_step = max_s * 1e3 / args.steps
 
-    # ---- per-step latency distribution (p50) ----
-    lat = []
+    # ---- per-frame latency distribution of one stream (p50) ----
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(min(args.steps, 200))]
     for i, (a, b) in enumerate(evs):
-        a.record(stream)
-        pb.pipeline.check(lib.stitch_b200_process_device(h, dev_sets[i % F], None))
-        b.record(stream)
+        a.record(cstreams[0])
+        pb.pipeline.check(lib.stitch_b200_process_device(hs_[0], dev_sets[i % F], None))
+        b.record(cstreams[0])
     torch.cuda.synchronize()
-    lat = [a.elapsed_time(b) for a, b in evs]
-    p50 = statistics.median(lat)
+    p50 = statistics.median(a.elapsed_time(b) for a, b in evs)
 
     # ---- e2e: reference-facing C-ABI call with pinned host buffers ----
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
     for i in range(min(args.warmup, 3)):
-        pb.pipeline.check(lib.stitch_b200_process(h, host_sets[i % F], out_rgb, out_mask, None))
+        pb.pipeline.check(lib.stitch_b200_process(hs_[0], host_sets[i % F], out_rgb, out_mask,
+                                                  None))
     barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for i in range(e2e_steps):
-        pb.pipeline.check(lib.stitch_b200_process(h, host_sets[i % F], out_rgb, out_mask, None))
-    e2e_s = max_over_ranks(time.perf_counter() - t0)
+        pb.pipeline.check(lib.stitch_b200_process(hs_[0], host_sets[i % F], out_rgb, out_mask,
+                                                  None))
+    e2e_s = sharding.max_over_ranks(time.perf_counter() - t0, dev)
     e2e_value = world * e2e_steps / e2e_s
 
-    # ---- per-kernel profile (eager, CUDA events around each launch) ----
+    # ---- per-kernel profile (eager plan, CUDA events around each launch) ----
     n_ops = 4096
     kinds = (C.c_int * n_ops)()
     ms = (C.c_float * n_ops)()
     per_kind = {}
     prof_frames = 5
     for i in range(prof_frames):
-        n = lib.stitch_b200_profile_frame(h, dev_sets[i % F], n_ops, kinds, ms)
+        n = lib.stitch_b200_profile_frame(hs_[0], dev_sets[i % F], n_ops, kinds, ms)
         if n < 0:
             pb.pipeline.check(-n)
         for j in range(min(n, n_ops)):
@@ -310,6 +332,8 @@ def run_b200(args, rank, world, local_rank):
     peak, peak_kind = load_peaks()
     model = kernel_model(state, wl)
     total_kernel_ms = sum(v[0] for v in per_kind.values())
+    clk = clocks.summary()
+    fp32_peak = 148 * 128 * (clk.get("sm_mhz") or 1965.0) * 1e6 / 1e12  # add/mul, no FMA
     kernels = {}
     for name, (t_ms, count) in sorted(per_kind.items(), key=lambda kv: -kv[1][0]):
         mdl = model.get(name, {})
@@ -320,7 +344,8 @@ def run_b200(args, rank, world, local_rank):
             k["hbm_gbs"] = round(mdl["bytes"] / (t_ms * 1e-3) / 1e9, 1)
             k["hbm_frac"] = round(k["hbm_gbs"] / peak, 4)
         if "flops" in mdl and t_ms > 0:
-            k["fp32_gflops"] = round(mdl["flops"] / (t_ms * 1e-3) / 1e9, 1)
+            k["fp32_tflops"] = round(mdl["flops"] / (t_ms * 1e-3) / 1e12, 3)
+            k["fp32_frac"] = round(k["fp32_tflops"] / fp32_peak, 4)
         kernels[name] = k
     dominant = max(per_kind, key=lambda n: per_kind[n][0])
     dk = kernels[dominant]
@@ -330,37 +355,48 @@ def run_b200(args, rank, world, local_rank):
             traffic = json.load(f).get(dominant)
     except Exception:
         pass
-    roofline = {"kernel": dominant, "bound": "hbm",
-                "achieved": dk.get("hbm_gbs"), "peak": peak, "unit": "GB/s",
-                "frac": dk.get("hbm_frac"), "traffic": traffic,
-                "peak_source": peak_kind,
-                "alg_bytes_per_launch": (model[dominant]["bytes"] / max(1, dk["launches_per_frame"])
-                                         if dominant in model else None)}
-    hbm_kernels = {n: kernels[n] for n in ("canvas", "tone", "crop_warp", "pair_stats")
+    launches_dom = max(1, dk["launches_per_frame"])
+    roofline = {"kernel": dominant, "bound": "hbm", "achieved": dk.get("hbm_gbs"), "peak": peak,
+                "unit": "GB/s", "frac": dk.get("hbm_frac"), "traffic": traffic,
+                "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                "alg_bytes_per_launch": (model[dominant]["bytes"] / launches_dom
+                                         if dominant in model else None),
+                "note": ("the dominant kernel is FP32-issue/SMEM bound (bit-exact unfused "
+                         "Jacobi), see roofline_fp32; HBM-streaming kernels in hbm_kernels")}
+    roofline_fp32 = None
+    if "fp32_tflops" in dk:
+        roofline_fp32 = {"kernel": dominant, "bound": "fp32 (add/mul issue, FMA not allowed)",
+                         "achieved": dk["fp32_tflops"], "peak": round(fp32_peak, 2),
+                         "unit": "TFLOP/s", "frac": dk["fp32_frac"]}
+    hbm_kernels = {n: kernels[n] for n in ("tone", "expand_rgba", "canvas_balance", "crop_warp",
+                                           "pair_color", "flow_prepare", "hs_linearize")
                    if n in kernels}
 
     result = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
-        "p50_ms_per_frame": round(p50, 4), "higher_is_better": True, "scaling": "weak",
+        "p50_ms_per_frame": round(p50, 4), "higher_is_better": True,
+        "scaling": "strong" if args.total_streams else "weak",
         "vs_baseline": None, "dtype": "u8 (fp64 warp, fp32 flow)",
-        "data": "synthetic (procedural plane scene, SynthScene restatement; seeds 1..N)",
+        "data": "synthetic (procedural plane scene, SynthScene restatement; seed 1+rank)",
         "config": {"workload": wl["desc"], "config_key": args.config, "cameras": nv,
                    "camera_size": [wl["width"], wl["height"]],
                    "canvas": [state.canvas_width, state.canvas_height],
                    "pairs": [list(p.bounds) for p in state.pairs],
-                   "streams_per_gpu": 1, "parallelism": f"stream-sharded x{world}",
+                   "streams_total": int(total_streams), "streams_this_rank": ns,
+                   "parallelism": f"independent streams sharded over {world} GPU(s), no collective",
                    "l2": (f"inputs cycle over {F} pre-rendered frame sets "
                           f"({F * nv * frame_bytes / 1e6:.0f} MB > 126 MB L2)")},
         "e2e": {"value": round(e2e_value, 2), "unit": UNIT,
                 "h2d_bytes_per_step": nv * frame_bytes, "d2h_bytes_per_step": P * 4,
-                "steps": e2e_steps},
-        "gpu_launches": launches * args.steps,
+                "steps": e2e_steps, "streams": 1},
+        "gpu_launches": launches * args.steps * ns,
         "kernels_per_frame": launches,
         "roofline": roofline,
+        "roofline_fp32": roofline_fp32,
         "hbm_kernels": hbm_kernels,
         "kernels": kernels,
-        "clocks": clocks.summary(),
+        "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(args, wl, sample_seconds=args.cpu_seconds)
@@ -445,6 +481,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--frame-sets", type=int, default=16)
+    ap.add_argument("--streams-per-gpu", type=int, default=1)
+    ap.add_argument("--total-streams", type=int, default=0,
+                    help="fixed stream count sharded over the ranks (config c5: 64)")
     ap.add_argument("--e2e-steps", type=int, default=200)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-budget-s", type=float, default=120.0)

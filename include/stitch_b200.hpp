@@ -1,0 +1,355 @@
+// stitch_b200.hpp -- C++ mirror of the reference pipeline API over the C ABI.
+//
+// Same names, argument meaning and error behaviour as
+//   /root/reference/proj/include/stitch/pipeline.hpp:17-92   (StitchConfig,
+//       PipelineState, initialize, process_frame, run_sequence)
+//   /root/reference/proj/include/stitch/report.hpp:11-58     (Stage, FrameReport,
+//       RunReport)
+//   /root/reference/proj/include/stitch/types.hpp:9-62       (ErrorCode,
+//       StitchError, Region)
+//   /root/reference/proj/include/stitch/frame.hpp:17-57      (Frame)
+// with Eigen types replaced by std::array so the header has no third-party
+// dependency.  Header-only: everything crosses into libstitch_b200.so through
+// the extern "C" entry points of stitch_b200.h, so the C++ ABI of the caller
+// never has to match the library's.  Errors surface as StitchError, like the
+// reference; stage failures inside a frame degrade (identity matrix, zero
+// flow, unbalanced frame) and are reported, never thrown.
+#pragma once
+
+#include <array>
+#include <chrono>
+#include <cstdint>
+#include <functional>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "stitch_b200.h"
+
+namespace stitch_b200 {
+
+// ---- types.hpp ----
+enum class ErrorCode {
+  EmptyRegion,
+  EmptyHistogram,
+  RankDeficient,
+  RegionTooSmall,
+  InsufficientMatches,
+  NoConsensus,
+  ShapeMismatch,
+  NoOverlap,
+  SingularHomography,
+  DegeneratePose,
+  EmptyProjection,
+  MissingState,
+  TooSmall,
+  ConfigError,
+  ConfigurationError,
+  InputMismatch,
+  IoError,
+  // B200-side failures (no reference counterpart)
+  DeviceError,
+  Unsupported,
+};
+
+class StitchError : public std::runtime_error {
+ public:
+  StitchError(ErrorCode code, std::string message)
+      : std::runtime_error(std::move(message)), code_(code) {}
+  ErrorCode code() const noexcept { return code_; }
+
+ private:
+  ErrorCode code_;
+};
+
+inline void check(int status) {
+  if (status == STITCH_B200_OK) return;
+  ErrorCode code = ErrorCode::DeviceError;
+  if (status >= 1 && status <= 17)
+    code = static_cast<ErrorCode>(status - 1);
+  else if (status == STITCH_B200_Unsupported)
+    code = ErrorCode::Unsupported;
+  throw StitchError(code, stitch_b200_last_error());
+}
+
+struct Region {
+  int x0 = 0, y0 = 0, x1 = 0, y1 = 0;
+  int width() const { return x1 - x0; }
+  int height() const { return y1 - y0; }
+  bool empty() const { return x1 <= x0 || y1 <= y0; }
+};
+
+// ---- frame.hpp ----
+struct Frame {
+  int width = 0;
+  int height = 0;
+  std::vector<std::uint8_t> data;  // width*height*3, R,G,B interleaved
+  std::vector<std::uint8_t> mask;  // empty, or width*height 0/1
+
+  Frame() = default;
+  Frame(int w, int h, std::uint8_t fill = 0)
+      : width(w), height(h), data(static_cast<std::size_t>(w) * h * 3, fill) {}
+  bool has_mask() const { return !mask.empty(); }
+  std::size_t pixel_count() const { return static_cast<std::size_t>(width) * height; }
+};
+
+// ---- geometry.hpp / color_balance.hpp / flow.hpp ----
+struct CameraIntrinsics {
+  double fx = 1.0, fy = 1.0, cx = 0.0, cy = 0.0;
+};
+
+struct CameraExtrinsics {
+  std::array<double, 9> rotation{1, 0, 0, 0, 1, 0, 0, 0, 1};  // row-major world -> camera
+  std::array<double, 3> translation{0, 0, 0};
+};
+
+struct BalanceConfig {
+  double lambda = 0.05;
+  double gamma_dark = 1.5;
+  double gamma_bright = 1.5;
+  int target_black = 0;
+  int target_white = 255;
+};
+
+struct FlowOptions {
+  int levels = 4;
+  int iterations = 50;
+  double smoothness = 15.0;
+  int threads = 1;  // accepted for source compatibility; the GPU ignores it
+};
+
+enum class FuseWeighting { OwnWeightOnOwnFlow, CrossWeightOnOwnFlow };
+
+// ---- pipeline.hpp ----
+struct ViewSetup {
+  std::string dir;
+  CameraIntrinsics intrinsics;
+  CameraExtrinsics extrinsics;
+};
+
+struct RefineOptions {
+  // Feature refinement is init-only and outside the per-frame B200 path;
+  // refined maps enter through the C ABI's stitch_b200_create().  The mirror
+  // defaults it off (the reference defaults it on) and initialize() throws
+  // Unsupported when it is requested.
+  bool enabled = false;
+  double margin = 0.15;
+  int ransac_iters = 500;
+  double inlier_px = 2.0;
+  double detect_threshold = 2e-4;
+  double match_ratio = 0.8;
+  int rerefine_every = 0;
+};
+
+struct StitchConfig {
+  std::vector<ViewSetup> views;
+  int reference = 0;
+  BalanceConfig balance;
+  FlowOptions flow;
+  RefineOptions refine;
+  int threads = 1;
+  std::uint64_t seed = 0;
+  int window_capacity = 3;
+  FuseWeighting fuse_weighting = FuseWeighting::OwnWeightOnOwnFlow;
+  std::string scene_id = "scene";
+  int topology = 0;  // extension: 0 auto (star <= 3 views, chain beyond), 1 star, 2 chain
+  int device = 0;
+};
+
+// ---- report.hpp ----
+enum class Stage : int { GeometricWarping = 0, ColorCorrection = 1, LocalWarping = 2, ImageBlending = 3 };
+constexpr int kStageCount = 4;
+
+struct StageTimes {
+  std::array<double, kStageCount> seconds{};
+  double total() const {
+    double t = 0.0;
+    for (double s : seconds) t += s;
+    return t;
+  }
+  double& operator[](Stage s) { return seconds[static_cast<int>(s)]; }
+  double operator[](Stage s) const { return seconds[static_cast<int>(s)]; }
+  StageTimes& operator+=(const StageTimes& o) {
+    for (int i = 0; i < kStageCount; ++i) seconds[i] += o.seconds[i];
+    return *this;
+  }
+};
+
+using Matrix3d = std::array<double, 9>;  // row-major
+
+struct FrameReport {
+  long frame_index = 0;
+  StageTimes times;
+  std::vector<Matrix3d> color_matrices;
+  std::vector<bool> rank_deficient;
+  std::array<int, 3> threshold_m1{};
+  std::array<int, 3> threshold_m2{};
+};
+
+struct RunReport {
+  std::string scene_id;
+  int threads = 1;
+  long frames = 0;
+  StageTimes totals;
+  double wall_seconds = 0.0;
+  std::vector<FrameReport> per_frame;
+  std::string config_hash;
+  bool refine_warning = false;
+  double fps() const { return wall_seconds > 0 ? frames / wall_seconds : 0.0; }
+};
+
+// Device-resident pipeline state: owns one stitch_b200_ctx.
+class PipelineState {
+ public:
+  PipelineState() = default;
+  explicit PipelineState(stitch_b200_ctx* ctx, StitchConfig cfg)
+      : ctx_(ctx, &stitch_b200_destroy), config(std::move(cfg)) {}
+  stitch_b200_ctx* handle() const { return ctx_.get(); }
+  int canvas_width() const {
+    int w = 0;
+    stitch_b200_canvas(ctx_.get(), &w, nullptr, nullptr, nullptr);
+    return w;
+  }
+  int canvas_height() const {
+    int h = 0;
+    stitch_b200_canvas(ctx_.get(), nullptr, &h, nullptr, nullptr);
+    return h;
+  }
+  int n_pairs() const { return stitch_b200_n_pairs(ctx_.get()); }
+
+ private:
+  std::unique_ptr<stitch_b200_ctx, void (*)(stitch_b200_ctx*)> ctx_{nullptr, &stitch_b200_destroy};
+
+ public:
+  StitchConfig config;
+  long frame_counter = 0;
+};
+
+struct ProcessResult {
+  Frame panorama;
+  FrameReport report;
+};
+
+inline stitch_b200_config to_c(const StitchConfig& config, const std::vector<Frame>& first) {
+  stitch_b200_config c;
+  stitch_b200_config_defaults(&c);
+  c.n_views = static_cast<int>(config.views.size());
+  c.reference = config.reference;
+  for (std::size_t v = 0; v < config.views.size() && v < STITCH_B200_MAX_VIEWS; ++v) {
+    c.width[v] = first[v].width;
+    c.height[v] = first[v].height;
+    const ViewSetup& s = config.views[v];
+    c.cams[v].fx = s.intrinsics.fx;
+    c.cams[v].fy = s.intrinsics.fy;
+    c.cams[v].cx = s.intrinsics.cx;
+    c.cams[v].cy = s.intrinsics.cy;
+    for (int i = 0; i < 9; ++i) c.cams[v].rotation[i] = s.extrinsics.rotation[i];
+    for (int i = 0; i < 3; ++i) c.cams[v].translation[i] = s.extrinsics.translation[i];
+  }
+  c.lambda = config.balance.lambda;
+  c.gamma_dark = config.balance.gamma_dark;
+  c.gamma_bright = config.balance.gamma_bright;
+  c.target_black = config.balance.target_black;
+  c.target_white = config.balance.target_white;
+  c.flow_levels = config.flow.levels;
+  c.flow_iterations = config.flow.iterations;
+  c.smoothness = config.flow.smoothness;
+  c.window_capacity = config.window_capacity;
+  c.fuse_weighting = config.fuse_weighting == FuseWeighting::CrossWeightOnOwnFlow ? 1 : 0;
+  c.topology = config.topology;
+  c.refine_enabled = config.refine.enabled ? 1 : 0;
+  return c;
+}
+
+// initialize (pipeline.hpp:73-74), refinement off.
+inline PipelineState initialize(const StitchConfig& config, const std::vector<Frame>& first_frames) {
+  const int n = static_cast<int>(config.views.size());
+  if (n < 2 || n > STITCH_B200_MAX_VIEWS)
+    throw StitchError(ErrorCode::ConfigurationError, "pipeline supports 2 to 16 views");
+  if (first_frames.size() != config.views.size())
+    throw StitchError(ErrorCode::ConfigurationError, "frame count does not match configured views");
+  stitch_b200_config c = to_c(config, first_frames);
+  stitch_b200_ctx* ctx = nullptr;
+  check(stitch_b200_initialize(&c, config.device, &ctx));
+  return PipelineState(ctx, config);
+}
+
+// process_frame (pipeline.hpp:79-80): one frame through warp -> 3D-M colour
+// -> flow -> blend -> balance on the GPU.
+inline ProcessResult process_frame(PipelineState& state, const std::vector<Frame>& frames) {
+  if (frames.size() != state.config.views.size())
+    throw StitchError(ErrorCode::ConfigurationError, "frame count does not match configured views");
+  std::vector<const std::uint8_t*> ptrs;
+  for (const Frame& f : frames) {
+    if (f.data.size() != f.pixel_count() * 3)
+      throw StitchError(ErrorCode::InputMismatch, "frame data must be width*height*3 bytes");
+    ptrs.push_back(f.data.data());
+  }
+  ProcessResult result;
+  Frame& pano = result.panorama;
+  pano.width = state.canvas_width();
+  pano.height = state.canvas_height();
+  pano.data.resize(pano.pixel_count() * 3);
+  pano.mask.resize(pano.pixel_count());
+  stitch_b200_report r;
+  check(stitch_b200_process(state.handle(), ptrs.data(), pano.data.data(), pano.mask.data(), &r));
+  FrameReport& rep = result.report;
+  rep.frame_index = static_cast<long>(r.frame_index);
+  for (int i = 0; i < kStageCount; ++i) rep.times.seconds[i] = r.stage_ms[i] * 1e-3;
+  for (int k = 0; k < r.n_pairs; ++k) {
+    Matrix3d m;
+    for (int i = 0; i < 9; ++i) m[i] = r.color_matrices[k][i];
+    rep.color_matrices.push_back(m);
+    rep.rank_deficient.push_back(r.rank_deficient[k] != 0);
+  }
+  for (int c = 0; c < 3; ++c) {
+    rep.threshold_m1[c] = r.threshold_m1[c];
+    rep.threshold_m2[c] = r.threshold_m2[c];
+  }
+  ++state.frame_counter;
+  return result;
+}
+
+struct RunResult {
+  std::vector<Frame> panoramas;
+  RunReport report;
+};
+
+// run_sequence (pipeline.hpp:90-92, pipeline.cpp:362-420); periodic
+// re-refinement is not part of the B200 path.
+inline RunResult run_sequence(const StitchConfig& config, const std::vector<std::vector<Frame>>& views,
+                              const std::function<void(long, const Frame&)>& sink = {}) {
+  if (views.size() != config.views.size())
+    throw StitchError(ErrorCode::ConfigurationError, "stream count does not match configured views");
+  const std::size_t frames = views.front().size();
+  for (const auto& s : views)
+    if (s.size() != frames)
+      throw StitchError(ErrorCode::ConfigurationError, "streams must have equal length");
+  if (frames == 0) throw StitchError(ErrorCode::ConfigurationError, "empty input streams");
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<Frame> first;
+  for (const auto& s : views) first.push_back(s[0]);
+  PipelineState state = initialize(config, first);
+  RunResult result;
+  result.report.scene_id = config.scene_id;
+  result.report.threads = config.threads;
+  result.report.frames = static_cast<long>(frames);
+  for (std::size_t t = 0; t < frames; ++t) {
+    std::vector<Frame> set;
+    for (const auto& s : views) set.push_back(s[t]);
+    ProcessResult pr = process_frame(state, set);
+    result.report.totals += pr.report.times;
+    result.report.per_frame.push_back(pr.report);
+    if (sink)
+      sink(static_cast<long>(t), pr.panorama);
+    else
+      result.panoramas.push_back(std::move(pr.panorama));
+  }
+  result.report.wall_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return result;
+}
+
+}  // namespace stitch_b200

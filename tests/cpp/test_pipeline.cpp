@@ -1,0 +1,194 @@
+// C++ parity test of the reference-signature API (include/stitch_b200.hpp)
+// against the CPU oracle, written in the style of the reference's doctest
+// suites (proj/tests/test_imaging.cpp).  Needs a B200; run by
+// tests/test_cpp_api.py (gpu marker).
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "../../oracle/stitch_oracle.h"
+#include "stitch_b200.hpp"
+
+static int g_failures = 0, g_checks = 0;
+#define CHECK(cond)                                                      \
+  do {                                                                   \
+    ++g_checks;                                                          \
+    if (!(cond)) {                                                       \
+      ++g_failures;                                                      \
+      std::fprintf(stderr, "%s:%d: CHECK failed: %s\n", __FILE__, __LINE__, #cond); \
+    }                                                                    \
+  } while (0)
+#define TEST_CASE(name) static void name()
+
+using namespace stitch_b200;
+
+static stitch_b200_synth* make_scene(int views, int w, int h) {
+  stitch_b200_synth_spec spec;
+  stitch_b200_synth_defaults(&spec);
+  spec.views = views;
+  spec.width = w;
+  spec.height = h;
+  spec.frames = 4;
+  spec.n_casts = views;
+  for (int v = 0; v < views; ++v) {
+    spec.color_casts[v][0] = 1.0 - 0.05 * v;
+    spec.color_casts[v][1] = 1.0;
+    spec.color_casts[v][2] = 1.0 + 0.04 * v;
+  }
+  spec.object_enabled = 1;
+  spec.object_velocity[0] = 3.0;
+  stitch_b200_synth* s = nullptr;
+  check(stitch_b200_synth_create(&spec, &s));
+  return s;
+}
+
+static StitchConfig config_of(stitch_b200_synth* s, stitch_b200_config& c) {
+  check(stitch_b200_synth_config(s, &c));
+  StitchConfig cfg;
+  cfg.reference = c.reference;
+  for (int v = 0; v < c.n_views; ++v) {
+    ViewSetup vs;
+    vs.intrinsics = {c.cams[v].fx, c.cams[v].fy, c.cams[v].cx, c.cams[v].cy};
+    for (int i = 0; i < 9; ++i) vs.extrinsics.rotation[i] = c.cams[v].rotation[i];
+    for (int i = 0; i < 3; ++i) vs.extrinsics.translation[i] = c.cams[v].translation[i];
+    cfg.views.push_back(vs);
+  }
+  return cfg;
+}
+
+static so_config oracle_config(const stitch_b200_config& c) {
+  so_config o{};
+  o.n_views = c.n_views;
+  o.reference = c.reference;
+  for (int v = 0; v < c.n_views; ++v) {
+    o.width[v] = c.width[v];
+    o.height[v] = c.height[v];
+    o.cams[v].fx = c.cams[v].fx;
+    o.cams[v].fy = c.cams[v].fy;
+    o.cams[v].cx = c.cams[v].cx;
+    o.cams[v].cy = c.cams[v].cy;
+    for (int i = 0; i < 9; ++i) o.cams[v].rotation[i] = c.cams[v].rotation[i];
+    for (int i = 0; i < 3; ++i) o.cams[v].translation[i] = c.cams[v].translation[i];
+  }
+  o.lambda = 0.05;
+  o.gamma_dark = o.gamma_bright = 1.5;
+  o.target_black = 0;
+  o.target_white = 255;
+  o.flow_levels = 4;
+  o.flow_iterations = 50;
+  o.smoothness = 15.0;
+  o.window_capacity = 3;
+  o.threads = 4;
+  return o;
+}
+
+TEST_CASE(process_frame_matches_oracle) {
+  for (int views : {2, 3}) {
+    stitch_b200_synth* s = make_scene(views, 320, 240);
+    stitch_b200_config c;
+    StitchConfig cfg = config_of(s, c);
+    std::vector<std::vector<Frame>> streams(views);
+    for (int v = 0; v < views; ++v)
+      for (int t = 0; t < 4; ++t) {
+        Frame f(320, 240);
+        check(stitch_b200_synth_render(s, v, t, f.data.data(), 4));
+        streams[v].push_back(f);
+      }
+    std::vector<Frame> first;
+    for (int v = 0; v < views; ++v) first.push_back(streams[v][0]);
+    PipelineState state = initialize(cfg, first);
+    so_config oc = oracle_config(c);
+    int err = 0;
+    so_state* os = so_initialize(&oc, &err);
+    CHECK(os != nullptr);
+    for (int t = 0; t < 4; ++t) {
+      std::vector<Frame> set;
+      std::vector<so_frame> oset;
+      for (int v = 0; v < views; ++v) {
+        set.push_back(streams[v][t]);
+        oset.push_back(so_frame{320, 240, streams[v][t].data.data(), nullptr});
+      }
+      ProcessResult r = process_frame(state, set);
+      so_frame pano{};
+      so_report rep{};
+      CHECK(so_process_frame(os, oset.data(), &pano, &rep) == SO_OK);
+      CHECK(pano.width == r.panorama.width && pano.height == r.panorama.height);
+      int maxdiff = 0;
+      bool mask_same = true;
+      for (std::size_t i = 0; i < r.panorama.pixel_count(); ++i) {
+        mask_same = mask_same && (r.panorama.mask[i] != 0) == (pano.mask[i] != 0);
+        for (int ch = 0; ch < 3; ++ch)
+          maxdiff = std::max(maxdiff, std::abs(int(r.panorama.data[3 * i + ch]) - int(pano.data[3 * i + ch])));
+      }
+      CHECK(mask_same);
+      CHECK(maxdiff == 0);
+      CHECK(static_cast<int>(r.report.color_matrices.size()) == rep.n_pairs);
+      for (int k = 0; k < rep.n_pairs; ++k)
+        for (int i = 0; i < 9; ++i) CHECK(r.report.color_matrices[k][i] == rep.m[k][i]);
+      for (int ch = 0; ch < 3; ++ch) {
+        CHECK(r.report.threshold_m1[ch] == rep.threshold_m1[ch]);
+        CHECK(r.report.threshold_m2[ch] == rep.threshold_m2[ch]);
+      }
+      so_free_frame(&pano);
+    }
+    so_destroy(os);
+    stitch_b200_synth_destroy(s);
+  }
+}
+
+TEST_CASE(errors_surface_as_stitch_error) {
+  StitchConfig cfg;
+  cfg.views.resize(1);
+  bool threw = false;
+  try {
+    initialize(cfg, std::vector<Frame>(1, Frame(16, 16)));
+  } catch (const StitchError& e) {
+    threw = e.code() == ErrorCode::ConfigurationError;
+  }
+  CHECK(threw);
+  stitch_b200_synth* s = make_scene(2, 64, 48);
+  stitch_b200_config c;
+  StitchConfig ok = config_of(s, c);
+  ok.refine.enabled = true;
+  threw = false;
+  try {
+    initialize(ok, std::vector<Frame>(2, Frame(64, 48)));
+  } catch (const StitchError& e) {
+    threw = e.code() == ErrorCode::Unsupported;
+  }
+  CHECK(threw);
+  stitch_b200_synth_destroy(s);
+}
+
+TEST_CASE(run_sequence_reports_every_frame) {
+  stitch_b200_synth* s = make_scene(2, 160, 120);
+  stitch_b200_config c;
+  StitchConfig cfg = config_of(s, c);
+  std::vector<std::vector<Frame>> streams(2);
+  for (int v = 0; v < 2; ++v)
+    for (int t = 0; t < 3; ++t) {
+      Frame f(160, 120);
+      check(stitch_b200_synth_render(s, v, t, f.data.data(), 4));
+      streams[v].push_back(f);
+    }
+  long seen = 0;
+  RunResult r = run_sequence(cfg, streams, [&](long t, const Frame& p) {
+    CHECK(t == seen);
+    CHECK(p.width > 0);
+    ++seen;
+  });
+  CHECK(seen == 3);
+  CHECK(r.report.frames == 3);
+  CHECK(r.report.per_frame.size() == 3);
+  CHECK(r.panoramas.empty());
+  stitch_b200_synth_destroy(s);
+}
+
+int main() {
+  process_frame_matches_oracle();
+  errors_surface_as_stitch_error();
+  run_sequence_reports_every_frame();
+  std::printf("%d checks, %d failures\n", g_checks, g_failures);
+  return g_failures ? 1 : 0;
+}
