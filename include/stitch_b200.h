@@ -171,6 +171,22 @@ int stitch_b200_process(stitch_b200_ctx* ctx, const uint8_t* const* frames,
                         uint8_t* pano_rgb, uint8_t* pano_mask,
                         stitch_b200_report* report);
 
+/* Pipelined variant of stitch_b200_process: enqueue one frame (upload of the
+ * host frames on the context's copy stream, the frame on the compute stream,
+ * download of the panorama into pano_rgb / pano_mask on a second copy
+ * stream) and return a ticket without waiting.  Two frames can be in flight:
+ * frame t+1's upload and frame t-1's download overlap frame t's kernels.
+ * Frames are processed in submission order (the temporal state is
+ * sequential).  Host buffers must stay valid until the ticket is waited and
+ * should be pinned (stitch_b200_host_alloc) for the copies to be
+ * asynchronous.  stitch_b200_wait blocks until the ticket's panorama is in
+ * host memory and fills its report; a ticket older than the last 8 frames
+ * is reported as MissingState. */
+int stitch_b200_submit(stitch_b200_ctx* ctx, const uint8_t* const* frames,
+                       uint8_t* pano_rgb, uint8_t* pano_mask, long long* ticket);
+int stitch_b200_wait(stitch_b200_ctx* ctx, long long ticket,
+                     stitch_b200_report* report);
+
 /* Device-resident variant: frames[v] are device pointers; outputs stay in
  * the context (see stitch_b200_device_pano).  Enqueued on the context's
  * stream; returns without synchronising unless report != NULL. */

@@ -85,6 +85,9 @@ SYMBOLS = [
     ("stitch_b200_get_inv_map", C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_double)]),
     ("stitch_b200_process", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.c_void_p, C.c_void_p,
                                       C.POINTER(Report)]),
+    ("stitch_b200_submit", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.c_void_p, C.c_void_p,
+                                     C.POINTER(C.c_longlong)]),
+    ("stitch_b200_wait", C.c_int, [C.c_void_p, C.c_longlong, C.POINTER(Report)]),
     ("stitch_b200_process_device", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p),
                                              C.POINTER(Report)]),
     ("stitch_b200_device_pano", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p),

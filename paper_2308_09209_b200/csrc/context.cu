@@ -59,8 +59,11 @@ struct Ctx {
   std::uint8_t* d_frames[kMaxViews] = {};
   size_t frame_bytes[kMaxViews] = {};
   uchar4* d_pano = nullptr;
-  std::uint8_t* d_out_rgb = nullptr;
-  std::uint8_t* d_out_mask = nullptr;
+  // two pipeline slots: inputs, outputs, graph, stage events, report
+  static constexpr int kSlots = 2;
+  std::uint8_t* d_in[kSlots][kMaxViews] = {};
+  std::uint8_t* d_out_rgb[kSlots] = {};
+  std::uint8_t* d_out_mask[kSlots] = {};
   long long n_px = 0;
   int max_crop_px = 0;
   int max_crop_w = 0, max_crop_h = 0;
@@ -73,26 +76,40 @@ struct Ctx {
   PrepTask* d_hp = nullptr;
   PyrTask* d_pyr = nullptr;
   int* d_lists = nullptr;
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph[kSlots] = {};
+  cudaGraphExec_t exec[kSlots] = {};
   int launches = 0;
-  cudaEvent_t ev[6] = {};
+  cudaEvent_t ev[kSlots][6] = {};
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t h2d_done[kSlots] = {}, comp_done[kSlots] = {}, d2h_done[kSlots] = {};
+  long long seq = 0;                       // frames submitted (any API)
+  long long slot_ticket[kSlots] = {-1, -1};  // ticket occupying each slot
+  bool slot_pending[kSlots] = {false, false};
+  std::vector<std::pair<long long, stitch_b200_report>> done_reports;
+  int last_slot = 0;
   // pinned ring for device-frame pointer tables
   const std::uint8_t** h_ptr_ring = nullptr;
   cudaEvent_t ring_ev[16] = {};
   int ring_pos = 0;
-  DevReport* h_report = nullptr;
-  bool frames_are_own = true;
+  DevReport* h_report = nullptr;  // one per slot (pinned)
   std::vector<int> pair_levels;
   float* d_zero = nullptr;
   CanvasParams cparams{};
 
   ~Ctx() {
     if (stream) cudaStreamSynchronize(stream);
-    if (exec) cudaGraphExecDestroy(exec);
-    if (graph) cudaGraphDestroy(graph);
-    for (auto& e : ev)
-      if (e) cudaEventDestroy(e);
+    if (h2d) cudaStreamSynchronize(h2d);
+    if (d2h) cudaStreamSynchronize(d2h);
+    for (int s = 0; s < kSlots; ++s) {
+      if (exec[s]) cudaGraphExecDestroy(exec[s]);
+      if (graph[s]) cudaGraphDestroy(graph[s]);
+      for (auto& e : ev[s])
+        if (e) cudaEventDestroy(e);
+      for (cudaEvent_t e : {h2d_done[s], comp_done[s], d2h_done[s]})
+        if (e) cudaEventDestroy(e);
+    }
+    if (h2d) cudaStreamDestroy(h2d);
+    if (d2h) cudaStreamDestroy(d2h);
     for (auto& e : ring_ev)
       if (e) cudaEventDestroy(e);
     for (void* p : allocs) cudaFree(p);
@@ -199,7 +216,7 @@ void fill_views(Geometry& g, const stitch_b200_init* in) {
   }
 }
 
-int enqueue_op(Ctx* ctx, const Op& op, cudaStream_t s) {
+int enqueue_op(Ctx* ctx, const Op& op, cudaStream_t s, int slot = 0) {
   const Geometry& g = ctx->hg;
   switch (op.kind) {
     case OP_EXPAND:
@@ -229,7 +246,7 @@ int enqueue_op(Ctx* ctx, const Op& op, cudaStream_t s) {
       launch_canvas(ctx->cparams, ctx->dg, ctx->dst, ctx->d_pano, ctx->num_sms, s);
       return 1;
     case OP_TONE:
-      launch_tone(ctx->dst, ctx->d_pano, ctx->n_px, ctx->d_out_rgb, ctx->d_out_mask, s);
+      launch_tone(ctx->dst, ctx->d_pano, ctx->n_px, ctx->d_out_rgb[slot], ctx->d_out_mask[slot], s);
       return 1;
     default:
       return 0;
@@ -282,14 +299,18 @@ int build_context(const stitch_b200_init* in, int device,
     ctx->frame_bytes[v] = static_cast<size_t>(in->view_width[v]) * in->view_height[v] * 3;
     CUDA_TRY(ctx->alloc(&ctx->d_frames[v], ctx->frame_bytes[v]));
     g.frames[v] = ctx->d_frames[v];
+    ctx->d_in[0][v] = ctx->d_frames[v];
+    for (int sl = 1; sl < Ctx::kSlots; ++sl) CUDA_TRY(ctx->alloc(&ctx->d_in[sl][v], ctx->frame_bytes[v]));
     const long long vpx = static_cast<long long>(in->view_width[v]) * in->view_height[v];
     CUDA_TRY(ctx->alloc(&g.rgba[v], vpx));
     ctx->max_view_px = std::max(ctx->max_view_px, vpx);
   }
   ctx->n_px = static_cast<long long>(g.canvas_w) * g.canvas_h;
   CUDA_TRY(ctx->alloc(&ctx->d_pano, static_cast<size_t>(ctx->n_px) + 4));
-  CUDA_TRY(ctx->alloc(&ctx->d_out_rgb, static_cast<size_t>(ctx->n_px) * 3 + 16));
-  CUDA_TRY(ctx->alloc(&ctx->d_out_mask, static_cast<size_t>(ctx->n_px) + 16));
+  for (int sl = 0; sl < Ctx::kSlots; ++sl) {
+    CUDA_TRY(ctx->alloc(&ctx->d_out_rgb[sl], static_cast<size_t>(ctx->n_px) * 3 + 16));
+    CUDA_TRY(ctx->alloc(&ctx->d_out_mask[sl], static_cast<size_t>(ctx->n_px) + 16));
+  }
 
   ctx->sweeps = std::max(1, in->flow_iterations / 5);  // flow.cpp:79-80
   ctx->alpha2 = static_cast<float>(in->smoothness * in->smoothness);
@@ -578,28 +599,39 @@ int build_context(const stitch_b200_init* in, int device,
   }
   CUDA_TRY(prepare_hs(ctx->sweeps));
   for (int j = 1; j <= ctx->sweeps; ++j) CUDA_TRY(prepare_hs(j));
-  for (auto& e : ctx->ev) CUDA_TRY(cudaEventCreate(&e));
+  for (int sl = 0; sl < Ctx::kSlots; ++sl) {
+    for (auto& e : ctx->ev[sl]) CUDA_TRY(cudaEventCreate(&e));
+    CUDA_TRY(cudaEventCreateWithFlags(&ctx->h2d_done[sl], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&ctx->comp_done[sl], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&ctx->d2h_done[sl], cudaEventDisableTiming));
+  }
+  CUDA_TRY(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
   for (auto& e : ctx->ring_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_ptr_ring),
                          sizeof(void*) * kMaxViews * 16, cudaHostAllocDefault));
-  CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_report), sizeof(DevReport),
-                         cudaHostAllocDefault));
+  CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_report),
+                         sizeof(DevReport) * Ctx::kSlots, cudaHostAllocDefault));
 
-  // ---- capture the per-frame launch sequence once ----
+  // ---- capture the per-frame launch sequence once per pipeline slot ----
   cudaStream_t s = ctx->stream;
-  CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   int launches = 0;
-  for (const Op& op : plan) {
-    if (op.kind == OP_EVENT)
-      cudaEventRecordWithFlags(ctx->ev[op.event], s, cudaEventRecordExternal);
-    else
-      launches += enqueue_op(ctx.get(), op, s);
+  for (int sl = 0; sl < Ctx::kSlots; ++sl) {
+    CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    launches = 0;
+    for (const Op& op : plan) {
+      if (op.kind == OP_EVENT)
+        cudaEventRecordWithFlags(ctx->ev[sl][op.event], s, cudaEventRecordExternal);
+      else
+        launches += enqueue_op(ctx.get(), op, s, sl);
+    }
+    cudaError_t cap_err = cudaStreamEndCapture(s, &ctx->graph[sl]);
+    if (cap_err != cudaSuccess)
+      return fail(STITCH_B200_CudaError,
+                  std::string("graph capture: ") + cudaGetErrorString(cap_err));
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaGraphInstantiate(&ctx->exec[sl], ctx->graph[sl], 0));
   }
-  cudaError_t cap_err = cudaStreamEndCapture(s, &ctx->graph);
-  if (cap_err != cudaSuccess)
-    return fail(STITCH_B200_CudaError, std::string("graph capture: ") + cudaGetErrorString(cap_err));
-  CUDA_TRY(cudaGetLastError());
-  CUDA_TRY(cudaGraphInstantiate(&ctx->exec, ctx->graph, 0));
   ctx->launches = launches;
   out = std::move(ctx);
   return STITCH_B200_OK;
@@ -617,8 +649,8 @@ int set_frame_pointers(Ctx* ctx, const std::uint8_t* const* ptrs) {
   return STITCH_B200_OK;
 }
 
-void fill_report(Ctx* ctx, stitch_b200_report* r) {
-  const DevReport& d = *ctx->h_report;
+void fill_report(Ctx* ctx, int slot, stitch_b200_report* r) {
+  const DevReport& d = ctx->h_report[slot];
   std::memset(r, 0, sizeof(*r));
   r->frame_index = d.frame_index;
   r->n_pairs = ctx->hg.n_pairs;
@@ -632,15 +664,94 @@ void fill_report(Ctx* ctx, stitch_b200_report* r) {
   }
   r->balanced = d.balanced;
   float t01 = 0, t12 = 0, t23 = 0, t34 = 0, t45 = 0;
-  cudaEventElapsedTime(&t01, ctx->ev[0], ctx->ev[1]);
-  cudaEventElapsedTime(&t12, ctx->ev[1], ctx->ev[2]);
-  cudaEventElapsedTime(&t23, ctx->ev[2], ctx->ev[3]);
-  cudaEventElapsedTime(&t34, ctx->ev[3], ctx->ev[4]);
-  cudaEventElapsedTime(&t45, ctx->ev[4], ctx->ev[5]);
+  cudaEvent_t* ev = ctx->ev[slot];
+  cudaEventElapsedTime(&t01, ev[0], ev[1]);
+  cudaEventElapsedTime(&t12, ev[1], ev[2]);
+  cudaEventElapsedTime(&t23, ev[2], ev[3]);
+  cudaEventElapsedTime(&t34, ev[3], ev[4]);
+  cudaEventElapsedTime(&t45, ev[4], ev[5]);
   r->stage_ms[0] = t01;
   r->stage_ms[1] = t12 + t45;
   r->stage_ms[2] = t23;
   r->stage_ms[3] = t34;
+}
+
+// Retire the frame occupying `slot` (if any): wait for its download and keep
+// its report for a later stitch_b200_wait().
+int retire_slot(Ctx* ctx, int slot) {
+  if (!ctx->slot_pending[slot]) return STITCH_B200_OK;
+  CUDA_TRY(cudaEventSynchronize(ctx->d2h_done[slot]));
+  stitch_b200_report r;
+  fill_report(ctx, slot, &r);
+  ctx->done_reports.emplace_back(ctx->slot_ticket[slot], r);
+  if (ctx->done_reports.size() > 8) ctx->done_reports.erase(ctx->done_reports.begin());
+  ctx->slot_pending[slot] = false;
+  return STITCH_B200_OK;
+}
+
+// Compute-stream part of one frame on `slot`: wait until the slot's
+// previous download has drained, point the frame table at `dev_in`, launch
+// the slot's graph, fetch the report, mark completion.
+int enqueue_frame(Ctx* ctx, int slot, const std::uint8_t* const* dev_in) {
+  CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->d2h_done[slot], 0));
+  int rc = set_frame_pointers(ctx, dev_in);
+  if (rc) return rc;
+  CUDA_TRY(cudaGraphLaunch(ctx->exec[slot], ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(&ctx->h_report[slot], &ctx->dst->report, sizeof(DevReport),
+                           cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaEventRecord(ctx->comp_done[slot], ctx->stream));
+  ctx->last_slot = slot;
+  return STITCH_B200_OK;
+}
+
+// Host-buffer frame: H2D on the upload stream, compute, D2H on the download
+// stream; returns the frame's ticket.
+int submit_host(Ctx* ctx, const std::uint8_t* const* frames, std::uint8_t* pano_rgb,
+                std::uint8_t* pano_mask, long long* ticket) {
+  const int slot = static_cast<int>(ctx->seq % Ctx::kSlots);
+  int rc = retire_slot(ctx, slot);
+  if (rc) return rc;
+  for (int v = 0; v < ctx->hg.n_views; ++v)
+    if (!frames[v]) return fail(STITCH_B200_InputMismatch, "null frame");
+  // the slot's inputs were last read by the frame two submissions ago
+  CUDA_TRY(cudaStreamWaitEvent(ctx->h2d, ctx->comp_done[slot], 0));
+  for (int v = 0; v < ctx->hg.n_views; ++v)
+    CUDA_TRY(cudaMemcpyAsync(ctx->d_in[slot][v], frames[v], ctx->frame_bytes[v],
+                             cudaMemcpyHostToDevice, ctx->h2d));
+  CUDA_TRY(cudaEventRecord(ctx->h2d_done[slot], ctx->h2d));
+  CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->h2d_done[slot], 0));
+  const std::uint8_t* in[kMaxViews];
+  for (int v = 0; v < ctx->hg.n_views; ++v) in[v] = ctx->d_in[slot][v];
+  rc = enqueue_frame(ctx, slot, in);
+  if (rc) return rc;
+  CUDA_TRY(cudaStreamWaitEvent(ctx->d2h, ctx->comp_done[slot], 0));
+  if (pano_rgb)
+    CUDA_TRY(cudaMemcpyAsync(pano_rgb, ctx->d_out_rgb[slot], static_cast<size_t>(ctx->n_px) * 3,
+                             cudaMemcpyDeviceToHost, ctx->d2h));
+  if (pano_mask)
+    CUDA_TRY(cudaMemcpyAsync(pano_mask, ctx->d_out_mask[slot], static_cast<size_t>(ctx->n_px),
+                             cudaMemcpyDeviceToHost, ctx->d2h));
+  CUDA_TRY(cudaEventRecord(ctx->d2h_done[slot], ctx->d2h));
+  ctx->slot_ticket[slot] = ctx->seq;
+  ctx->slot_pending[slot] = true;
+  if (ticket) *ticket = ctx->seq;
+  ++ctx->seq;
+  return STITCH_B200_OK;
+}
+
+int wait_ticket(Ctx* ctx, long long ticket, stitch_b200_report* report) {
+  for (auto& d : ctx->done_reports)
+    if (d.first == ticket) {
+      if (report) *report = d.second;
+      return STITCH_B200_OK;
+    }
+  for (int sl = 0; sl < Ctx::kSlots; ++sl)
+    if (ctx->slot_pending[sl] && ctx->slot_ticket[sl] == ticket) {
+      int rc = retire_slot(ctx, sl);
+      if (rc) return rc;
+      return wait_ticket(ctx, ticket, report);
+    }
+  return fail(STITCH_B200_MissingState, "unknown or expired ticket");
 }
 
 }  // namespace
@@ -776,7 +887,9 @@ int stitch_b200_update_geometry(stitch_b200_ctx* h, const stitch_b200_init* init
   std::unique_ptr<Ctx> fresh;
   int rc = build_context(init, ctx->device, nullptr, fresh);
   if (rc) return rc;
+  CUDA_TRY(cudaStreamSynchronize(ctx->h2d));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->d2h));
   // carry windows, threshold history and the frame counter over
   // (pipeline.cpp:399-405)
   CUDA_TRY(cudaMemcpy(&fresh->dst->windows, &ctx->dst->windows, sizeof(DevState::windows),
@@ -830,46 +943,40 @@ int stitch_b200_process(stitch_b200_ctx* h, const uint8_t* const* frames, uint8_
                         uint8_t* pano_mask, stitch_b200_report* report) {
   Ctx* ctx = h->c.get();
   CUDA_TRY(cudaSetDevice(ctx->device));
-  cudaStream_t s = ctx->stream;
-  for (int v = 0; v < ctx->hg.n_views; ++v) {
-    if (!frames[v]) return fail(STITCH_B200_InputMismatch, "null frame");
-    CUDA_TRY(cudaMemcpyAsync(ctx->d_frames[v], frames[v], ctx->frame_bytes[v],
-                             cudaMemcpyHostToDevice, s));
-  }
-  if (!ctx->frames_are_own) {
-    const std::uint8_t* own[kMaxViews];
-    for (int v = 0; v < ctx->hg.n_views; ++v) own[v] = ctx->d_frames[v];
-    int rc = set_frame_pointers(ctx, own);
-    if (rc) return rc;
-    ctx->frames_are_own = true;
-  }
-  CUDA_TRY(cudaGraphLaunch(ctx->exec, s));
-  if (pano_rgb)
-    CUDA_TRY(cudaMemcpyAsync(pano_rgb, ctx->d_out_rgb, static_cast<size_t>(ctx->n_px) * 3,
-                             cudaMemcpyDeviceToHost, s));
-  if (pano_mask)
-    CUDA_TRY(cudaMemcpyAsync(pano_mask, ctx->d_out_mask, static_cast<size_t>(ctx->n_px),
-                             cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaMemcpyAsync(ctx->h_report, &ctx->dst->report, sizeof(DevReport),
-                           cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaStreamSynchronize(s));
-  if (report) fill_report(ctx, report);
-  return STITCH_B200_OK;
+  long long ticket = -1;
+  int rc = submit_host(ctx, frames, pano_rgb, pano_mask, &ticket);
+  if (rc) return rc;
+  stitch_b200_report tmp;
+  return wait_ticket(ctx, ticket, report ? report : &tmp);
+}
+
+int stitch_b200_submit(stitch_b200_ctx* h, const uint8_t* const* frames, uint8_t* pano_rgb,
+                       uint8_t* pano_mask, long long* ticket) {
+  Ctx* ctx = h->c.get();
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  return submit_host(ctx, frames, pano_rgb, pano_mask, ticket);
+}
+
+int stitch_b200_wait(stitch_b200_ctx* h, long long ticket, stitch_b200_report* report) {
+  Ctx* ctx = h->c.get();
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  stitch_b200_report tmp;
+  return wait_ticket(ctx, ticket, report ? report : &tmp);
 }
 
 int stitch_b200_process_device(stitch_b200_ctx* h, const uint8_t* const* dev_frames,
                                stitch_b200_report* report) {
   Ctx* ctx = h->c.get();
   CUDA_TRY(cudaSetDevice(ctx->device));
-  int rc = set_frame_pointers(ctx, dev_frames);
+  const int slot = static_cast<int>(ctx->seq % Ctx::kSlots);
+  int rc = retire_slot(ctx, slot);
   if (rc) return rc;
-  ctx->frames_are_own = false;
-  CUDA_TRY(cudaGraphLaunch(ctx->exec, ctx->stream));
+  rc = enqueue_frame(ctx, slot, dev_frames);
+  if (rc) return rc;
+  ++ctx->seq;
   if (report) {
-    CUDA_TRY(cudaMemcpyAsync(ctx->h_report, &ctx->dst->report, sizeof(DevReport),
-                             cudaMemcpyDeviceToHost, ctx->stream));
-    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    fill_report(ctx, report);
+    CUDA_TRY(cudaEventSynchronize(ctx->comp_done[slot]));
+    fill_report(ctx, slot, report);
   }
   return STITCH_B200_OK;
 }
@@ -878,9 +985,16 @@ int stitch_b200_profile_frame(stitch_b200_ctx* h, const uint8_t* const* dev_fram
                               int* kinds, float* ms) {
   Ctx* ctx = h->c.get();
   CUDA_TRY(cudaSetDevice(ctx->device));
+  // eager run on slot 0 after draining the pipeline
+  for (int sl = 0; sl < Ctx::kSlots; ++sl) {
+    int rc = retire_slot(ctx, sl);
+    if (rc) return -rc;
+  }
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->d2h));
   int rc = set_frame_pointers(ctx, dev_frames);
   if (rc) return -rc;
-  ctx->frames_are_own = false;
+  ctx->last_slot = 0;
   std::vector<cudaEvent_t> evs;
   std::vector<int> ks;
   cudaStream_t s = ctx->stream;
@@ -919,8 +1033,8 @@ int stitch_b200_profile_frame(stitch_b200_ctx* h, const uint8_t* const* dev_fram
 
 int stitch_b200_device_pano(const stitch_b200_ctx* h, uint8_t** rgb, uint8_t** mask) {
   const Ctx* ctx = h->c.get();
-  if (rgb) *rgb = ctx->d_out_rgb;
-  if (mask) *mask = ctx->d_out_mask;
+  if (rgb) *rgb = ctx->d_out_rgb[ctx->last_slot];
+  if (mask) *mask = ctx->d_out_mask[ctx->last_slot];
   return STITCH_B200_OK;
 }
 
@@ -928,7 +1042,9 @@ void* stitch_b200_stream(const stitch_b200_ctx* h) { return h->c->stream; }
 
 int stitch_b200_synchronize(stitch_b200_ctx* h) {
   Ctx* ctx = h->c.get();
+  CUDA_TRY(cudaStreamSynchronize(ctx->h2d));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->d2h));
   return STITCH_B200_OK;
 }
 
