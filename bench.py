@@ -180,8 +180,9 @@ def kernel_model(state, wl, sweeps=10, warps=5):
         # per segment and pixel: state (8) + constants (16) read, state (8) written
         "hs_sweeps": dict(bytes=warps * segs * 32 * flow_px,
                           flops=warps * sweeps * 17 * flow_px),
-        # RGBA inputs once (4 B/px), pano uchar4 write, overlap crops + flows + weights
-        "canvas_balance": dict(bytes=4 * in_px + 4 * P + sum((8 + 16 + 4) * n for n in o)),
+        # per canvas pixel one RGBA source pixel read + uchar4 write; overlap pixels add
+        # raw crops (8) + corrected crop samples (8) + flows (16) + weight (4)
+        "canvas_balance": dict(bytes=8 * P + 36 * sum(o)),
         # uchar4 pano read, RGB + mask write
         "tone": dict(bytes=8 * P),
         "_coarse_px": coarse_px,

@@ -243,10 +243,19 @@ __device__ void balance_lut(const Geometry* __restrict__ g, DevState* __restrict
   }
 }
 
+__device__ __forceinline__ bool in_rect(const CanvasPair& p, int x, int y) {
+  return x >= p.x0 && x < p.x0 + p.w && y >= p.y0 && y < p.y0 + p.h;
+}
+
+// mode 0: every canvas pixel; mode 1: pixels outside every pair's bounds
+// (independent of the flow, runs concurrently with it); mode 2: pixels inside
+// some pair's bounds (after the flow).  blocks_total: CTAs of all canvas
+// launches of the frame (the last one builds the balance LUT).
 __global__ void __launch_bounds__(256, 3) k_canvas(const __grid_constant__ CanvasParams P,
                                                    const Geometry* __restrict__ g,
                                                    DevState* __restrict__ st,
-                                                   uchar4* __restrict__ pano) {
+                                                   uchar4* __restrict__ pano, int mode,
+                                                   unsigned blocks_total) {
   __shared__ unsigned int hist[3][256];
   __shared__ double mview[kMaxViews][9];
   __shared__ bool last;
@@ -262,12 +271,41 @@ __global__ void __launch_bounds__(256, 3) k_canvas(const __grid_constant__ Canva
   const CanvasView& vr = P.views[ref];
   const int np = P.np;
   const int tiles_x = (cw + 63) / 64;
-  const int ntiles = tiles_x * ((ch + 3) / 4);
+  int ntiles = tiles_x * ((ch + 3) / 4);
+  if (mode == 2) {
+    ntiles = 0;
+    for (int k = 0; k < np; ++k) ntiles += ((P.pairs[k].w + 63) / 64) * ((P.pairs[k].h + 3) / 4);
+  }
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int ty = tile / tiles_x;
-    const int x = (tile - ty * tiles_x) * 64 + threadIdx.x % 64;
-    const int y = ty * 4 + threadIdx.x / 64;
-    if (x >= cw || y >= ch) continue;
+    int x, y;
+    if (mode != 2) {
+      const int ty = tile / tiles_x;
+      x = (tile - ty * tiles_x) * 64 + threadIdx.x % 64;
+      y = ty * 4 + threadIdx.x / 64;
+      if (x >= cw || y >= ch) continue;
+      if (mode == 1) {
+        bool inside = false;
+        for (int k = 0; k < np; ++k) inside = inside || in_rect(P.pairs[k], x, y);
+        if (inside) continue;
+      }
+    } else {
+      int t = tile, k = 0;
+      for (; k < np; ++k) {
+        const int n = ((P.pairs[k].w + 63) / 64) * ((P.pairs[k].h + 3) / 4);
+        if (t < n) break;
+        t -= n;
+      }
+      const CanvasPair& pk = P.pairs[k];
+      const int tx = (pk.w + 63) / 64;
+      const int tyy = t / tx;
+      const int dx = (t - tyy * tx) * 64 + threadIdx.x % 64, dy = tyy * 4 + threadIdx.x / 64;
+      if (dx >= pk.w || dy >= pk.h) continue;
+      x = pk.x0 + dx;
+      y = pk.y0 + dy;
+      bool earlier = false;  // each pixel once: owned by the first rect containing it
+      for (int k2 = 0; k2 < k; ++k2) earlier = earlier || in_rect(P.pairs[k2], x, y);
+      if (earlier) continue;
+    }
     const long long idx = static_cast<long long>(y) * cw + x;
     const double X = static_cast<double>(x) + P.offx;
     const double Y = static_cast<double>(y) + P.offy;
@@ -319,7 +357,7 @@ __global__ void __launch_bounds__(256, 3) k_canvas(const __grid_constant__ Canva
       if (hist[c][i]) atomicAdd(&st->pano_hist[c][i], hist[c][i]);
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(&st->canvas_done, 1u) == gridDim.x - 1;
+  if (threadIdx.x == 0) last = atomicAdd(&st->canvas_done, 1u) == blocks_total - 1;
   __syncthreads();
   if (!last) return;
   __threadfence();
@@ -459,11 +497,22 @@ void launch_crop_warp(const CanvasParams& P, int max_w, int max_h, cudaStream_t 
   k_crop_warp<<<grid, dim3(64, 4), 0, s>>>(P);
 }
 
+static int canvas_blocks(const CanvasParams& P, int mode, int num_sms) {
+  long long tiles = 0;
+  if (mode != 2) {
+    tiles = static_cast<long long>((P.cw + 63) / 64) * ((P.ch + 3) / 4);
+  } else {
+    for (int k = 0; k < P.np; ++k) tiles += ((P.pairs[k].w + 63) / 64) * ((P.pairs[k].h + 3) / 4);
+  }
+  const long long b = std::min<long long>(static_cast<long long>(num_sms) * 4, tiles);
+  return static_cast<int>(b < 1 ? 1 : b);
+}
+
 void launch_canvas(const CanvasParams& P, const Geometry* g, DevState* st, uchar4* pano,
-                   int num_sms, cudaStream_t s) {
-  const long long tiles = static_cast<long long>((P.cw + 63) / 64) * ((P.ch + 3) / 4);
-  const int blocks = static_cast<int>(std::min<long long>(static_cast<long long>(num_sms) * 4, tiles));
-  k_canvas<<<blocks < 1 ? 1 : blocks, 256, 0, s>>>(P, g, st, pano);
+                   int num_sms, int mode, cudaStream_t s) {
+  const unsigned total = mode == 0 ? canvas_blocks(P, 0, num_sms)
+                                   : canvas_blocks(P, 1, num_sms) + canvas_blocks(P, 2, num_sms);
+  k_canvas<<<canvas_blocks(P, mode, num_sms), 256, 0, s>>>(P, g, st, pano, mode, total);
 }
 
 void launch_tone(const DevState* st, const uchar4* pano, long long n_px, std::uint8_t* out_rgb,

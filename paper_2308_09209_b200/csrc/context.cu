@@ -34,7 +34,7 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 enum OpKind { OP_EXPAND, OP_CROP, OP_STATS, OP_SOLVE, OP_PREP, OP_PYR, OP_HSPREP, OP_HS, OP_CANVAS,
-              OP_BALANCE, OP_TONE, OP_EVENT };
+              OP_BALANCE, OP_TONE, OP_EVENT, OP_CANVAS_OUT };
 
 struct Op {
   OpKind kind;
@@ -80,7 +80,8 @@ struct Ctx {
   cudaGraphExec_t exec[kSlots] = {};
   int launches = 0;
   cudaEvent_t ev[kSlots][6] = {};
-  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaStream_t h2d = nullptr, d2h = nullptr, side = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   cudaEvent_t h2d_done[kSlots] = {}, comp_done[kSlots] = {}, d2h_done[kSlots] = {};
   long long seq = 0;                       // frames submitted (any API)
   long long slot_ticket[kSlots] = {-1, -1};  // ticket occupying each slot
@@ -110,6 +111,9 @@ struct Ctx {
     }
     if (h2d) cudaStreamDestroy(h2d);
     if (d2h) cudaStreamDestroy(d2h);
+    if (side) cudaStreamDestroy(side);
+    if (fork_ev) cudaEventDestroy(fork_ev);
+    if (join_ev) cudaEventDestroy(join_ev);
     for (auto& e : ring_ev)
       if (e) cudaEventDestroy(e);
     for (void* p : allocs) cudaFree(p);
@@ -243,7 +247,10 @@ int enqueue_op(Ctx* ctx, const Op& op, cudaStream_t s, int slot = 0) {
       launch_hs_iter(ctx->d_hs + op.offset, op.count, op.max_w, op.max_h, op.sweeps, s);
       return 1;
     case OP_CANVAS:
-      launch_canvas(ctx->cparams, ctx->dg, ctx->dst, ctx->d_pano, ctx->num_sms, s);
+      launch_canvas(ctx->cparams, ctx->dg, ctx->dst, ctx->d_pano, ctx->num_sms, 0, s);
+      return 1;
+    case OP_CANVAS_OUT:
+      launch_canvas(ctx->cparams, ctx->dg, ctx->dst, ctx->d_pano, ctx->num_sms, 1, s);
       return 1;
     case OP_TONE:
       launch_tone(ctx->dst, ctx->d_pano, ctx->n_px, ctx->d_out_rgb[slot], ctx->d_out_mask[slot], s);
@@ -428,6 +435,7 @@ int build_context(const stitch_b200_init* in, int device,
   }
   plan.push_back({OP_PREP});
   plan.push_back({OP_EVENT, 0, 0, 0, 0, 0, 2});
+
   for (int l = 1; l < Lmax; ++l) {
     Op op{OP_PYR};
     op.offset = static_cast<int>(pyr_table.size());
@@ -606,6 +614,9 @@ int build_context(const stitch_b200_init* in, int device,
     CUDA_TRY(cudaEventCreateWithFlags(&ctx->d2h_done[sl], cudaEventDisableTiming));
   }
   CUDA_TRY(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
   CUDA_TRY(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
   for (auto& e : ctx->ring_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_ptr_ring),
@@ -619,11 +630,23 @@ int build_context(const stitch_b200_init* in, int device,
   for (int sl = 0; sl < Ctx::kSlots; ++sl) {
     CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     launches = 0;
+    bool forked = false;
     for (const Op& op : plan) {
-      if (op.kind == OP_EVENT)
+      if (op.kind == OP_EVENT) {
         cudaEventRecordWithFlags(ctx->ev[sl][op.event], s, cudaEventRecordExternal);
-      else
+      } else if (op.kind == OP_CANVAS_OUT) {
+        cudaEventRecord(ctx->fork_ev, s);
+        cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0);
+        launches += enqueue_op(ctx.get(), op, ctx->side, sl);
+        cudaEventRecord(ctx->join_ev, ctx->side);
+        forked = true;
+      } else {
+        if (op.kind == OP_CANVAS && forked) {
+          cudaStreamWaitEvent(s, ctx->join_ev, 0);
+          forked = false;
+        }
         launches += enqueue_op(ctx.get(), op, s, sl);
+      }
     }
     cudaError_t cap_err = cudaStreamEndCapture(s, &ctx->graph[sl]);
     if (cap_err != cudaSuccess)
