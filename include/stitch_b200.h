@@ -79,8 +79,15 @@ typedef struct {
   double smoothness;
   int window_capacity; /* 1..3 (clamped like TransferWindow) */
   int fuse_weighting;  /* 0 = own (OwnWeightOnOwnFlow), 1 = cross */
-  int topology;        /* 0 = auto (star <= 3 views, chain beyond), 1 star, 2 chain */
+  int topology;        /* 0 = auto (star <= 3 views, chain beyond), 1 star, 2 chain,
+                          3 ring chain (360 degree rigs) */
   int refine_enabled;  /* must be 0 */
+  /* Extension (not in the reference, which is planar only): 0 = planar
+   * canvas (the reference's world plane), 1 = cylindrical 360-degree canvas
+   * around the reference camera, cyl_focal pixels per radian (0: the
+   * reference camera's fx).  Cameras must share their centre. */
+  int projection;
+  double cyl_focal;
 } stitch_b200_config;
 
 /* Fill a config with the reference defaults (pipeline.hpp:23-44,
@@ -114,6 +121,13 @@ typedef struct {
   int flow_levels, flow_iterations;
   double smoothness;
   int fuse_weighting;
+  /* 0: planar -- inv_maps are the inverse homographies applied to
+   * (x + offset_x, y + offset_y, 1).  1: cylindrical extension -- inv_maps
+   * are K_v R_v R_ref^T applied to (sin t, h, cos t) with
+   * t = (x + offset_x) / cyl_focal, h = (y + offset_y) / cyl_focal; a
+   * sample is valid only in front of the camera. */
+  int projection;
+  double cyl_focal;
 } stitch_b200_init;
 
 /* FrameReport (report.hpp:38-45) without the host-only fields. */
@@ -263,7 +277,9 @@ typedef struct {
   double perturb_focal_scale, perturb_principal_px;
   /* 0 = auto: the reference yaw rig (synth.cpp:60-152) for <= 3 views, the
    * strip rig (N-view extension: small toe-in yaw, baseline solved for the
-   * overlap fraction) beyond. 1 = yaw, 2 = strip. */
+   * overlap fraction) beyond. 1 = yaw, 2 = strip, 3 = ring (extension:
+   * cameras sharing one centre, yaw step 2pi/N, focal chosen for the
+   * overlap fraction, textured cylinder scene, cylindrical canvas). */
   int rig;
   double strip_yaw; /* radians per view step for the strip rig */
 } stitch_b200_synth_spec;

@@ -53,7 +53,7 @@ class SoConfig(C.Structure):
                 ("flow_levels", C.c_int), ("flow_iterations", C.c_int),
                 ("smoothness", C.c_double), ("window_capacity", C.c_int),
                 ("fuse_weighting", C.c_int), ("topology", C.c_int), ("threads", C.c_int),
-                ("keep_debug", C.c_int)]
+                ("keep_debug", C.c_int), ("projection", C.c_int), ("cyl_focal", C.c_double)]
 
 
 class SoReport(C.Structure):
@@ -330,7 +330,8 @@ def blend_weights(mask_i, mask_j, region):
 # ---------------------------------------------------------------------------
 def make_config(n_views, reference, sizes, cams, *, lam=0.05, gamma_dark=1.5, gamma_bright=1.5,
                 target_black=0, target_white=255, levels=4, iterations=50, smoothness=15.0,
-                window=3, weighting=0, topology=0, threads=1, keep_debug=0) -> SoConfig:
+                window=3, weighting=0, topology=0, threads=1, keep_debug=0, projection=0,
+                cyl_focal=0.0) -> SoConfig:
     """cams: list of (fx, fy, cx, cy, R[9] row-major, t[3])."""
     c = SoConfig()
     c.n_views = n_views
@@ -352,6 +353,8 @@ def make_config(n_views, reference, sizes, cams, *, lam=0.05, gamma_dark=1.5, ga
     c.topology = topology
     c.threads = threads
     c.keep_debug = keep_debug
+    c.projection = projection
+    c.cyl_focal = cyl_focal
     return c
 
 

@@ -332,6 +332,40 @@ int so_warp_frame(const so_frame* src, const double inv[9], int cw, int ch,
   return SO_OK;
 }
 
+/* Warp over a lifted canvas (extension).  lsin == NULL: the reference's
+ * planar lift (x + offx, y + offy, 1), identical arithmetic to
+ * so_warp_frame since a*1.0 == a; otherwise the cylindrical lift
+ * (sin t[x], h[y], cos t[x]) and points behind the camera are invalid. */
+int so_warp_frame_lift(const so_frame* src, const double a[9], int cw, int ch,
+                       double offx, double offy, const double* lsin,
+                       const double* lcos, const double* lh, int threads,
+                       so_frame* out) {
+  if (!lsin) return so_warp_frame(src, a, cw, ch, offx, offy, threads, out);
+  frame_alloc(out, cw, ch, 1, 0);
+  int any = 0;
+#pragma omp parallel for schedule(static) num_threads(threads > 0 ? threads : 1) reduction(| : any)
+  for (int y = 0; y < ch; ++y) {
+    for (int x = 0; x < cw; ++x) {
+      const double L0 = lsin[x], L1 = lh[y], L2 = lcos[x];
+      const double sx0 = (a[0] * L0 + a[1] * L1) + a[2] * L2;
+      const double sy0 = (a[3] * L0 + a[4] * L1) + a[5] * L2;
+      const double sz0 = (a[6] * L0 + a[7] * L1) + a[8] * L2;
+      if (fabs(sz0) < 1e-12) continue;
+      if (!(sz0 > 0.0)) continue;
+      float rgb[3];
+      if (!so_sample_bilinear(src, sx0 / sz0, sy0 / sz0, rgb)) continue;
+      uint8_t* p = out->data + ((size_t)y * cw + x) * 3;
+      p[0] = so_quantize_channel(rgb[0]);
+      p[1] = so_quantize_channel(rgb[1]);
+      p[2] = so_quantize_channel(rgb[2]);
+      out->mask[(size_t)y * cw + x] = 1;
+      any = 1;
+    }
+  }
+  if (!any) return SO_EmptyProjection;
+  return SO_OK;
+}
+
 /* overlap_regions, geometry.cpp:85-117 (bounds only) */
 static int overlap_bounds(const so_frame* a, const so_frame* b, so_region* r) {
   if (a->width != b->width || a->height != b->height) return SO_ShapeMismatch;
@@ -1130,6 +1164,9 @@ struct so_state {
   so_config cfg;
   int canvas_w, canvas_h;
   double offx, offy;
+  double* lsin;  /* cylindrical lift tables (NULL: planar) */
+  double* lcos;
+  double* lh;
   double maps[SO_MAX_VIEWS][9];
   double inv[SO_MAX_VIEWS][9];
   so_region view_bbox[SO_MAX_VIEWS];
@@ -1154,8 +1191,23 @@ static int effective_topology(const so_config* c) {
  * the reference then by index, so a partner is always corrected first. */
 static void build_pairs(so_state* s) {
   const so_config* c = &s->cfg;
-  const int topo = effective_topology(c);
+  const int topo = (c->topology == 3 || (c->topology == 0 && c->projection == 1))
+                       ? 3 : effective_topology(c);
   s->n_pairs = 0;
+  if (topo == 3) {
+    /* ring chain: k = (v - ref) mod N, distance min(k, N - k), partner one
+     * step toward the reference (the k = N/2 view pairs with k - 1) */
+    const int n = c->n_views;
+    for (int d = 1; d <= n / 2; ++d)
+      for (int v = 0; v < n; ++v) {
+        const int k = ((v - c->reference) % n + n) % n;
+        if ((k < n - k ? k : n - k) != d) continue;
+        s->pairs[s->n_pairs].view = v;
+        s->pairs[s->n_pairs].partner = (k <= n / 2) ? (v - 1 + n) % n : (v + 1) % n;
+        s->n_pairs++;
+      }
+    return;
+  }
   if (topo == 1) {
     for (int v = 0; v < c->n_views; ++v) {
       if (v == c->reference) continue;
@@ -1189,6 +1241,56 @@ so_state* so_initialize(const so_config* cfg, int* err) {
   int wc = cfg->window_capacity;
   if (wc < 1) wc = 1;
   if (wc > 3) wc = 3;
+  if (cfg->projection == 1) {
+    /* cylindrical 360-degree canvas (extension): A_v = K_v R_v R_ref^T */
+    const double f = cfg->cyl_focal > 0.0 ? cfg->cyl_focal : cfg->cams[cfg->reference].fx;
+    s->cfg.cyl_focal = f;
+    double rref[9], rrefT[9];
+    memcpy(rref, cfg->cams[cfg->reference].rotation, sizeof(rref));
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) rrefT[i * 3 + j] = rref[j * 3 + i];
+    double hmin = DBL_MAX, hmax = -DBL_MAX;
+    for (int v = 0; v < cfg->n_views; ++v) {
+      const so_camera* c = &cfg->cams[v];
+      const double k[9] = {c->fx, 0, c->cx, 0, c->fy, c->cy, 0, 0, 1};
+      double kr[9], rT[9], m[9];
+      mul3(k, c->rotation, kr);
+      mul3(kr, rrefT, s->inv[v]);
+      for (int i = 0; i < 9; ++i) s->maps[v][i] = s->inv[v][i];
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) rT[i * 3 + j] = c->rotation[j * 3 + i];
+      mul3(rref, rT, m); /* camera v -> reference frame */
+      const int W = cfg->width[v], H = cfg->height[v];
+      for (int e2 = 0; e2 < 2; ++e2) {
+        const int count = e2 == 0 ? W : H;
+        for (int i = 0; i < count; ++i)
+          for (int side = 0; side < 2; ++side) {
+            const double px = e2 == 0 ? (double)i : (side ? W - 1.0 : 0.0);
+            const double py = e2 == 0 ? (side ? H - 1.0 : 0.0) : (double)i;
+            const double cx = (px - c->cx) / c->fx, cy = (py - c->cy) / c->fy;
+            const double rx = (m[0] * cx + m[1] * cy) + m[2];
+            const double ry = (m[3] * cx + m[4] * cy) + m[5];
+            const double rz = (m[6] * cx + m[7] * cy) + m[8];
+            const double hh = ry / sqrt(rx * rx + rz * rz);
+            hmin = fmin(hmin, hh);
+            hmax = fmax(hmax, hh);
+          }
+      }
+    }
+    s->canvas_w = (int)ceil(2.0 * M_PI * f);
+    s->offx = -floor(s->canvas_w / 2.0);
+    s->offy = floor(hmin * f);
+    s->canvas_h = (int)(ceil(hmax * f) - s->offy) + 1;
+    s->lsin = (double*)malloc(sizeof(double) * s->canvas_w);
+    s->lcos = (double*)malloc(sizeof(double) * s->canvas_w);
+    s->lh = (double*)malloc(sizeof(double) * s->canvas_h);
+    for (int x = 0; x < s->canvas_w; ++x) {
+      const double t = (x + s->offx) / f;
+      s->lsin[x] = sin(t);
+      s->lcos[x] = cos(t);
+    }
+    for (int y = 0; y < s->canvas_h; ++y) s->lh[y] = (y + s->offy) / f;
+  } else {
   double cam[SO_MAX_VIEWS][9];
   for (int v = 0; v < cfg->n_views; ++v) {
     int e = planar_homography(&cfg->cams[v], cam[v]);
@@ -1223,6 +1325,7 @@ so_state* so_initialize(const so_config* cfg, int* err) {
   s->offy = floor(min_y);
   s->canvas_w = (int)(ceil(max_x) - s->offx) + 1;
   s->canvas_h = (int)(ceil(max_y) - s->offy) + 1;
+  }
 
   build_pairs(s);
   for (int k = 0; k < s->n_pairs; ++k) {
@@ -1234,8 +1337,8 @@ so_state* so_initialize(const so_config* cfg, int* err) {
   for (int v = 0; v < cfg->n_views; ++v) {
     so_frame zero;
     frame_alloc(&zero, cfg->width[v], cfg->height[v], 0, 0);
-    int e = so_warp_frame(&zero, s->inv[v], s->canvas_w, s->canvas_h, s->offx,
-                          s->offy, cfg->threads, &warped[v]);
+    int e = so_warp_frame_lift(&zero, s->inv[v], s->canvas_w, s->canvas_h, s->offx,
+                               s->offy, s->lsin, s->lcos, s->lh, cfg->threads, &warped[v]);
     so_free_frame(&zero);
     if (e != SO_OK) {
       *err = e;
@@ -1279,6 +1382,9 @@ void so_destroy(so_state* s) {
       for (int c = 0; c < 2; ++c) free(s->dbg_flow[k][d][c]);
   }
   for (int v = 0; v < SO_MAX_VIEWS; ++v) so_free_frame(&s->dbg_warped[v]);
+  free(s->lsin);
+  free(s->lcos);
+  free(s->lh);
   free(s);
 }
 
@@ -1299,8 +1405,8 @@ int so_process_frame(so_state* s, const so_frame* frames, so_frame* pano_out,
   double t0 = now_seconds();
   so_frame warped[SO_MAX_VIEWS];
   for (int v = 0; v < nv; ++v) {
-    int e = so_warp_frame(&frames[v], s->inv[v], s->canvas_w, s->canvas_h,
-                          s->offx, s->offy, nt, &warped[v]);
+    int e = so_warp_frame_lift(&frames[v], s->inv[v], s->canvas_w, s->canvas_h,
+                               s->offx, s->offy, s->lsin, s->lcos, s->lh, nt, &warped[v]);
     if (e != SO_OK) {
       for (int u = 0; u <= v; ++u) so_free_frame(&warped[u]);
       return e;

@@ -91,9 +91,15 @@ typedef struct {
   double smoothness;
   int window_capacity;
   int fuse_weighting; /* 0 = own (OwnWeightOnOwnFlow), 1 = cross */
-  int topology;       /* 0 = auto (star <= 3 views, chain otherwise), 1 = star, 2 = chain */
+  int topology;       /* 0 = auto (star <= 3 views, chain otherwise), 1 = star, 2 = chain,
+                         3 = ring chain */
   int threads;
   int keep_debug;     /* keep raw warped views + flows of the last frame */
+  /* extension: 0 planar (the reference), 1 cylindrical 360-degree canvas
+   * (cameras share a centre; A_v = K_v R_v R_ref^T applied to
+   * (sin t, h, cos t); samples behind the camera are invalid) */
+  int projection;
+  double cyl_focal;   /* pixels per radian; 0 = reference fx */
 } so_config;
 
 typedef struct {
@@ -119,6 +125,12 @@ double so_det3(const double m[9]);
 /* ---- geometry ---- */
 int so_warp_frame(const so_frame* src, const double inv[9], int cw, int ch,
                   double offx, double offy, int threads, so_frame* out);
+/* generalised warp: lift = NULL -> planar (x+offx, y+offy, 1); else the
+ * cylindrical lift tables lsin[cw], lcos[cw], lh[ch] */
+int so_warp_frame_lift(const so_frame* src, const double a[9], int cw, int ch,
+                       double offx, double offy, const double* lsin,
+                       const double* lcos, const double* lh, int threads,
+                       so_frame* out);
 
 /* ---- color transfer ---- */
 int so_histogram_specification(const so_hist* src, const so_hist* ref,

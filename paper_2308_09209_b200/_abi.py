@@ -24,7 +24,8 @@ class Config(C.Structure):
                 ("target_black", C.c_int), ("target_white", C.c_int),
                 ("flow_levels", C.c_int), ("flow_iterations", C.c_int),
                 ("smoothness", C.c_double), ("window_capacity", C.c_int),
-                ("fuse_weighting", C.c_int), ("topology", C.c_int), ("refine_enabled", C.c_int)]
+                ("fuse_weighting", C.c_int), ("topology", C.c_int), ("refine_enabled", C.c_int),
+                ("projection", C.c_int), ("cyl_focal", C.c_double)]
 
 
 class Pair(C.Structure):
@@ -41,7 +42,8 @@ class Init(C.Structure):
                 ("lambda_", C.c_double), ("gamma_dark", C.c_double), ("gamma_bright", C.c_double),
                 ("target_black", C.c_int), ("target_white", C.c_int),
                 ("flow_levels", C.c_int), ("flow_iterations", C.c_int),
-                ("smoothness", C.c_double), ("fuse_weighting", C.c_int)]
+                ("smoothness", C.c_double), ("fuse_weighting", C.c_int),
+                ("projection", C.c_int), ("cyl_focal", C.c_double)]
 
 
 class Report(C.Structure):

@@ -53,13 +53,13 @@ __global__ void __launch_bounds__(256) k_expand_one(const std::uint8_t* __restri
 // (pipeline.cpp:310-311) evaluated directly on the bounds.
 // grid: (ceil(max_w/64), ceil(max_h/4), 2*n_pairs), block (64, 4)
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uchar4 warp_cv(const CanvasView& v, double X, double Y) {
+__device__ __forceinline__ uchar4 warp_cv(const CanvasView& v, Lift L, bool cyl) {
   ViewDesc d;
   d.width = v.w;
   d.height = v.h;
 #pragma unroll
   for (int i = 0; i < 9; ++i) d.inv[i] = v.inv[i];
-  return warp_sample(d, v.rgba, X, Y);
+  return warp_sample(d, v.rgba, L, cyl);
 }
 
 __global__ void __launch_bounds__(256) k_crop_warp(const __grid_constant__ CanvasParams P) {
@@ -70,9 +70,8 @@ __global__ void __launch_bounds__(256) k_crop_warp(const __grid_constant__ Canva
   const int dy = blockIdx.y * 4 + threadIdx.y;
   if (dx >= p.w || dy >= p.h) return;
   const int view = side ? p.partner : p.view;
-  const double X = static_cast<double>(p.x0 + dx) + P.offx;
-  const double Y = static_cast<double>(p.y0 + dy) + P.offy;
-  p.crop_raw[side][dy * p.w + dx] = warp_cv(P.views[view], X, Y);
+  p.crop_raw[side][dy * p.w + dx] =
+      warp_cv(P.views[view], canvas_lift(P, p.x0 + dx, p.y0 + dy), P.projection == 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -307,8 +306,8 @@ __global__ void __launch_bounds__(256, 3) k_canvas(const __grid_constant__ Canva
       if (earlier) continue;
     }
     const long long idx = static_cast<long long>(y) * cw + x;
-    const double X = static_cast<double>(x) + P.offx;
-    const double Y = static_cast<double>(y) + P.offy;
+    const Lift L = canvas_lift(P, x, y);
+    const bool cyl = P.projection == 1;
     uchar4 pv = make_uchar4(0, 0, 0, 0);
     if (x >= vr.bbox[0] && x < vr.bbox[2] && y >= vr.bbox[1] && y < vr.bbox[3]) {
       // reuse a star pair's crop of the reference view when inside its bounds
@@ -324,7 +323,7 @@ __global__ void __launch_bounds__(256, 3) k_canvas(const __grid_constant__ Canva
         const CanvasPair& p = P.pairs[kc];
         pv = p.crop_raw[1][(y - p.y0) * p.w + (x - p.x0)];
       } else {
-        pv = warp_cv(vr, X, Y);
+        pv = warp_cv(vr, L, cyl);
       }
     }
     for (int k = 0; k < np; ++k) {
@@ -333,7 +332,7 @@ __global__ void __launch_bounds__(256, 3) k_canvas(const __grid_constant__ Canva
       if (x < vv.bbox[0] || x >= vv.bbox[2] || y < vv.bbox[1] || y >= vv.bbox[3]) continue;
       const int dx = x - p.x0, dy = y - p.y0;
       const bool inb = dx >= 0 && dy >= 0 && dx < p.w && dy < p.h;
-      const uchar4 q = inb ? p.crop_raw[0][dy * p.w + dx] : warp_cv(vv, X, Y);
+      const uchar4 q = inb ? p.crop_raw[0][dy * p.w + dx] : warp_cv(vv, L, cyl);
       if (!q.w) continue;
       if (pv.w) {
         if (inb) {
@@ -427,8 +426,7 @@ __global__ void __launch_bounds__(256) k_warp_view(const Geometry* __restrict__ 
        idx += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int y = static_cast<int>(idx / g->canvas_w);
     const int x = static_cast<int>(idx - static_cast<long long>(y) * g->canvas_w);
-    const uchar4 o = warp_sample(v, frame, static_cast<double>(x) + g->offx,
-                                 static_cast<double>(y) + g->offy);
+    const uchar4 o = warp_sample(v, frame, canvas_lift(*g, x, y), g->projection == 1);
     if (rgb) {
       rgb[3 * idx + 0] = o.x;
       rgb[3 * idx + 1] = o.y;
@@ -449,14 +447,13 @@ __global__ void __launch_bounds__(256) k_warp_mask(const Geometry* __restrict__ 
        idx += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int y = static_cast<int>(idx / g->canvas_w);
     const int x = static_cast<int>(idx - static_cast<long long>(y) * g->canvas_w);
-    const double X = static_cast<double>(x) + g->offx;
-    const double Y = static_cast<double>(y) + g->offy;
+    const Lift L = canvas_lift(*g, x, y);
     const double* m = v.inv;
-    const double sx0 = (m[0] * X + m[1] * Y) + m[2];
-    const double sy0 = (m[3] * X + m[4] * Y) + m[5];
-    const double sz0 = (m[6] * X + m[7] * Y) + m[8];
+    const double sx0 = (m[0] * L.l0 + m[1] * L.l1) + m[2] * L.l2;
+    const double sy0 = (m[3] * L.l0 + m[4] * L.l1) + m[5] * L.l2;
+    const double sz0 = (m[6] * L.l0 + m[7] * L.l1) + m[8] * L.l2;
     unsigned char ok = 0;
-    if (!(fabs(sz0) < 1e-12)) {
+    if (!(fabs(sz0) < 1e-12) && (g->projection != 1 || sz0 > 0.0)) {
       const double sx = sx0 / sz0, sy = sy0 / sz0;
       const double fx0 = floor(sx), fy0 = floor(sy);
       const int x0 = static_cast<int>(fx0), y0 = static_cast<int>(fy0);

@@ -181,19 +181,51 @@ int validate_init(const stitch_b200_init* in) {
 
 // Warp validity masks of every view over the full canvas, evaluated on the
 // device with the per-frame sampler's geometry (init only).
-int compute_masks(int device, const Geometry& geom, int n_views,
+// Lift tables of the cylindrical canvas (extension); empty for planar.
+struct LiftTables {
+  std::vector<double> s, c, h;
+};
+
+LiftTables make_lift(const stitch_b200_init* in) {
+  LiftTables t;
+  if (in->projection == 1) {
+    hg_ns::Canvas cv;
+    cv.width = in->canvas_width;
+    cv.height = in->canvas_height;
+    cv.offx = in->canvas_offset[0];
+    cv.offy = in->canvas_offset[1];
+    hg_ns::lift_tables(cv, in->cyl_focal, t.s, t.c, t.h);
+  }
+  return t;
+}
+
+// Warp validity masks of every view over the full canvas, evaluated on the
+// device with the per-frame sampler's geometry (init only).
+int compute_masks(int device, Geometry geom, const LiftTables& lt, int n_views,
                   std::vector<std::vector<std::uint8_t>>& masks) {
   CUDA_TRY(cudaSetDevice(device));
   Geometry* d = nullptr;
   std::uint8_t* dm = nullptr;
+  double* dl = nullptr;
   const size_t n = static_cast<size_t>(geom.canvas_w) * geom.canvas_h;
   CUDA_TRY(cudaMalloc(&d, sizeof(Geometry)));
   cudaError_t e = cudaMalloc(&dm, n);
-  if (e != cudaSuccess) {
-    cudaFree(d);
-    return fail(STITCH_B200_CudaError, cudaGetErrorString(e));
+  if (e == cudaSuccess && geom.projection == 1) {
+    e = cudaMalloc(&dl, sizeof(double) * (lt.s.size() + lt.c.size() + lt.h.size()));
+    if (e == cudaSuccess) {
+      geom.lift_sin = dl;
+      geom.lift_cos = dl + lt.s.size();
+      geom.lift_h = dl + lt.s.size() + lt.c.size();
+      e = cudaMemcpy(dl, lt.s.data(), sizeof(double) * lt.s.size(), cudaMemcpyHostToDevice);
+      if (e == cudaSuccess)
+        e = cudaMemcpy(dl + lt.s.size(), lt.c.data(), sizeof(double) * lt.c.size(),
+                       cudaMemcpyHostToDevice);
+      if (e == cudaSuccess)
+        e = cudaMemcpy(dl + lt.s.size() + lt.c.size(), lt.h.data(), sizeof(double) * lt.h.size(),
+                       cudaMemcpyHostToDevice);
+    }
   }
-  e = cudaMemcpy(d, &geom, sizeof(Geometry), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(d, &geom, sizeof(Geometry), cudaMemcpyHostToDevice);
   masks.assign(n_views, std::vector<std::uint8_t>(n));
   for (int v = 0; v < n_views && e == cudaSuccess; ++v) {
     launch_warp_mask(d, v, dm, 0);
@@ -202,11 +234,13 @@ int compute_masks(int device, const Geometry& geom, int n_views,
   }
   cudaFree(d);
   cudaFree(dm);
+  if (dl) cudaFree(dl);
   if (e != cudaSuccess) return fail(STITCH_B200_CudaError, cudaGetErrorString(e));
   return STITCH_B200_OK;
 }
 
 void fill_views(Geometry& g, const stitch_b200_init* in) {
+  g.projection = in->projection == 1 ? 1 : 0;
   g.canvas_w = in->canvas_width;
   g.canvas_h = in->canvas_height;
   g.offx = in->canvas_offset[0];
@@ -289,8 +323,24 @@ int build_context(const stitch_b200_init* in, int device,
   // view footprints (bbox of the warp mask); EmptyProjection if none.
   std::vector<std::vector<std::uint8_t>> masks_local;
   const std::vector<std::vector<std::uint8_t>>* masks = masks_in;
+  const LiftTables lift = make_lift(in);
+  if (g.projection == 1) {
+    if (!(in->cyl_focal > 0.0) ||
+        static_cast<size_t>(in->canvas_width) != lift.s.size())
+      return fail(STITCH_B200_ConfigurationError, "cylindrical canvas needs cyl_focal > 0");
+    double* dl;
+    CUDA_TRY(ctx->alloc(&dl, lift.s.size() + lift.c.size() + lift.h.size()));
+    CUDA_TRY(cudaMemcpy(dl, lift.s.data(), sizeof(double) * lift.s.size(), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(dl + lift.s.size(), lift.c.data(), sizeof(double) * lift.c.size(),
+                        cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(dl + lift.s.size() + lift.c.size(), lift.h.data(),
+                        sizeof(double) * lift.h.size(), cudaMemcpyHostToDevice));
+    g.lift_sin = dl;
+    g.lift_cos = dl + lift.s.size();
+    g.lift_h = dl + lift.s.size() + lift.c.size();
+  }
   if (!masks) {
-    rc = compute_masks(device, g, in->n_views, masks_local);
+    rc = compute_masks(device, g, lift, in->n_views, masks_local);
     if (rc) return rc;
     masks = &masks_local;
   }
@@ -564,6 +614,10 @@ int build_context(const stitch_b200_init* in, int device,
     P.weighting = g.weighting;
     P.offx = g.offx;
     P.offy = g.offy;
+    P.projection = g.projection;
+    P.lift_sin = g.lift_sin;
+    P.lift_cos = g.lift_cos;
+    P.lift_h = g.lift_h;
     for (int v = 0; v < g.n_views; ++v) {
       for (int i = 0; i < 9; ++i) P.views[v].inv[i] = g.views[v].inv[i];
       P.views[v].rgba = g.rgba[v];
@@ -801,6 +855,8 @@ void stitch_b200_config_defaults(stitch_b200_config* c) {
   c->fuse_weighting = 0;
   c->topology = 0;
   c->refine_enabled = 0;
+  c->projection = 0;
+  c->cyl_focal = 0.0;
   for (int v = 0; v < STITCH_B200_MAX_VIEWS; ++v) {
     c->cams[v].fx = c->cams[v].fy = 1.0;
     c->cams[v].rotation[0] = c->cams[v].rotation[4] = c->cams[v].rotation[8] = 1.0;
@@ -826,19 +882,30 @@ int stitch_b200_initialize(const stitch_b200_config* cfg, int device, stitch_b20
     return fail(STITCH_B200_ConfigurationError, "n_views must be in [2, 16]");
   if (cfg->reference < 0 || cfg->reference >= cfg->n_views)
     return fail(STITCH_B200_ConfigurationError, "reference view index out of range");
-  // camera homographies and pairwise maps (pipeline.cpp:219-229)
-  std::vector<hg_ns::Mat3> cam(cfg->n_views), maps(cfg->n_views);
-  std::vector<std::pair<int, int>> sizes;
-  for (int v = 0; v < cfg->n_views; ++v) {
-    int rc = hg_ns::planar_homography(cfg->cams[v], cam[v]);
-    if (rc) return fail(rc, "camera homography failed (rotation or degenerate pose)");
+  std::vector<hg_ns::Mat3> maps(cfg->n_views), invs(cfg->n_views);
+  hg_ns::Canvas canvas;
+  double cyl_f = 0.0;
+  if (cfg->projection == 1) {
+    // cylindrical 360-degree canvas (extension): A_v = K_v R_v R_ref^T
+    cyl_f = cfg->cyl_focal > 0.0 ? cfg->cyl_focal : cfg->cams[cfg->reference].fx;
+    hg_ns::cylinder_maps(*cfg, invs);
+    canvas = hg_ns::cylinder_canvas(*cfg, cyl_f);
+  } else {
+    // camera homographies and pairwise maps (pipeline.cpp:219-229)
+    std::vector<hg_ns::Mat3> cam(cfg->n_views);
+    std::vector<std::pair<int, int>> sizes;
+    for (int v = 0; v < cfg->n_views; ++v) {
+      int rc = hg_ns::planar_homography(cfg->cams[v], cam[v]);
+      if (rc) return fail(rc, "camera homography failed (rotation or degenerate pose)");
+    }
+    for (int v = 0; v < cfg->n_views; ++v) {
+      int rc = hg_ns::pairwise_homography(cam[cfg->reference], cam[v], maps[v]);
+      if (rc) return fail(rc, "singular pairwise homography");
+      sizes.emplace_back(cfg->width[v], cfg->height[v]);
+      hg_ns::inverse3(maps[v], invs[v]);  // pipeline.cpp:40
+    }
+    canvas = hg_ns::compute_canvas(maps, sizes);  // pipeline.cpp:231
   }
-  for (int v = 0; v < cfg->n_views; ++v) {
-    int rc = hg_ns::pairwise_homography(cam[cfg->reference], cam[v], maps[v]);
-    if (rc) return fail(rc, "singular pairwise homography");
-    sizes.emplace_back(cfg->width[v], cfg->height[v]);
-  }
-  const hg_ns::Canvas canvas = hg_ns::compute_canvas(maps, sizes);  // pipeline.cpp:231
   stitch_b200_init in{};
   in.canvas_width = canvas.width;
   in.canvas_height = canvas.height;
@@ -846,12 +913,12 @@ int stitch_b200_initialize(const stitch_b200_config* cfg, int device, stitch_b20
   in.canvas_offset[1] = canvas.offy;
   in.n_views = cfg->n_views;
   in.reference = cfg->reference;
+  in.projection = cfg->projection == 1 ? 1 : 0;
+  in.cyl_focal = cyl_f;
   for (int v = 0; v < cfg->n_views; ++v) {
     in.view_width[v] = cfg->width[v];
     in.view_height[v] = cfg->height[v];
-    hg_ns::Mat3 inv;
-    hg_ns::inverse3(maps[v], inv);  // pipeline.cpp:40
-    for (int i = 0; i < 9; ++i) in.inv_maps[v][i] = inv[i];
+    for (int i = 0; i < 9; ++i) in.inv_maps[v][i] = invs[v][i];
   }
   in.window_capacity = cfg->window_capacity;
   in.lambda = cfg->lambda;
@@ -866,15 +933,15 @@ int stitch_b200_initialize(const stitch_b200_config* cfg, int device, stitch_b20
   if (canvas.width <= 0 || canvas.height <= 0 ||
       static_cast<long long>(canvas.width) * canvas.height > (1ll << 31))
     return fail(STITCH_B200_ConfigurationError, "canvas size out of range");
-
   // rebuild_pair_geometry (pipeline.cpp:181-205): warp masks on the device,
   // overlap bounds and chamfer blend weights on the host (init only).
   Geometry g{};
   fill_views(g, &in);
   std::vector<std::vector<std::uint8_t>> masks;
-  int rc = compute_masks(device, g, cfg->n_views, masks);
+  int rc = compute_masks(device, g, make_lift(&in), cfg->n_views, masks);
   if (rc) return rc;
-  const auto pairs = hg_ns::build_pairs(cfg->n_views, cfg->reference, cfg->topology);
+  const int topo = (cfg->projection == 1 && cfg->topology == 0) ? 3 : cfg->topology;
+  const auto pairs = hg_ns::build_pairs(cfg->n_views, cfg->reference, topo);
   if (static_cast<int>(pairs.size()) > kMaxPairs)
     return fail(STITCH_B200_ConfigurationError, "too many pairs");
   std::vector<std::vector<float>> thetas(pairs.size());

@@ -139,8 +139,20 @@ Canvas compute_canvas(const std::vector<Mat3>& maps,
 }
 
 std::vector<PairSpec> build_pairs(int n_views, int reference, int topology) {
-  const int topo = (topology == 1 || topology == 2) ? topology : (n_views <= 3 ? 1 : 2);
   std::vector<PairSpec> pairs;
+  if (topology == 3) {
+    // ring: k = (v - ref) mod N; distance min(k, N - k); partner one step
+    // toward the reference (the k = N/2 view pairs with k - 1)
+    for (int d = 1; d <= n_views / 2; ++d)
+      for (int v = 0; v < n_views; ++v) {
+        const int k = ((v - reference) % n_views + n_views) % n_views;
+        if (std::min(k, n_views - k) != d) continue;
+        const int partner = (k <= n_views / 2) ? (v - 1 + n_views) % n_views : (v + 1) % n_views;
+        pairs.push_back({v, partner});
+      }
+    return pairs;
+  }
+  const int topo = (topology == 1 || topology == 2) ? topology : (n_views <= 3 ? 1 : 2);
   if (topo == 1) {
     for (int v = 0; v < n_views; ++v)
       if (v != reference) pairs.push_back({v, reference});
@@ -151,6 +163,77 @@ std::vector<PairSpec> build_pairs(int n_views, int reference, int topology) {
       if (std::abs(v - reference) == d)
         pairs.push_back({v, v < reference ? v + 1 : v - 1});
   return pairs;
+}
+
+static void rot_of(const stitch_b200_camera& c, Mat3& r) {
+  for (int i = 0; i < 9; ++i) r[i] = c.rotation[i];
+}
+
+void cylinder_maps(const stitch_b200_config& cfg, std::vector<Mat3>& maps) {
+  Mat3 rref, rrefT;
+  rot_of(cfg.cams[cfg.reference], rref);
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) rrefT[i * 3 + j] = rref[j * 3 + i];
+  maps.resize(cfg.n_views);
+  for (int v = 0; v < cfg.n_views; ++v) {
+    const stitch_b200_camera& c = cfg.cams[v];
+    const Mat3 k = {c.fx, 0, c.cx, 0, c.fy, c.cy, 0, 0, 1};
+    Mat3 r, kr;
+    rot_of(c, r);
+    mul3(k, r, kr);
+    mul3(kr, rrefT, maps[v]);
+  }
+}
+
+Canvas cylinder_canvas(const stitch_b200_config& cfg, double f) {
+  Mat3 rref;
+  rot_of(cfg.cams[cfg.reference], rref);
+  double hmin = std::numeric_limits<double>::max(), hmax = std::numeric_limits<double>::lowest();
+  for (int v = 0; v < cfg.n_views; ++v) {
+    const stitch_b200_camera& c = cfg.cams[v];
+    Mat3 r, rT, m;
+    rot_of(c, r);
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) rT[i * 3 + j] = r[j * 3 + i];
+    mul3(rref, rT, m);  // camera v -> reference frame
+    const int W = cfg.width[v], H = cfg.height[v];
+    auto visit = [&](double px, double py) {
+      const double cx = (px - c.cx) / c.fx, cy = (py - c.cy) / c.fy;
+      const double rx = (m[0] * cx + m[1] * cy) + m[2];
+      const double ry = (m[3] * cx + m[4] * cy) + m[5];
+      const double rz = (m[6] * cx + m[7] * cy) + m[8];
+      const double h = ry / std::sqrt(rx * rx + rz * rz);
+      hmin = std::min(hmin, h);
+      hmax = std::max(hmax, h);
+    };
+    for (int x = 0; x < W; ++x) {
+      visit(x, 0.0);
+      visit(x, H - 1.0);
+    }
+    for (int y = 0; y < H; ++y) {
+      visit(0.0, y);
+      visit(W - 1.0, y);
+    }
+  }
+  Canvas cv;
+  cv.width = static_cast<int>(std::ceil(2.0 * M_PI * f));
+  cv.offx = -std::floor(cv.width / 2.0);
+  cv.offy = std::floor(hmin * f);
+  cv.height = static_cast<int>(std::ceil(hmax * f) - cv.offy) + 1;
+  return cv;
+}
+
+void lift_tables(const Canvas& c, double f, std::vector<double>& lsin, std::vector<double>& lcos,
+                 std::vector<double>& lh) {
+  lsin.resize(c.width);
+  lcos.resize(c.width);
+  lh.resize(c.height);
+  for (int x = 0; x < c.width; ++x) {
+    const double t = (x + c.offx) / f;
+    lsin[x] = std::sin(t);
+    lcos[x] = std::cos(t);
+  }
+  for (int y = 0; y < c.height; ++y) lh[y] = (y + c.offy) / f;
 }
 
 bool overlap_bounds(const std::uint8_t* mi, const std::uint8_t* mj, int w, int h,

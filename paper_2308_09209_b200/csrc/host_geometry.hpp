@@ -40,8 +40,19 @@ Canvas compute_canvas(const std::vector<Mat3>& maps, const std::vector<std::pair
 struct PairSpec {
   int view = 0, partner = 0;
 };
-// Star pairs (pipeline.cpp:233-239) or the N-view chain extension.
+// Star pairs (pipeline.cpp:233-239), the N-view chain extension, or the
+// ring chain (topology 3: partner = ring neighbour toward the reference).
 std::vector<PairSpec> build_pairs(int n_views, int reference, int topology);
+
+// ---- cylindrical 360-degree canvas (extension) ----
+// A_v = K_v R_v R_ref^T: reference-frame ray -> homogeneous pixel of view v.
+void cylinder_maps(const stitch_b200_config& cfg, std::vector<Mat3>& maps);
+// canvas covering 2*pi around the reference camera, height from the
+// cameras' border rays; f = pixels per radian.
+Canvas cylinder_canvas(const stitch_b200_config& cfg, double f);
+// per-column sin/cos of t = (x + offx)/f and per-row h = (y + offy)/f
+void lift_tables(const Canvas& c, double f, std::vector<double>& lsin, std::vector<double>& lcos,
+                 std::vector<double>& lh);
 
 // Overlap bbox of two canvas masks (geometry.cpp:85-117); false if empty.
 bool overlap_bounds(const std::uint8_t* mi, const std::uint8_t* mj, int w, int h,

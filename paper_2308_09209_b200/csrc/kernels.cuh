@@ -81,6 +81,12 @@ struct BalanceState {
 struct Geometry {
   const std::uint8_t* frames[kMaxViews];  // device RGB8 inputs (per frame)
   uchar4* rgba[kMaxViews];                // the inputs expanded to RGBA8
+  // canvas lift (extension): 0 planar (x+offx, y+offy, 1); 1 cylindrical
+  // (sin t[x], h[y], cos t[x]) from host-computed tables
+  int projection;
+  const double* lift_sin;
+  const double* lift_cos;
+  const double* lift_h;
   int canvas_w, canvas_h;
   double offx, offy;
   int n_views, reference, n_pairs;
@@ -138,6 +144,10 @@ struct CanvasPair {
 struct CanvasParams {
   int cw, ch, ref, np, weighting;
   double offx, offy;
+  int projection;
+  const double* lift_sin;
+  const double* lift_cos;
+  const double* lift_h;
   CanvasView views[kMaxViews];
   CanvasPair pairs[kMaxPairs];
 };

@@ -98,6 +98,9 @@ struct stitch_b200_synth {
       if (rig == 1) {  // synth.cpp:76-95
         yaw = k * step;
         cx_world = k * baseline;
+      } else if (rig == 3) {  // ring rig (extension): shared centre
+        yaw = k * step;
+        cx_world = 0.0;
       } else {  // strip rig (extension)
         yaw = k * spec.strip_yaw;
         cx_world = k * step;
@@ -107,7 +110,7 @@ struct stitch_b200_synth {
       const double ry[9] = {cs, 0, sn, 0, 1, 0, -sn, 0, cs};
       for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j) c.rotation[i * 3 + j] = ry[j * 3 + i];
-      const double cen[3] = {cx_world, 0.0, -distance};
+      const double cen[3] = {cx_world, 0.0, rig == 3 ? 0.0 : -distance};
       for (int i = 0; i < 3; ++i) {
         // translation = -R * centre
         c.translation[i] = (-c.rotation[i * 3 + 0] * cen[0] +
@@ -181,6 +184,19 @@ struct stitch_b200_synth {
                            (r[3] * px + r[4] * py) + r[5],
                            (r[6] * px + r[7] * py) + r[8]};
     const auto& c = centre[view];
+    if (rig == 3) {
+      // ring scene (extension): textured cylinder of radius `distance`
+      // around the shared camera centre, texture at (angle * radius, height)
+      const double rr = std::sqrt(dir[0] * dir[0] + dir[2] * dir[2]);
+      if (rr < 1e-12) {
+        rgb[0] = rgb[1] = rgb[2] = 0.0;
+        return;
+      }
+      const double s = distance / rr;
+      const double hx = s * dir[0], hy = s * dir[1], hz = s * dir[2];
+      texture_rgb(spec.seed, std::atan2(hx, hz) * distance, hy, rgb);
+      return;
+    }
     if (spec.object_enabled && std::abs(dir[2]) > 1e-12) {
       const double zo = -spec.object_depth_fraction * distance;
       const double s = (zo - c[2]) / dir[2];
@@ -238,6 +254,21 @@ int stitch_b200_synth_create(const stitch_b200_synth_spec* spec,
     delete s;
     return STITCH_B200_ConfigError;  // the yaw rig cannot exceed 3 views
   }
+  if (s->rig == 3) {
+    if (spec->views < 3) {
+      delete s;
+      return STITCH_B200_ConfigError;
+    }
+    // ring: yaw step 2pi/N, horizontal FOV = step / (1 - overlap)
+    s->reference = 0;
+    s->yaw_step = 2.0 * M_PI / spec->views;
+    const double fov = s->yaw_step / (1.0 - spec->overlap_fraction);
+    s->focal = 0.5 * spec->width / std::tan(0.5 * fov);
+    s->build(s->yaw_step);
+    s->prepare_render();
+    *out = s;
+    return STITCH_B200_OK;
+  }
   // reference_ = views == 3 ? 1 : 0 (synth.cpp:71); (views-1)/2 generalises it.
   s->reference = (spec->views - 1) / 2;
   s->focal = 0.9 * spec->width;
@@ -266,6 +297,11 @@ int stitch_b200_synth_config(const stitch_b200_synth* s, stitch_b200_config* cfg
   stitch_b200_config_defaults(cfg);
   cfg->n_views = s->spec.views;
   cfg->reference = s->reference;
+  if (s->rig == 3) {
+    cfg->projection = 1;
+    cfg->cyl_focal = s->focal;
+    cfg->topology = 3;
+  }
   for (int v = 0; v < s->spec.views; ++v) {
     cfg->width[v] = s->spec.width;
     cfg->height[v] = s->spec.height;

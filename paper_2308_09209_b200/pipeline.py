@@ -145,8 +145,10 @@ class StitchConfig:  # pipeline.hpp:33-44
     window_capacity: int = 3
     fuse_weighting: str = "own"  # "own" | "cross"
     scene_id: str = "scene"
-    topology: str = "auto"  # extension: "auto" | "star" | "chain"
+    topology: str = "auto"  # extension: "auto" | "star" | "chain" | "ring"
     device: int = 0
+    projection: str = "planar"  # extension: "planar" | "cylindrical" (360-degree rigs)
+    cyl_focal: float = 0.0
 
 
 def _config_to_c(cfg: StitchConfig, sizes: Sequence[tuple]) -> _abi.Config:
@@ -176,13 +178,18 @@ def _config_to_c(cfg: StitchConfig, sizes: Sequence[tuple]) -> _abi.Config:
     c.smoothness = cfg.flow.smoothness
     c.window_capacity = cfg.window_capacity
     c.fuse_weighting = 1 if cfg.fuse_weighting == "cross" else 0
-    c.topology = {"auto": 0, "star": 1, "chain": 2}[cfg.topology]
+    c.topology = {"auto": 0, "star": 1, "chain": 2, "ring": 3}[cfg.topology]
+    c.projection = 1 if cfg.projection == "cylindrical" else 0
+    c.cyl_focal = cfg.cyl_focal
     c.refine_enabled = 1 if cfg.refine.enabled else 0
     return c
 
 
 def _config_from_c(c: _abi.Config) -> StitchConfig:
     cfg = StitchConfig(reference=c.reference)
+    cfg.projection = "cylindrical" if c.projection == 1 else "planar"
+    cfg.cyl_focal = c.cyl_focal
+    cfg.topology = {0: "auto", 1: "star", 2: "chain", 3: "ring"}[c.topology]
     for v in range(c.n_views):
         cam = c.cams[v]
         cfg.views.append(ViewSetup(
@@ -428,7 +435,7 @@ class SynthSpec:
     object: ParallaxObject = field(default_factory=ParallaxObject)
     perturb_focal_scale: float = 1.0
     perturb_principal_px: float = 0.0
-    rig: str = "auto"  # "auto" | "yaw" (reference) | "strip" (N-view extension)
+    rig: str = "auto"  # "auto" | "yaw" (reference) | "strip" | "ring" (N-view extensions)
     strip_yaw: float = 0.05
 
     def to_c(self) -> _abi.SynthSpec:
@@ -457,7 +464,7 @@ class SynthSpec:
         s.object_velocity[0], s.object_velocity[1] = self.object.velocity
         s.perturb_focal_scale = self.perturb_focal_scale
         s.perturb_principal_px = self.perturb_principal_px
-        s.rig = {"auto": 0, "yaw": 1, "strip": 2}[self.rig]
+        s.rig = {"auto": 0, "yaw": 1, "strip": 2, "ring": 3}[self.rig]
         s.strip_yaw = self.strip_yaw
         return s
 

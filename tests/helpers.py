@@ -33,7 +33,9 @@ def oracle_config(sc: pb.SynthScene, *, threads=4, keep_debug=1, window=3, weigh
                          gamma_bright=gamma_bright, target_black=target_black,
                          target_white=target_white, levels=levels, iterations=iterations,
                          smoothness=smoothness, window=window, weighting=weighting,
-                         topology=topology, threads=threads, keep_debug=keep_debug)
+                         topology=topology if topology else c.topology, threads=threads,
+                         keep_debug=keep_debug, projection=c.projection,
+                         cyl_focal=c.cyl_focal)
 
 
 def product_config(sc: pb.SynthScene, *, window=3, weighting=0, topology=0, levels=4,
@@ -42,7 +44,8 @@ def product_config(sc: pb.SynthScene, *, window=3, weighting=0, topology=0, leve
     cfg = sc.config()
     cfg.window_capacity = window
     cfg.fuse_weighting = "cross" if weighting else "own"
-    cfg.topology = {0: "auto", 1: "star", 2: "chain"}[topology]
+    if topology:
+        cfg.topology = {1: "star", 2: "chain", 3: "ring"}[topology]
     cfg.flow = pb.FlowOptions(levels=levels, iterations=iterations, smoothness=smoothness)
     cfg.balance = pb.BalanceConfig(lam, gamma_dark, gamma_bright, target_black, target_white)
     return cfg

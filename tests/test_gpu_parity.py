@@ -347,3 +347,29 @@ def test_pipelined_submit_matches_sync_and_oracle():
                 lib.stitch_b200_host_free(p)
             lib.stitch_b200_host_free(hout[t][0])
             lib.stitch_b200_host_free(hout[t][1])
+
+
+def test_eight_view_chain_parity():
+    """Config-4 topology (8 cameras, chain of 7 pairs, depth 4 colour
+    correction) at reduced resolution, bit-exact vs the extended oracle."""
+    casts = [(1.0 - 0.03 * v, 1.0, 1.0 + 0.02 * v) for v in range(8)]
+    sc = scene(views=8, width=240, height=135, frames=2, focal_scale=1.03, casts=casts)
+    state, ost = make_pair(sc)
+    check_geometry(state, ost, 8)
+    assert len(state.pairs) == 7
+    for t in range(2):
+        check_frame(state, ost, frames_at(sc, t), t)
+
+
+def test_ring_360_parity():
+    """BASELINE config 3 topology: 6-camera 360-degree ring on a cylindrical
+    canvas (extension: lift tables, ring-chain pairs, the opposite view
+    straddling the seam), bit-exact vs the extended oracle."""
+    spec = pb.SynthSpec(views=6, width=256, height=144, frames=3, rig="ring",
+                        color_casts=[(1.0 - 0.04 * v, 1.0, 1.0 + 0.03 * v) for v in range(6)])
+    sc = pb.SynthScene(spec)
+    state, ost = make_pair(sc)
+    check_geometry(state, ost, 6)
+    assert [(p.view, p.partner) for p in state.pairs] == [(1, 0), (5, 0), (2, 1), (4, 5), (3, 2)]
+    for t in range(3):
+        check_frame(state, ost, frames_at(sc, t), t)

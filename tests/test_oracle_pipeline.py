@@ -84,3 +84,24 @@ def test_four_view_chain_runs_and_pairs_are_adjacent():
     assert pairs == [(0, 1), (2, 1), (3, 2)]
     data, mask, rep = st.process([f.data for f in frames_at(sc, 0)])
     assert mask.sum() > 0 and rep.balanced == 1
+
+
+def test_ring_rig_oracle_geometry():
+    """360-degree ring extension: cylindrical canvas spans 2*pi*f, pairs form
+    a ring chain outward from the reference, the opposite view straddles the
+    canvas seam, and a frame stitches with every pixel column covered."""
+    import math
+
+    import paper_2308_09209_b200 as pb
+
+    sc = pb.SynthScene(pb.SynthSpec(views=6, width=192, height=108, rig="ring"))
+    st = O.OracleState(oracle_config(sc))
+    c = sc.config_c()
+    w, h, ox, oy = st.canvas
+    assert w == math.ceil(2 * math.pi * c.cyl_focal)
+    pairs = [st.pair(k)[:2] for k in range(st.n_pairs())]
+    assert pairs == [(1, 0), (5, 0), (2, 1), (4, 5), (3, 2)]
+    x0, _, x1, _ = st.view_bbox(3)
+    assert x0 == 0 and x1 == w  # wraps around the seam
+    data, mask, rep = st.process([f.data for f in frames_at(sc, 0)])
+    assert mask.any(axis=0).all() and rep.balanced == 1
