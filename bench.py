@@ -45,6 +45,10 @@ WORKLOADS = {
     # BASELINE.json configs[0] (reference CPU-runnable case)
     "c1": dict(views=2, width=640, height=480, focal_scale=1.0,
                desc="2 synthetic 640x480 RGB camera streams, one overlap, fixed homography"),
+    # BASELINE.json configs[2] (extension: cylindrical canvas, ring chain)
+    "c3": dict(views=6, width=1920, height=1080, focal_scale=1.0, rig="ring",
+               desc="6-camera 360-degree ring at 1080p, 3D-M temporal colour transfer, "
+                    "piecewise global balancing"),
     # BASELINE.json configs[3]
     "c4": dict(views=8, width=3840, height=2160, focal_scale=1.03,
                desc="8 cameras 3840x2160 RGB single panorama stream"),
@@ -58,7 +62,7 @@ def build_scene(wl, seed):
 
     spec = pb.SynthSpec(seed=seed, views=wl["views"], frames=300, width=wl["width"],
                         height=wl["height"], overlap_fraction=0.3,
-                        perturb_focal_scale=wl["focal_scale"])
+                        perturb_focal_scale=wl["focal_scale"], rig=wl.get("rig", "auto"))
     spec.color_casts = [(1.0, 1.0, 1.0) if v % 2 == 0 else (0.88, 1.0, 1.08)
                         for v in range(wl["views"])]
     spec.flicker = [pb.FlickerEvent(frame=5, view=wl["views"] - 1, gains=(1.15, 1.1, 0.95))]
@@ -435,7 +439,9 @@ def oracle_state_for(sc, threads):
     cams = [(c.cams[v].fx, c.cams[v].fy, c.cams[v].cx, c.cams[v].cy, list(c.cams[v].rotation),
              list(c.cams[v].translation)) for v in range(c.n_views)]
     sizes = [(c.width[v], c.height[v]) for v in range(c.n_views)]
-    return O.OracleState(O.make_config(c.n_views, c.reference, sizes, cams, threads=threads))
+    return O.OracleState(O.make_config(c.n_views, c.reference, sizes, cams, threads=threads,
+                                       topology=c.topology, projection=c.projection,
+                                       cyl_focal=c.cyl_focal))
 
 
 def cpu_baseline(args, wl, sample_seconds=15.0, max_frames=None):

@@ -242,6 +242,14 @@ __device__ void balance_lut(const Geometry* __restrict__ g, DevState* __restrict
   }
 }
 
+// the view's footprint may contain (x, y): inside its bbox and outside the
+// empty column run of a wrapped ring view (the warp is invalid there, so
+// skipping it is exact)
+__device__ __forceinline__ bool may_cover(const CanvasView& v, int x, int y) {
+  return x >= v.bbox[0] && x < v.bbox[2] && y >= v.bbox[1] && y < v.bbox[3] &&
+         !(x >= v.gap[0] && x < v.gap[1]);
+}
+
 __device__ __forceinline__ bool in_rect(const CanvasPair& p, int x, int y) {
   return x >= p.x0 && x < p.x0 + p.w && y >= p.y0 && y < p.y0 + p.h;
 }
@@ -309,7 +317,7 @@ __global__ void __launch_bounds__(256, 3) k_canvas(const __grid_constant__ Canva
     const Lift L = canvas_lift(P, x, y);
     const bool cyl = P.projection == 1;
     uchar4 pv = make_uchar4(0, 0, 0, 0);
-    if (x >= vr.bbox[0] && x < vr.bbox[2] && y >= vr.bbox[1] && y < vr.bbox[3]) {
+    if (may_cover(vr, x, y)) {
       // reuse a star pair's crop of the reference view when inside its bounds
       int kc = -1;
       for (int k = 0; k < np; ++k) {
@@ -329,7 +337,7 @@ __global__ void __launch_bounds__(256, 3) k_canvas(const __grid_constant__ Canva
     for (int k = 0; k < np; ++k) {
       const CanvasPair& p = P.pairs[k];
       const CanvasView& vv = P.views[p.view];
-      if (x < vv.bbox[0] || x >= vv.bbox[2] || y < vv.bbox[1] || y >= vv.bbox[3]) continue;
+      if (!may_cover(vv, x, y)) continue;
       const int dx = x - p.x0, dy = y - p.y0;
       const bool inb = dx >= 0 && dy >= 0 && dx < p.w && dy < p.h;
       const uchar4 q = inb ? p.crop_raw[0][dy * p.w + dx] : warp_cv(vv, L, cyl);

@@ -349,6 +349,7 @@ int build_context(const stitch_b200_init* in, int device,
     if (!hg_ns::mask_bbox((*masks)[v].data(), g.canvas_w, g.canvas_h, b))
       return fail(STITCH_B200_EmptyProjection, "a view projects to no canvas pixel");
     for (int i = 0; i < 4; ++i) g.views[v].bbox[i] = b[i];
+    hg_ns::mask_column_gap((*masks)[v].data(), g.canvas_w, g.canvas_h, b, g.views[v].gap);
   }
 
   // buffers
@@ -624,6 +625,8 @@ int build_context(const stitch_b200_init* in, int device,
       P.views[v].w = g.views[v].width;
       P.views[v].h = g.views[v].height;
       for (int i = 0; i < 4; ++i) P.views[v].bbox[i] = g.views[v].bbox[i];
+      P.views[v].gap[0] = g.views[v].gap[0];
+      P.views[v].gap[1] = g.views[v].gap[1];
     }
     for (int k = 0; k < g.n_pairs; ++k) {
       const PairDesc& p = g.pairs[k];

@@ -275,6 +275,29 @@ bool mask_bbox(const std::uint8_t* m, int w, int h, int b[4]) {
   return true;
 }
 
+void mask_column_gap(const std::uint8_t* m, int w, int h, const int b[4], int gap[2]) {
+  gap[0] = gap[1] = 0;
+  std::vector<std::uint8_t> col(static_cast<size_t>(w), 0);
+  for (int y = b[1]; y < b[3]; ++y)
+    for (int x = b[0]; x < b[2]; ++x)
+      if (m[static_cast<size_t>(y) * w + x]) col[x] = 1;
+  int best = 0;
+  for (int x = b[0]; x < b[2];) {
+    if (col[x]) {
+      ++x;
+      continue;
+    }
+    int e = x;
+    while (e < b[2] && !col[e]) ++e;
+    if (e - x > best) {
+      best = e - x;
+      gap[0] = x;
+      gap[1] = e;
+    }
+    x = e;
+  }
+}
+
 static constexpr float kFarAway = 1e9f;  // flow.cpp:14
 
 // chamfer_distance (flow.cpp:192-223)

@@ -28,6 +28,7 @@ constexpr int kMaxTasks = 2 * kMaxPairs;
 struct ViewDesc {
   int width, height;
   int bbox[4];  // x0,y0,x1,y1 of the view's valid canvas footprint
+  int gap[2];   // empty columns [gap0, gap1) inside bbox (wrapped ring views)
   double inv[9];
 };
 
@@ -130,6 +131,7 @@ struct CanvasView {
   const uchar4* rgba;
   int w, h;
   int bbox[4];
+  int gap[2];
 };
 
 struct CanvasPair {
