@@ -120,7 +120,7 @@ SYMBOLS = [
 ]
 
 OP_KIND_NAMES = ["expand_rgba", "crop_warp", "pair_color", "pair_solve", "flow_prepare", "pyr_down", "hs_linearize",
-                 "hs_sweeps", "canvas_balance", "balance", "tone", "event", "canvas_exclusive"]
+                 "hs_sweeps", "canvas_balance", "balance", "tone", "event"]
 
 _lib = None
 

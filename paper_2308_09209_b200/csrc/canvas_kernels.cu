@@ -53,13 +53,14 @@ __global__ void __launch_bounds__(256) k_expand_one(const std::uint8_t* __restri
 // (pipeline.cpp:310-311) evaluated directly on the bounds.
 // grid: (ceil(max_w/64), ceil(max_h/4), 2*n_pairs), block (64, 4)
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uchar4 warp_cv(const CanvasView& v, Lift L, bool cyl) {
+template <bool CYL>
+__device__ __forceinline__ uchar4 warp_cv(const CanvasView& v, Lift L) {
   ViewDesc d;
   d.width = v.w;
   d.height = v.h;
 #pragma unroll
   for (int i = 0; i < 9; ++i) d.inv[i] = v.inv[i];
-  return warp_sample(d, v.rgba, L, cyl);
+  return warp_sample<CYL>(d, v.rgba, L);
 }
 
 __global__ void __launch_bounds__(256) k_crop_warp(const __grid_constant__ CanvasParams P) {
@@ -71,7 +72,8 @@ __global__ void __launch_bounds__(256) k_crop_warp(const __grid_constant__ Canva
   if (dx >= p.w || dy >= p.h) return;
   const int view = side ? p.partner : p.view;
   p.crop_raw[side][dy * p.w + dx] =
-      warp_cv(P.views[view], canvas_lift(P, p.x0 + dx, p.y0 + dy), P.projection == 1);
+      P.projection == 1 ? warp_cv<true>(P.views[view], canvas_lift<true>(P, p.x0 + dx, p.y0 + dy))
+                        : warp_cv<false>(P.views[view], canvas_lift<false>(P, p.x0 + dx, p.y0 + dy));
 }
 
 // ---------------------------------------------------------------------------
@@ -254,15 +256,60 @@ __device__ __forceinline__ bool in_rect(const CanvasPair& p, int x, int y) {
   return x >= p.x0 && x < p.x0 + p.w && y >= p.y0 && y < p.y0 + p.h;
 }
 
-// mode 0: every canvas pixel; mode 1: pixels outside every pair's bounds
-// (independent of the flow, runs concurrently with it); mode 2: pixels inside
-// some pair's bounds (after the flow).  blocks_total: CTAs of all canvas
-// launches of the frame (the last one builds the balance LUT).
-__global__ void __launch_bounds__(256, 3) k_canvas(const __grid_constant__ CanvasParams P,
+// One canvas pixel: the warped reference view, then the compose_panorama
+// fold over pairs (pipeline.cpp:326-333, flow.cpp:324-357).
+template <bool CYL>
+__device__ __forceinline__ uchar4 canvas_pixel(const CanvasParams& P,
+                                               const double (*mview)[9], int x, int y) {
+  const int ref = P.ref;
+  const CanvasView& vr = P.views[ref];
+  const int np = P.np;
+  const Lift L = canvas_lift<CYL>(P, x, y);
+  uchar4 pv = make_uchar4(0, 0, 0, 0);
+  if (may_cover(vr, x, y)) {
+    // reuse a star pair's crop of the reference view when inside its bounds
+    int kc = -1;
+    for (int k = 0; k < np; ++k) {
+      const CanvasPair& p = P.pairs[k];
+      if (p.partner == ref && x >= p.x0 && x < p.x0 + p.w && y >= p.y0 && y < p.y0 + p.h) {
+        kc = k;
+        break;
+      }
+    }
+    if (kc >= 0) {
+      const CanvasPair& p = P.pairs[kc];
+      pv = p.crop_raw[1][(y - p.y0) * p.w + (x - p.x0)];
+    } else {
+      pv = warp_cv<CYL>(vr, L);
+    }
+  }
+  for (int k = 0; k < np; ++k) {
+    const CanvasPair& p = P.pairs[k];
+    const CanvasView& vv = P.views[p.view];
+    if (!may_cover(vv, x, y)) continue;
+    const int dx = x - p.x0, dy = y - p.y0;
+    const bool inb = dx >= 0 && dy >= 0 && dx < p.w && dy < p.h;
+    const uchar4 q = inb ? p.crop_raw[0][dy * p.w + dx] : warp_cv<CYL>(vv, L);
+    if (!q.w) continue;
+    if (pv.w) {
+      if (inb) {
+        uchar4 f;
+        if (fused_pixel(P, p, dx, dy, f)) pv = f;
+      }
+    } else {
+      pv = apply_matrix(mview[p.view], q);
+    }
+  }
+  return pv;
+}
+
+// Every canvas pixel once (64 x 4 tiles, grid-stride), per-CTA histogram
+// flushed to the frame histogram; the last CTA builds the balance LUT.
+template <bool CYL>
+__global__ void __launch_bounds__(256, 4) k_canvas(const __grid_constant__ CanvasParams P,
                                                    const Geometry* __restrict__ g,
                                                    DevState* __restrict__ st,
-                                                   uchar4* __restrict__ pano, int mode,
-                                                   unsigned blocks_total) {
+                                                   uchar4* __restrict__ pano) {
   __shared__ unsigned int hist[3][256];
   __shared__ double mview[kMaxViews][9];
   __shared__ bool last;
@@ -274,83 +321,15 @@ __global__ void __launch_bounds__(256, 3) k_canvas(const __grid_constant__ Canva
   for (int i = threadIdx.x; i < kMaxViews * 9; i += blockDim.x) mview[i / 9][i % 9] = st->mview[i / 9][i % 9];
   __syncthreads();
   const int cw = P.cw, ch = P.ch;
-  const int ref = P.ref;
-  const CanvasView& vr = P.views[ref];
-  const int np = P.np;
   const int tiles_x = (cw + 63) / 64;
-  int ntiles = tiles_x * ((ch + 3) / 4);
-  if (mode == 2) {
-    ntiles = 0;
-    for (int k = 0; k < np; ++k) ntiles += ((P.pairs[k].w + 63) / 64) * ((P.pairs[k].h + 3) / 4);
-  }
+  const int ntiles = tiles_x * ((ch + 3) / 4);
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    int x, y;
-    if (mode != 2) {
-      const int ty = tile / tiles_x;
-      x = (tile - ty * tiles_x) * 64 + threadIdx.x % 64;
-      y = ty * 4 + threadIdx.x / 64;
-      if (x >= cw || y >= ch) continue;
-      if (mode == 1) {
-        bool inside = false;
-        for (int k = 0; k < np; ++k) inside = inside || in_rect(P.pairs[k], x, y);
-        if (inside) continue;
-      }
-    } else {
-      int t = tile, k = 0;
-      for (; k < np; ++k) {
-        const int n = ((P.pairs[k].w + 63) / 64) * ((P.pairs[k].h + 3) / 4);
-        if (t < n) break;
-        t -= n;
-      }
-      const CanvasPair& pk = P.pairs[k];
-      const int tx = (pk.w + 63) / 64;
-      const int tyy = t / tx;
-      const int dx = (t - tyy * tx) * 64 + threadIdx.x % 64, dy = tyy * 4 + threadIdx.x / 64;
-      if (dx >= pk.w || dy >= pk.h) continue;
-      x = pk.x0 + dx;
-      y = pk.y0 + dy;
-      bool earlier = false;  // each pixel once: owned by the first rect containing it
-      for (int k2 = 0; k2 < k; ++k2) earlier = earlier || in_rect(P.pairs[k2], x, y);
-      if (earlier) continue;
-    }
+    const int ty = tile / tiles_x;
+    const int x = (tile - ty * tiles_x) * 64 + threadIdx.x % 64;
+    const int y = ty * 4 + threadIdx.x / 64;
+    if (x >= cw || y >= ch) continue;
     const long long idx = static_cast<long long>(y) * cw + x;
-    const Lift L = canvas_lift(P, x, y);
-    const bool cyl = P.projection == 1;
-    uchar4 pv = make_uchar4(0, 0, 0, 0);
-    if (may_cover(vr, x, y)) {
-      // reuse a star pair's crop of the reference view when inside its bounds
-      int kc = -1;
-      for (int k = 0; k < np; ++k) {
-        const CanvasPair& p = P.pairs[k];
-        if (p.partner == ref && x >= p.x0 && x < p.x0 + p.w && y >= p.y0 && y < p.y0 + p.h) {
-          kc = k;
-          break;
-        }
-      }
-      if (kc >= 0) {
-        const CanvasPair& p = P.pairs[kc];
-        pv = p.crop_raw[1][(y - p.y0) * p.w + (x - p.x0)];
-      } else {
-        pv = warp_cv(vr, L, cyl);
-      }
-    }
-    for (int k = 0; k < np; ++k) {
-      const CanvasPair& p = P.pairs[k];
-      const CanvasView& vv = P.views[p.view];
-      if (!may_cover(vv, x, y)) continue;
-      const int dx = x - p.x0, dy = y - p.y0;
-      const bool inb = dx >= 0 && dy >= 0 && dx < p.w && dy < p.h;
-      const uchar4 q = inb ? p.crop_raw[0][dy * p.w + dx] : warp_cv(vv, L, cyl);
-      if (!q.w) continue;
-      if (pv.w) {
-        if (inb) {
-          uchar4 f;
-          if (fused_pixel(P, p, dx, dy, f)) pv = f;
-        }
-      } else {
-        pv = apply_matrix(mview[p.view], q);
-      }
-    }
+    const uchar4 pv = canvas_pixel<CYL>(P, mview, x, y);
     pano[idx] = pv;
     if (pv.w) {
       atomicAdd(&hist[0][pv.x], 1u);
@@ -364,7 +343,7 @@ __global__ void __launch_bounds__(256, 3) k_canvas(const __grid_constant__ Canva
       if (hist[c][i]) atomicAdd(&st->pano_hist[c][i], hist[c][i]);
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(&st->canvas_done, 1u) == blocks_total - 1;
+  if (threadIdx.x == 0) last = atomicAdd(&st->canvas_done, 1u) == gridDim.x - 1;
   __syncthreads();
   if (!last) return;
   __threadfence();
@@ -434,7 +413,8 @@ __global__ void __launch_bounds__(256) k_warp_view(const Geometry* __restrict__ 
        idx += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int y = static_cast<int>(idx / g->canvas_w);
     const int x = static_cast<int>(idx - static_cast<long long>(y) * g->canvas_w);
-    const uchar4 o = warp_sample(v, frame, canvas_lift(*g, x, y), g->projection == 1);
+    const uchar4 o = g->projection == 1 ? warp_sample<true>(v, frame, canvas_lift<true>(*g, x, y))
+                                        : warp_sample<false>(v, frame, canvas_lift<false>(*g, x, y));
     if (rgb) {
       rgb[3 * idx + 0] = o.x;
       rgb[3 * idx + 1] = o.y;
@@ -455,11 +435,11 @@ __global__ void __launch_bounds__(256) k_warp_mask(const Geometry* __restrict__ 
        idx += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int y = static_cast<int>(idx / g->canvas_w);
     const int x = static_cast<int>(idx - static_cast<long long>(y) * g->canvas_w);
-    const Lift L = canvas_lift(*g, x, y);
-    const double* m = v.inv;
-    const double sx0 = (m[0] * L.l0 + m[1] * L.l1) + m[2] * L.l2;
-    const double sy0 = (m[3] * L.l0 + m[4] * L.l1) + m[5] * L.l2;
-    const double sz0 = (m[6] * L.l0 + m[7] * L.l1) + m[8] * L.l2;
+    double sx0, sy0, sz0;
+    if (g->projection == 1)
+      warp_point<true>(v.inv, canvas_lift<true>(*g, x, y), sx0, sy0, sz0);
+    else
+      warp_point<false>(v.inv, canvas_lift<false>(*g, x, y), sx0, sy0, sz0);
     unsigned char ok = 0;
     if (!(fabs(sz0) < 1e-12) && (g->projection != 1 || sz0 > 0.0)) {
       const double sx = sx0 / sz0, sy = sy0 / sz0;
@@ -502,22 +482,15 @@ void launch_crop_warp(const CanvasParams& P, int max_w, int max_h, cudaStream_t 
   k_crop_warp<<<grid, dim3(64, 4), 0, s>>>(P);
 }
 
-static int canvas_blocks(const CanvasParams& P, int mode, int num_sms) {
-  long long tiles = 0;
-  if (mode != 2) {
-    tiles = static_cast<long long>((P.cw + 63) / 64) * ((P.ch + 3) / 4);
-  } else {
-    for (int k = 0; k < P.np; ++k) tiles += ((P.pairs[k].w + 63) / 64) * ((P.pairs[k].h + 3) / 4);
-  }
-  const long long b = std::min<long long>(static_cast<long long>(num_sms) * 4, tiles);
-  return static_cast<int>(b < 1 ? 1 : b);
-}
-
 void launch_canvas(const CanvasParams& P, const Geometry* g, DevState* st, uchar4* pano,
-                   int num_sms, int mode, cudaStream_t s) {
-  const unsigned total = mode == 0 ? canvas_blocks(P, 0, num_sms)
-                                   : canvas_blocks(P, 1, num_sms) + canvas_blocks(P, 2, num_sms);
-  k_canvas<<<canvas_blocks(P, mode, num_sms), 256, 0, s>>>(P, g, st, pano, mode, total);
+                   int num_sms, cudaStream_t s) {
+  const long long tiles = static_cast<long long>((P.cw + 63) / 64) * ((P.ch + 3) / 4);
+  const long long b = std::min<long long>(static_cast<long long>(num_sms) * 4, tiles);
+  const int blocks = static_cast<int>(b < 1 ? 1 : b);
+  if (P.projection == 1)
+    k_canvas<true><<<blocks, 256, 0, s>>>(P, g, st, pano);
+  else
+    k_canvas<false><<<blocks, 256, 0, s>>>(P, g, st, pano);
 }
 
 void launch_tone(const DevState* st, const uchar4* pano, long long n_px, std::uint8_t* out_rgb,

@@ -34,7 +34,7 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 enum OpKind { OP_EXPAND, OP_CROP, OP_STATS, OP_SOLVE, OP_PREP, OP_PYR, OP_HSPREP, OP_HS, OP_CANVAS,
-              OP_BALANCE, OP_TONE, OP_EVENT, OP_CANVAS_OUT };
+              OP_BALANCE, OP_TONE, OP_EVENT };
 
 struct Op {
   OpKind kind;
@@ -80,8 +80,7 @@ struct Ctx {
   cudaGraphExec_t exec[kSlots] = {};
   int launches = 0;
   cudaEvent_t ev[kSlots][6] = {};
-  cudaStream_t h2d = nullptr, d2h = nullptr, side = nullptr;
-  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t h2d_done[kSlots] = {}, comp_done[kSlots] = {}, d2h_done[kSlots] = {};
   long long seq = 0;                       // frames submitted (any API)
   long long slot_ticket[kSlots] = {-1, -1};  // ticket occupying each slot
@@ -111,9 +110,6 @@ struct Ctx {
     }
     if (h2d) cudaStreamDestroy(h2d);
     if (d2h) cudaStreamDestroy(d2h);
-    if (side) cudaStreamDestroy(side);
-    if (fork_ev) cudaEventDestroy(fork_ev);
-    if (join_ev) cudaEventDestroy(join_ev);
     for (auto& e : ring_ev)
       if (e) cudaEventDestroy(e);
     for (void* p : allocs) cudaFree(p);
@@ -281,10 +277,7 @@ int enqueue_op(Ctx* ctx, const Op& op, cudaStream_t s, int slot = 0) {
       launch_hs_iter(ctx->d_hs + op.offset, op.count, op.max_w, op.max_h, op.sweeps, s);
       return 1;
     case OP_CANVAS:
-      launch_canvas(ctx->cparams, ctx->dg, ctx->dst, ctx->d_pano, ctx->num_sms, 0, s);
-      return 1;
-    case OP_CANVAS_OUT:
-      launch_canvas(ctx->cparams, ctx->dg, ctx->dst, ctx->d_pano, ctx->num_sms, 1, s);
+      launch_canvas(ctx->cparams, ctx->dg, ctx->dst, ctx->d_pano, ctx->num_sms, s);
       return 1;
     case OP_TONE:
       launch_tone(ctx->dst, ctx->d_pano, ctx->n_px, ctx->d_out_rgb[slot], ctx->d_out_mask[slot], s);
@@ -671,9 +664,6 @@ int build_context(const stitch_b200_init* in, int device,
     CUDA_TRY(cudaEventCreateWithFlags(&ctx->d2h_done[sl], cudaEventDisableTiming));
   }
   CUDA_TRY(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
-  CUDA_TRY(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
-  CUDA_TRY(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
-  CUDA_TRY(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
   CUDA_TRY(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
   for (auto& e : ctx->ring_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_ptr_ring),
@@ -687,23 +677,11 @@ int build_context(const stitch_b200_init* in, int device,
   for (int sl = 0; sl < Ctx::kSlots; ++sl) {
     CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     launches = 0;
-    bool forked = false;
     for (const Op& op : plan) {
-      if (op.kind == OP_EVENT) {
+      if (op.kind == OP_EVENT)
         cudaEventRecordWithFlags(ctx->ev[sl][op.event], s, cudaEventRecordExternal);
-      } else if (op.kind == OP_CANVAS_OUT) {
-        cudaEventRecord(ctx->fork_ev, s);
-        cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0);
-        launches += enqueue_op(ctx.get(), op, ctx->side, sl);
-        cudaEventRecord(ctx->join_ev, ctx->side);
-        forked = true;
-      } else {
-        if (op.kind == OP_CANVAS && forked) {
-          cudaStreamWaitEvent(s, ctx->join_ev, 0);
-          forked = false;
-        }
+      else
         launches += enqueue_op(ctx.get(), op, s, sl);
-      }
     }
     cudaError_t cap_err = cudaStreamEndCapture(s, &ctx->graph[sl]);
     if (cap_err != cudaSuccess)

@@ -275,7 +275,7 @@ bool mask_bbox(const std::uint8_t* m, int w, int h, int b[4]) {
   return true;
 }
 
-void mask_column_gap(const std::uint8_t* m, int w, int h, const int b[4], int gap[2]) {
+void mask_column_gap(const std::uint8_t* m, int w, int /*h*/, const int b[4], int gap[2]) {
   gap[0] = gap[1] = 0;
   std::vector<std::uint8_t> col(static_cast<size_t>(w), 0);
   for (int y = b[1]; y < b[3]; ++y)
