@@ -94,15 +94,18 @@ __device__ __forceinline__ bool fused_pixel(const CanvasParams& P, const CanvasP
   const float tj = 1.0f - ti;  // BlendWeights::theta_j (flow.cpp:276)
   const float wi = P.weighting == 0 ? ti : tj;
   const float wj = P.weighting == 0 ? tj : ti;
+  // dense_flow zeroes both fields where either crop is invalid
+  // (flow.cpp:178-185); the Jacobi kernels leave that to this consumer
+  const bool valid = p.crop_cor[0][i].w && p.crop_cor[1][i].w;
+  const float uij = valid ? p.fu[0][i] : 0.0f, vij = valid ? p.fv[0][i] : 0.0f;
+  const float uji = valid ? p.fu[1][i] : 0.0f, vji = valid ? p.fv[1][i] : 0.0f;
   float ri, gi, bi, rj, gj, bj;
   const bool vi = sample_crop(p.crop_cor[0], p.w, p.h,
-                              static_cast<double>(static_cast<float>(dx) + wi * p.fu[0][i]),
-                              static_cast<double>(static_cast<float>(dy) + wi * p.fv[0][i]),
-                              ri, gi, bi);
+                              static_cast<double>(static_cast<float>(dx) + wi * uij),
+                              static_cast<double>(static_cast<float>(dy) + wi * vij), ri, gi, bi);
   const bool vj = sample_crop(p.crop_cor[1], p.w, p.h,
-                              static_cast<double>(static_cast<float>(dx) + wj * p.fu[1][i]),
-                              static_cast<double>(static_cast<float>(dy) + wj * p.fv[1][i]),
-                              rj, gj, bj);
+                              static_cast<double>(static_cast<float>(dx) + wj * uji),
+                              static_cast<double>(static_cast<float>(dy) + wj * vji), rj, gj, bj);
   if (!vi && !vj) return false;
   float r, gg, b;
   if (vi && vj) {

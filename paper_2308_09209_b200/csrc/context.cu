@@ -42,6 +42,7 @@ struct Op {
   int max_w = 0, max_h = 0, max_px = 0;
   int event = 0;
   int sweeps = 0;  // OP_HS: Jacobi sweeps of this launch (segment length)
+  int fuse = 0;    // OP_HS: the launch also linearises the warp iteration
 };
 
 }  // namespace
@@ -274,7 +275,8 @@ int enqueue_op(Ctx* ctx, const Op& op, cudaStream_t s, int slot = 0) {
       launch_hs_prepare(ctx->d_hp + op.offset, op.count, op.max_w, op.max_h, ctx->alpha2, s);
       return 1;
     case OP_HS:
-      launch_hs_iter(ctx->d_hs + op.offset, op.count, op.max_w, op.max_h, op.sweeps, s);
+      launch_hs_iter(ctx->d_hs + op.offset, op.count, op.max_w, op.max_h, op.sweeps, op.fuse,
+                     ctx->alpha2, s);
       return 1;
     case OP_CANVAS:
       launch_canvas(ctx->cparams, ctx->dg, ctx->dst, ctx->d_pano, ctx->num_sms, s);
@@ -501,47 +503,64 @@ int build_context(const stitch_b200_init* in, int device,
     op.count = static_cast<int>(pyr_table.size()) - op.offset;
     if (op.count) plan.push_back(op);
   }
-  // Each warp iteration (5 per level, flow.cpp:78) is one linearisation
-  // launch (constants planes) followed by its `sweeps` Jacobi sweeps as
-  // nseg launches (segments), ping-ponging two flow buffers per task.
+  // Each warp iteration (5 per level, flow.cpp:78) is a linearisation (the
+  // constants planes) followed by its `sweeps` Jacobi sweeps as nseg
+  // launches (segments), ping-ponging two flow buffers per task.  The
+  // linearisation is fused into the first segment on the levels where the
+  // sweep launcher says it pays (hs_fuse_wanted), else it is a launch of its
+  // own.
   const int nseg = hs_segments(ctx->sweeps);
   std::vector<int> seg_len(nseg, ctx->sweeps / nseg);
   for (int j = 0; j < ctx->sweeps % nseg; ++j) seg_len[j]++;
   for (int l = Lmax - 1; l >= 0; --l) {
-    for (int it = 0; it < 5; ++it) {
-      Op pop{OP_HSPREP};
-      pop.offset = static_cast<int>(hp_table.size());
-      for (auto& t : tasks) {
-        if (l >= t.L) continue;
-        const PairDesc& p = g.pairs[t.k];
-        const int sa = t.dir == 0 ? 0 : 1, sb = 1 - sa;
-        PrepTask q{};
-        q.a = p.pyr[sa][l];
-        q.b = p.pyr[sb][l];
-        // u0: zero at the coarsest level's first warp, the coarser flow
-        // upsampled at a finer level's first warp, else the previous warp's
-        q.mode = (l == t.L - 1 && it == 0) ? 0 : (it == 0 ? 2 : 1);
-        q.u_in = t.U[t.cur];
-        q.v_in = t.V[t.cur];
-        q.wc = q.mode == 2 ? t.dims[l + 1][0] : 0;
-        q.hc = q.mode == 2 ? t.dims[l + 1][1] : 0;
-        q.w = t.dims[l][0];
-        q.h = t.dims[l][1];
-        for (int b = 0; b < 4; ++b) (&q.kgx)[b] = t.K[b];
-        if (q.mode != 1) {
-          q.u0_out = t.U[1 - t.cur];
-          q.v0_out = t.V[1 - t.cur];
-          t.cur ^= 1;
-        }
-        hp_table.push_back(q);
-        pop.max_w = std::max(pop.max_w, q.w);
-        pop.max_h = std::max(pop.max_h, q.h);
+    int n_l = 0, w_l = 0, h_l = 0;
+    for (const auto& t : tasks)
+      if (l < t.L) {
+        ++n_l;
+        w_l = std::max(w_l, t.dims[l][0]);
+        h_l = std::max(h_l, t.dims[l][1]);
       }
-      pop.count = static_cast<int>(hp_table.size()) - pop.offset;
-      if (pop.count) plan.push_back(pop);
+    const bool fuse = n_l > 0 && hs_fuse_wanted(n_l, w_l, h_l, seg_len[0]);
+    for (int it = 0; it < 5; ++it) {
+      // u0: zero at the coarsest level's first warp, the coarser flow
+      // upsampled at a finer level's first warp, else the previous warp's
+      auto lin_mode = [&](const TaskState& t) {
+        return (l == t.L - 1 && it == 0) ? 0 : (it == 0 ? 2 : 1);
+      };
+      if (!fuse) {
+        Op pop{OP_HSPREP};
+        pop.offset = static_cast<int>(hp_table.size());
+        for (auto& t : tasks) {
+          if (l >= t.L) continue;
+          const PairDesc& p = g.pairs[t.k];
+          const int sa = t.dir == 0 ? 0 : 1, sb = 1 - sa;
+          PrepTask q{};
+          q.a = p.pyr[sa][l];
+          q.b = p.pyr[sb][l];
+          q.mode = lin_mode(t);
+          q.u_in = t.U[t.cur];
+          q.v_in = t.V[t.cur];
+          q.wc = q.mode == 2 ? t.dims[l + 1][0] : 0;
+          q.hc = q.mode == 2 ? t.dims[l + 1][1] : 0;
+          q.w = t.dims[l][0];
+          q.h = t.dims[l][1];
+          for (int b = 0; b < 4; ++b) (&q.kgx)[b] = t.K[b];
+          if (q.mode != 1) {
+            q.u0_out = t.U[1 - t.cur];
+            q.v0_out = t.V[1 - t.cur];
+            t.cur ^= 1;
+          }
+          hp_table.push_back(q);
+          pop.max_w = std::max(pop.max_w, q.w);
+          pop.max_h = std::max(pop.max_h, q.h);
+        }
+        pop.count = static_cast<int>(hp_table.size()) - pop.offset;
+        if (pop.count) plan.push_back(pop);
+      }
       for (int j = 0; j < nseg; ++j) {
         Op op{OP_HS};
         op.sweeps = seg_len[j];
+        op.fuse = (fuse && j == 0) ? 1 : 0;
         op.offset = static_cast<int>(hs_table.size());
         for (auto& t : tasks) {
           if (l >= t.L) continue;
@@ -558,9 +577,13 @@ int build_context(const stitch_b200_init* in, int device,
           h.v_out = t.V[1 - t.cur];
           h.w = t.dims[l][0];
           h.h = t.dims[l][1];
-          h.zero_invalid = (l == 0 && it == 4 && j == nseg - 1) ? 1 : 0;
-          h.mask_a = p.crop_cor[sa];
-          h.mask_b = p.crop_cor[sb];
+          if (op.fuse) {
+            h.lin_a = p.pyr[sa][l];
+            h.lin_b = p.pyr[sb][l];
+            h.lin_mode = lin_mode(t);
+            h.wc = h.lin_mode == 2 ? t.dims[l + 1][0] : 0;
+            h.hc = h.lin_mode == 2 ? t.dims[l + 1][1] : 0;
+          }
           t.cur ^= 1;
           hs_table.push_back(h);
           op.max_w = std::max(op.max_w, h.w);
@@ -1176,6 +1199,14 @@ int stitch_b200_debug_flow(stitch_b200_ctx* h, int k, int dir, float* u, float* 
   const size_t n = static_cast<size_t>(p.w) * p.h;
   CUDA_TRY(cudaMemcpy(u, p.flow_u[dir], n * sizeof(float), cudaMemcpyDeviceToHost));
   CUDA_TRY(cudaMemcpy(v, p.flow_v[dir], n * sizeof(float), cudaMemcpyDeviceToHost));
+  // dense_flow's final zeroing where either crop is invalid (flow.cpp:178-185)
+  // is applied by the flow's consumer (fused_pixel) instead of being written
+  // into the plane; apply it here so the readback is the reference's field
+  std::vector<uchar4> ca(n), cb(n);
+  CUDA_TRY(cudaMemcpy(ca.data(), p.crop_cor[0], n * sizeof(uchar4), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(cb.data(), p.crop_cor[1], n * sizeof(uchar4), cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < n; ++i)
+    if (!ca[i].w || !cb[i].w) u[i] = v[i] = 0.0f;
   return STITCH_B200_OK;
 }
 

@@ -155,18 +155,20 @@ struct CanvasParams {
 };
 
 struct HsTask {
-  const float* kgx;
-  const float* kgy;
-  const float* kcc;
-  const float* kdn;
-  const float* u_in;  // state at the start of the segment
-  const float* v_in;
+  float* kgx;  // constant planes: read by plain segments, written (output
+  float* kgy;  // tile) by a segment that fuses the linearisation
+  float* kcc;
+  float* kdn;
+  const float* u_in;  // state at the start of the segment (fused: the u0
+  const float* v_in;  // source of lin_mode, see PrepTask::mode)
   float* u_out;
   float* v_out;
   int w, h;
-  int zero_invalid;  // final write: zero where either crop is invalid
-  const uchar4* mask_a;
-  const uchar4* mask_b;
+  // fused linearisation (first segment of a warp iteration)
+  const float* lin_a;  // luma of the first / second image at this level
+  const float* lin_b;
+  int lin_mode;  // 0: u0 = 0, 1: u0 = u_in, 2: u_in upsampled from wc x hc
+  int wc, hc;
 };
 
 struct PyrTask {
@@ -204,8 +206,14 @@ int hs_segments(int sweeps);
 cudaError_t prepare_hs(int sweeps);
 void launch_hs_prepare(const PrepTask* tasks, int n, int max_w, int max_h, float alpha2,
                        cudaStream_t s);
-void launch_hs_iter(const HsTask* tasks, int n, int max_w, int max_h, int sweeps,
-                    cudaStream_t s);
+// fuse_lin: the segment first linearises the warp (HsTask lin_* fields)
+void launch_hs_iter(const HsTask* tasks, int n, int max_w, int max_h, int sweeps, int fuse_lin,
+                    float alpha2, cudaStream_t s);
+// the fused linearisation serves segments of up to this many sweeps
+int hs_fuse_max_sweeps();
+// whether the first segment of a warp iteration with these dimensions should
+// fuse the linearisation (the launch it would use supports and profits from it)
+int hs_fuse_wanted(int n, int max_w, int max_h, int sweeps);
 // mode 0: whole canvas; 1: outside every pair's bounds (flow-independent);
 // 2: inside the bounds.  Modes 1 + 2 together cover the canvas once.
 void launch_canvas(const CanvasParams& P, const Geometry* g, DevState* st, uchar4* pano,
