@@ -158,15 +158,20 @@ def pair_levels(p, levels=4):
     return dims
 
 
-def kernel_model(state, wl, sweeps=10, warps=5):
+def kernel_model(state, wl, sweeps=10, warps=5, lin_levels=None):
     """Algorithmic HBM bytes (and FP32 flops for the flow) per frame, per
-    kernel family."""
+    kernel family.  lin_levels: how many of the finest
+    levels run the separate linearisation launch (the coarser ones fuse it
+    into their first Jacobi segment); None = all."""
     pairs = state.pairs
     o = [(p.bounds[2] - p.bounds[0]) * (p.bounds[3] - p.bounds[1]) for p in pairs]
     P = state.canvas_width * state.canvas_height
     in_px = wl["views"] * wl["width"] * wl["height"]
     lv = [pair_levels(p) for p in pairs]
     flow_px = 2 * sum(a * b for dims in lv for a, b in dims)  # both directions, all levels
+    nl = max((len(d) for d in lv), default=0) if lin_levels is None else lin_levels
+    lin_px = 2 * sum(a * b for dims in lv for a, b in dims[:nl])  # separately linearised
+    fused_px = flow_px - lin_px
     coarse_px = 2 * sum(a * b for dims in lv for a, b in dims[:-1])  # finer levels (upsampled u0)
     segs = int(os.environ.get("STITCH_B200_HS_SEGS", "2"))
     return {
@@ -180,9 +185,10 @@ def kernel_model(state, wl, sweeps=10, warps=5):
         "flow_prepare": dict(bytes=sum(2 * (4 + 4 + 4) * n for n in o)),
         # per warp iteration and pixel: u0 (8) + a (4) + b (4) read, 4 constant planes
         # (16) written; + u0 materialised (8) on each level's first warp
-        "hs_linearize": dict(bytes=warps * 32 * flow_px + 8 * flow_px),
-        # per segment and pixel: state (8) + constants (16) read, state (8) written
-        "hs_sweeps": dict(bytes=warps * segs * 32 * flow_px,
+        "hs_linearize": dict(bytes=warps * 32 * lin_px + 8 * lin_px),
+        # per segment and pixel: state (8) + constants (16) read, state (8) written; a
+        # fused first segment reads u0 (8) + a, b (8), writes constants (16) + state (8)
+        "hs_sweeps": dict(bytes=warps * segs * 32 * flow_px + warps * 8 * fused_px,
                           flops=warps * sweeps * 17 * flow_px),
         # per canvas pixel one RGBA source pixel read + uchar4 write; overlap pixels add
         # raw crops (8) + corrected crop samples (8) + flows (16) + weight (4)
@@ -354,7 +360,8 @@ def run_b200(args, rank, world, local_rank):
     clocks.stop()
 
     peak, peak_kind = load_peaks()
-    model = kernel_model(state, wl)
+    lin_launches = per_kind.get("hs_linearize", [0.0, 0])[1]
+    model = kernel_model(state, wl, lin_levels=lin_launches // 5)
     total_kernel_ms = sum(v[0] for v in per_kind.values())
     clk = clocks.summary()
     fp32_peak = 148 * 128 * (clk.get("sm_mhz") or 1965.0) * 1e6 / 1e12  # add/mul, no FMA
