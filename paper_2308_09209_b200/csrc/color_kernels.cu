@@ -146,9 +146,36 @@ __device__ void pair_solve(const PairDesc& p, int k, DevState* __restrict__ st) 
     normal[i] = static_cast<double>(sx[i]);
     xty[i] = static_cast<double>(sy[i]);
   }
-  sym3_eigen(normal, sv);
+  // Rank guard (color_transfer.cpp:88-91): sigma_min < 1e-8 sigma_max, with
+  // sigma = the eigenvalues of the PSD normal matrix.  The decision is
+  // settled without the eigensolve whenever det / tr^3 bounds it with
+  // margin: lambda_min / lambda_max >= det / tr^3 (lambda_max <= tr) and
+  // <= sqrt(27 det / tr^3) (lambda_max >= tr / 3, lambda_min^2 <= det /
+  // lambda_max); det carries a generous rounding bound.  The 2 % margins
+  // dwarf the eigensolver's ~1e-15 relative error, so the outcome equals
+  // the full cyclic-Jacobi test, which runs only in the narrow band between.
+  int rank_ok = -1;
+  {
+    const double* a = normal;
+    const double c0 = a[4] * a[8] - a[5] * a[7];
+    const double c1 = a[3] * a[8] - a[5] * a[6];
+    const double c2 = a[3] * a[7] - a[4] * a[6];
+    const double det = (a[0] * c0 - a[1] * c1) + a[2] * c2;
+    const double mag = fabs(a[0]) * (fabs(a[4] * a[8]) + fabs(a[5] * a[7])) +
+                       fabs(a[1]) * (fabs(a[3] * a[8]) + fabs(a[5] * a[6])) +
+                       fabs(a[2]) * (fabs(a[3] * a[7]) + fabs(a[4] * a[6]));
+    const double err = 1e-13 * mag;
+    const double tr = (a[0] + a[4]) + a[8];
+    const double tr3 = tr * tr * tr;
+    if (tr > 0.0 && det - err > 1.02e-8 * tr3) rank_ok = 1;
+    else if (tr > 0.0 && 27.0 * (det + err) < 0.98e-16 * tr3) rank_ok = 0;
+  }
+  if (rank_ok < 0) {
+    sym3_eigen(normal, sv);
+    rank_ok = sv[2] < 1e-8 * sv[0] ? 0 : 1;
+  }
   int degraded = 0;
-  if (total < 3 || sv[2] < 1e-8 * sv[0]) {
+  if (total < 3 || !rank_ok) {
     for (int i = 0; i < 9; ++i) m[i] = (i % 4 == 0) ? 1.0 : 0.0;  // RankDeficient
     degraded = 1;
   } else {
