@@ -416,7 +416,7 @@ int build_context(const stitch_b200_init* in, int device,
     int dims[kMaxLevels][2];
     float* U[2];
     float* V[2];
-    float* K[4];  // gx, gy, c, denom planes of the current warp iteration
+    float4* KQ;  // (gx, gy, c, denom) per pixel of the current warp iteration
     int cur;
   };
   std::vector<TaskState> tasks;
@@ -455,7 +455,7 @@ int build_context(const stitch_b200_init* in, int device,
         CUDA_TRY(ctx->alloc(&t.U[b], p.w * p.h));
         CUDA_TRY(ctx->alloc(&t.V[b], p.w * p.h));
       }
-      for (int b = 0; b < 4; ++b) CUDA_TRY(ctx->alloc(&t.K[b], p.w * p.h));
+      CUDA_TRY(ctx->alloc(&t.KQ, p.w * p.h));
       t.cur = 0;
       tasks.push_back(t);
     }
@@ -544,7 +544,7 @@ int build_context(const stitch_b200_init* in, int device,
           q.hc = q.mode == 2 ? t.dims[l + 1][1] : 0;
           q.w = t.dims[l][0];
           q.h = t.dims[l][1];
-          for (int b = 0; b < 4; ++b) (&q.kgx)[b] = t.K[b];
+          q.kq = t.KQ;
           if (q.mode != 1) {
             q.u0_out = t.U[1 - t.cur];
             q.v0_out = t.V[1 - t.cur];
@@ -567,10 +567,7 @@ int build_context(const stitch_b200_init* in, int device,
           const PairDesc& p = g.pairs[t.k];
           const int sa = t.dir == 0 ? 0 : 1, sb = 1 - sa;
           HsTask h{};
-          h.kgx = t.K[0];
-          h.kgy = t.K[1];
-          h.kcc = t.K[2];
-          h.kdn = t.K[3];
+          h.kq = t.KQ;
           h.u_in = t.U[t.cur];
           h.v_in = t.V[t.cur];
           h.u_out = t.U[1 - t.cur];

@@ -116,10 +116,7 @@ struct PrepTask {
   int w, h;
   float* u0_out;  // modes 0 and 2: u0 materialised here (the sweeps' start state)
   float* v0_out;
-  float* kgx;
-  float* kgy;
-  float* kcc;
-  float* kdn;
+  float4* kq;  // Jacobi constants per pixel: (gx, gy, c, denom)
 };
 
 // One segment of Jacobi sweeps (flow.cpp:109-134) on constant planes.
@@ -155,10 +152,9 @@ struct CanvasParams {
 };
 
 struct HsTask {
-  float* kgx;  // constant planes: read by plain segments, written (output
-  float* kgy;  // tile) by a segment that fuses the linearisation
-  float* kcc;
-  float* kdn;
+  float4* kq;  // Jacobi constants (gx, gy, c, denom) per pixel: read by plain
+               // segments, written (output tile) by a segment that fuses the
+               // linearisation
   const float* u_in;  // state at the start of the segment (fused: the u0
   const float* v_in;  // source of lin_mode, see PrepTask::mode)
   float* u_out;
