@@ -97,8 +97,9 @@ __device__ __forceinline__ bool fused_pixel(const CanvasParams& P, const CanvasP
   // dense_flow zeroes both fields where either crop is invalid
   // (flow.cpp:178-185); the Jacobi kernels leave that to this consumer
   const bool valid = p.crop_cor[0][i].w && p.crop_cor[1][i].w;
-  const float uij = valid ? p.fu[0][i] : 0.0f, vij = valid ? p.fv[0][i] : 0.0f;
-  const float uji = valid ? p.fu[1][i] : 0.0f, vji = valid ? p.fv[1][i] : 0.0f;
+  const float2 fij = valid ? p.fuv[0][i] : make_float2(0.0f, 0.0f);
+  const float2 fji = valid ? p.fuv[1][i] : make_float2(0.0f, 0.0f);
+  const float uij = fij.x, vij = fij.y, uji = fji.x, vji = fji.y;
   float ri, gi, bi, rj, gj, bj;
   const bool vi = sample_crop(p.crop_cor[0], p.w, p.h,
                               static_cast<double>(static_cast<float>(dx) + wi * uij),

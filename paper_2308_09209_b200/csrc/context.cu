@@ -94,7 +94,7 @@ struct Ctx {
   int ring_pos = 0;
   DevReport* h_report = nullptr;  // one per slot (pinned)
   std::vector<int> pair_levels;
-  float* d_zero = nullptr;
+  float2* d_zero = nullptr;
   CanvasParams cparams{};
 
   ~Ctx() {
@@ -414,8 +414,7 @@ int build_context(const stitch_b200_init* in, int device,
   struct TaskState {
     int k, dir, L;
     int dims[kMaxLevels][2];
-    float* U[2];
-    float* V[2];
+    float2* UV[2];  // (u, v) ping-pong
     float4* KQ;  // (gx, gy, c, denom) per pixel of the current warp iteration
     int cur;
   };
@@ -426,8 +425,7 @@ int build_context(const stitch_b200_init* in, int device,
     PairDesc& p = g.pairs[k];
     if (!p.flow_ok) {
       for (int d = 0; d < 2; ++d) {
-        p.flow_u[d] = ctx->d_zero;
-        p.flow_v[d] = ctx->d_zero;
+        p.flow_uv[d] = ctx->d_zero;
       }
       continue;
     }
@@ -452,8 +450,7 @@ int build_context(const stitch_b200_init* in, int device,
       t.L = L;
       std::memcpy(t.dims, dims, sizeof(dims));
       for (int b = 0; b < 2; ++b) {
-        CUDA_TRY(ctx->alloc(&t.U[b], p.w * p.h));
-        CUDA_TRY(ctx->alloc(&t.V[b], p.w * p.h));
+        CUDA_TRY(ctx->alloc(&t.UV[b], p.w * p.h));
       }
       CUDA_TRY(ctx->alloc(&t.KQ, p.w * p.h));
       t.cur = 0;
@@ -538,16 +535,14 @@ int build_context(const stitch_b200_init* in, int device,
           q.a = p.pyr[sa][l];
           q.b = p.pyr[sb][l];
           q.mode = lin_mode(t);
-          q.u_in = t.U[t.cur];
-          q.v_in = t.V[t.cur];
+          q.uv_in = t.UV[t.cur];
           q.wc = q.mode == 2 ? t.dims[l + 1][0] : 0;
           q.hc = q.mode == 2 ? t.dims[l + 1][1] : 0;
           q.w = t.dims[l][0];
           q.h = t.dims[l][1];
           q.kq = t.KQ;
           if (q.mode != 1) {
-            q.u0_out = t.U[1 - t.cur];
-            q.v0_out = t.V[1 - t.cur];
+            q.uv0_out = t.UV[1 - t.cur];
             t.cur ^= 1;
           }
           hp_table.push_back(q);
@@ -568,10 +563,8 @@ int build_context(const stitch_b200_init* in, int device,
           const int sa = t.dir == 0 ? 0 : 1, sb = 1 - sa;
           HsTask h{};
           h.kq = t.KQ;
-          h.u_in = t.U[t.cur];
-          h.v_in = t.V[t.cur];
-          h.u_out = t.U[1 - t.cur];
-          h.v_out = t.V[1 - t.cur];
+          h.uv_in = t.UV[t.cur];
+          h.uv_out = t.UV[1 - t.cur];
           h.w = t.dims[l][0];
           h.h = t.dims[l][1];
           if (op.fuse) {
@@ -593,8 +586,7 @@ int build_context(const stitch_b200_init* in, int device,
   }
   for (auto& t : tasks) {
     PairDesc& p = g.pairs[t.k];
-    p.flow_u[t.dir] = t.U[t.cur];
-    p.flow_v[t.dir] = t.V[t.cur];
+    p.flow_uv[t.dir] = t.UV[t.cur];
   }
   plan.push_back({OP_EVENT, 0, 0, 0, 0, 0, 3});
   plan.push_back({OP_CANVAS});
@@ -654,8 +646,7 @@ int build_context(const stitch_b200_init* in, int device,
       for (int s2 = 0; s2 < 2; ++s2) {
         q.crop_raw[s2] = p.crop_raw[s2];
         q.crop_cor[s2] = p.crop_cor[s2];
-        q.fu[s2] = p.flow_u[s2];
-        q.fv[s2] = p.flow_v[s2];
+        q.fuv[s2] = p.flow_uv[s2];
       }
     }
   }
@@ -1194,8 +1185,12 @@ int stitch_b200_debug_flow(stitch_b200_ctx* h, int k, int dir, float* u, float* 
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   const PairDesc& p = ctx->hg.pairs[k];
   const size_t n = static_cast<size_t>(p.w) * p.h;
-  CUDA_TRY(cudaMemcpy(u, p.flow_u[dir], n * sizeof(float), cudaMemcpyDeviceToHost));
-  CUDA_TRY(cudaMemcpy(v, p.flow_v[dir], n * sizeof(float), cudaMemcpyDeviceToHost));
+  std::vector<float2> uv(n);
+  CUDA_TRY(cudaMemcpy(uv.data(), p.flow_uv[dir], n * sizeof(float2), cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < n; ++i) {
+    u[i] = uv[i].x;
+    v[i] = uv[i].y;
+  }
   // dense_flow's final zeroing where either crop is invalid (flow.cpp:178-185)
   // is applied by the flow's consumer (fused_pixel) instead of being written
   // into the plane; apply it here so the readback is the reference's field

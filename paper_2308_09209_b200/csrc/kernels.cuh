@@ -40,8 +40,7 @@ struct PairDesc {
   uchar4* crop_raw[2];
   uchar4* crop_cor[2];
   float* pyr[2][kMaxLevels];
-  const float* flow_u[2];  // final level-0 flow, dir 0: view->partner
-  const float* flow_v[2];
+  const float2* flow_uv[2];  // final level-0 flow (u, v), dir 0: view->partner
 };
 
 // Per-pair integer moments of one frame (k_pair_stats -> k_pair_solve).
@@ -109,13 +108,11 @@ struct Geometry {
 struct PrepTask {
   const float* a;  // luma of the first image at this level
   const float* b;  // luma of the second image
-  int mode;        // 0: u0 = 0, 1: u0 = (u_in, v_in), 2: upsample (u_in, v_in) from wc x hc
-  const float* u_in;
-  const float* v_in;
+  int mode;        // 0: u0 = 0, 1: u0 = uv_in, 2: upsample uv_in from wc x hc
+  const float2* uv_in;
   int wc, hc;
   int w, h;
-  float* u0_out;  // modes 0 and 2: u0 materialised here (the sweeps' start state)
-  float* v0_out;
+  float2* uv0_out;  // modes 0 and 2: u0 materialised here (the sweeps' start state)
   float4* kq;  // Jacobi constants per pixel: (gx, gy, c, denom)
 };
 
@@ -136,8 +133,7 @@ struct CanvasPair {
   const float* theta;
   uchar4* crop_raw[2];
   const uchar4* crop_cor[2];
-  const float* fu[2];
-  const float* fv[2];
+  const float2* fuv[2];
 };
 
 struct CanvasParams {
@@ -155,15 +151,14 @@ struct HsTask {
   float4* kq;  // Jacobi constants (gx, gy, c, denom) per pixel: read by plain
                // segments, written (output tile) by a segment that fuses the
                // linearisation
-  const float* u_in;  // state at the start of the segment (fused: the u0
-  const float* v_in;  // source of lin_mode, see PrepTask::mode)
-  float* u_out;
-  float* v_out;
+  const float2* uv_in;  // state (u, v) at the start of the segment (fused:
+                        // the u0 source of lin_mode, see PrepTask::mode)
+  float2* uv_out;
   int w, h;
   // fused linearisation (first segment of a warp iteration)
   const float* lin_a;  // luma of the first / second image at this level
   const float* lin_b;
-  int lin_mode;  // 0: u0 = 0, 1: u0 = u_in, 2: u_in upsampled from wc x hc
+  int lin_mode;  // 0: u0 = 0, 1: u0 = uv_in, 2: uv_in upsampled from wc x hc
   int wc, hc;
 };
 
