@@ -423,6 +423,7 @@ def run_b200(args, rank, world, local_rank):
                 "steps": e2e_steps, "streams": 1,
                 "api": "stitch_b200_submit/stitch_b200_wait (2 frames in flight, pinned host)",
                 "sync_process_value": round(e2e_sync, 2)},
+        "realtime_streams": round(value / 30.0, 1),  # sustained 30 fps streams
         "gpu_launches": launches * args.steps * ns,
         "kernels_per_frame": launches,
         "roofline": roofline,
@@ -466,9 +467,22 @@ def cpu_baseline(args, wl, sample_seconds=15.0, max_frames=None):
         if el >= sample_seconds or (max_frames and n >= max_frames):
             break
     st.close()
-    return {"value": round(n / el, 4), "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{n} frames of the same workload after 1 warm-up frame "
-                      f"({el:.1f} s, oracle/liboracle.so, {threads} OpenMP threads)"}
+    out = {"value": round(n / el, 4), "unit": UNIT, "cores": threads, "kind": "port",
+           "sample": f"{n} frames of the same workload after 1 warm-up frame "
+                     f"({el:.1f} s, oracle/liboracle.so, {threads} OpenMP threads)"}
+    # single-thread rate (the paper's Table-4 shaped CPU ratio), a shorter sample
+    st1 = oracle_state_for(sc, 1)
+    n1, t1 = 0, time.perf_counter()
+    while True:
+        st1.process(frames[n1 % 2])
+        n1 += 1
+        el1 = time.perf_counter() - t1
+        if el1 >= sample_seconds / 3 or (max_frames and n1 >= max_frames):
+            break
+    st1.close()
+    out["value_1_thread"] = round(n1 / el1, 4)
+    out["sample_1_thread"] = f"{n1} frames, {el1:.1f} s, 1 thread"
+    return out
 
 
 def run_reference(args):

@@ -154,8 +154,9 @@ int stitch_b200_create(const stitch_b200_init* init, int device,
                        stitch_b200_ctx** out);
 
 /* Standalone initialize (pipeline.cpp:209-257 with refinement off): camera
- * homographies, canvas, pairs, overlap bounds and blend weights.  The warp
- * masks are evaluated on the device with the per-frame warp sampler. */
+ * homographies and canvas on the host; warp masks, view footprints, overlap
+ * bounds and chamfer blend weights (rebuild_pair_geometry,
+ * pipeline.cpp:181-205) on the device. */
 int stitch_b200_initialize(const stitch_b200_config* cfg, int device,
                            stitch_b200_ctx** out);
 
@@ -163,6 +164,19 @@ int stitch_b200_initialize(const stitch_b200_config* cfg, int device,
  * windows, threshold history and frame counter are kept. */
 int stitch_b200_update_geometry(stitch_b200_ctx* ctx,
                                 const stitch_b200_init* init);
+
+/* Re-refinement from new view->reference homographies (the refined
+ * `warp_maps[v].h`, row-major, planar canvas only): the canvas
+ * (compute_canvas, geometry.cpp:147-171), the inverse maps and the whole pair
+ * geometry (rebuild_pair_geometry, pipeline.cpp:181-205) are recomputed --
+ * the pair geometry on the device -- and the windows, threshold history and
+ * frame counter are carried over as run_sequence does (pipeline.cpp:395-406).
+ * The pair set is kept. */
+int stitch_b200_update_maps(stitch_b200_ctx* ctx, const double* maps /* n_views * 9 */);
+
+/* The unrefined view->reference homographies initialize() derives from the
+ * camera models (pipeline.cpp:219-229), row-major, n_views * 9 doubles. */
+int stitch_b200_camera_maps(const stitch_b200_config* cfg, double* maps);
 
 void stitch_b200_destroy(stitch_b200_ctx* ctx);
 

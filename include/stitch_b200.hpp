@@ -218,6 +218,14 @@ class PipelineState {
     return h;
   }
   int n_pairs() const { return stitch_b200_n_pairs(ctx_.get()); }
+  // Re-refinement from new view->reference homographies (row-major, 9 per
+  // view): canvas and pair geometry rebuilt on the device, temporal state
+  // kept (run_sequence's rerefine branch, pipeline.cpp:395-406).
+  void update_maps(const std::vector<std::array<double, 9>>& maps) {
+    std::vector<double> flat;
+    for (const auto& m : maps) flat.insert(flat.end(), m.begin(), m.end());
+    check(stitch_b200_update_maps(ctx_.get(), flat.data()));
+  }
 
  private:
   std::unique_ptr<stitch_b200_ctx, void (*)(stitch_b200_ctx*)> ctx_{nullptr, &stitch_b200_destroy};

@@ -27,6 +27,7 @@ from .pipeline import (  # noqa: F401
     SynthScene,
     SynthSpec,
     ViewSetup,
+    camera_maps,
     create_from_init,
     initialize,
     process_frame,

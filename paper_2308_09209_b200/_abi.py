@@ -78,6 +78,8 @@ SYMBOLS = [
     ("stitch_b200_create", C.c_int, [C.POINTER(Init), C.c_int, C.POINTER(C.c_void_p)]),
     ("stitch_b200_initialize", C.c_int, [C.POINTER(Config), C.c_int, C.POINTER(C.c_void_p)]),
     ("stitch_b200_update_geometry", C.c_int, [C.c_void_p, C.POINTER(Init)]),
+    ("stitch_b200_update_maps", C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
+    ("stitch_b200_camera_maps", C.c_int, [C.POINTER(Config), C.POINTER(C.c_double)]),
     ("stitch_b200_destroy", None, [C.c_void_p]),
     ("stitch_b200_canvas", C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                      C.POINTER(C.c_double), C.POINTER(C.c_double)]),

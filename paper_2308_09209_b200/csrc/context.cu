@@ -176,8 +176,6 @@ int validate_init(const stitch_b200_init* in) {
   return STITCH_B200_OK;
 }
 
-// Warp validity masks of every view over the full canvas, evaluated on the
-// device with the per-frame sampler's geometry (init only).
 // Lift tables of the cylindrical canvas (extension); empty for planar.
 struct LiftTables {
   std::vector<double> s, c, h;
@@ -196,43 +194,15 @@ LiftTables make_lift(const stitch_b200_init* in) {
   return t;
 }
 
-// Warp validity masks of every view over the full canvas, evaluated on the
-// device with the per-frame sampler's geometry (init only).
-int compute_masks(int device, Geometry geom, const LiftTables& lt, int n_views,
-                  std::vector<std::vector<std::uint8_t>>& masks) {
+// Init geometry on the device (geometry_kernels.cu): view footprints and,
+// for the given pairs, overlap bounds + blend weights.
+int init_geometry(int device, const Geometry& geom, const LiftTables& lt, int n_views,
+                  const std::vector<std::pair<int, int>>& pairs, std::vector<ViewFootprint>& views,
+                  std::vector<PairGeometry>& pair_geo) {
   CUDA_TRY(cudaSetDevice(device));
-  Geometry* d = nullptr;
-  std::uint8_t* dm = nullptr;
-  double* dl = nullptr;
-  const size_t n = static_cast<size_t>(geom.canvas_w) * geom.canvas_h;
-  CUDA_TRY(cudaMalloc(&d, sizeof(Geometry)));
-  cudaError_t e = cudaMalloc(&dm, n);
-  if (e == cudaSuccess && geom.projection == 1) {
-    e = cudaMalloc(&dl, sizeof(double) * (lt.s.size() + lt.c.size() + lt.h.size()));
-    if (e == cudaSuccess) {
-      geom.lift_sin = dl;
-      geom.lift_cos = dl + lt.s.size();
-      geom.lift_h = dl + lt.s.size() + lt.c.size();
-      e = cudaMemcpy(dl, lt.s.data(), sizeof(double) * lt.s.size(), cudaMemcpyHostToDevice);
-      if (e == cudaSuccess)
-        e = cudaMemcpy(dl + lt.s.size(), lt.c.data(), sizeof(double) * lt.c.size(),
-                       cudaMemcpyHostToDevice);
-      if (e == cudaSuccess)
-        e = cudaMemcpy(dl + lt.s.size() + lt.c.size(), lt.h.data(), sizeof(double) * lt.h.size(),
-                       cudaMemcpyHostToDevice);
-    }
-  }
-  if (e == cudaSuccess) e = cudaMemcpy(d, &geom, sizeof(Geometry), cudaMemcpyHostToDevice);
-  masks.assign(n_views, std::vector<std::uint8_t>(n));
-  for (int v = 0; v < n_views && e == cudaSuccess; ++v) {
-    launch_warp_mask(d, v, dm, 0);
-    e = cudaGetLastError();
-    if (e == cudaSuccess) e = cudaMemcpy(masks[v].data(), dm, n, cudaMemcpyDeviceToHost);
-  }
-  cudaFree(d);
-  cudaFree(dm);
-  if (dl) cudaFree(dl);
-  if (e != cudaSuccess) return fail(STITCH_B200_CudaError, cudaGetErrorString(e));
+  CUDA_TRY(gpu_init_geometry(geom, lt.s.data(), lt.c.data(), lt.h.data(),
+                             static_cast<int>(lt.s.size()), static_cast<int>(lt.h.size()), n_views,
+                             pairs, views, pair_geo));
   return STITCH_B200_OK;
 }
 
@@ -290,8 +260,7 @@ int enqueue_op(Ctx* ctx, const Op& op, cudaStream_t s, int slot = 0) {
 }
 
 int build_context(const stitch_b200_init* in, int device,
-                  const std::vector<std::vector<std::uint8_t>>* masks_in,
-                  std::unique_ptr<Ctx>& out) {
+                  const std::vector<ViewFootprint>* views_in, std::unique_ptr<Ctx>& out) {
   int rc = validate_init(in);
   if (rc) return rc;
   auto ctx = std::make_unique<Ctx>();
@@ -316,8 +285,8 @@ int build_context(const stitch_b200_init* in, int device,
                    : 0;
 
   // view footprints (bbox of the warp mask); EmptyProjection if none.
-  std::vector<std::vector<std::uint8_t>> masks_local;
-  const std::vector<std::vector<std::uint8_t>>* masks = masks_in;
+  std::vector<ViewFootprint> views_local;
+  const std::vector<ViewFootprint>* views = views_in;
   const LiftTables lift = make_lift(in);
   if (g.projection == 1) {
     if (!(in->cyl_focal > 0.0) ||
@@ -334,17 +303,18 @@ int build_context(const stitch_b200_init* in, int device,
     g.lift_cos = dl + lift.s.size();
     g.lift_h = dl + lift.s.size() + lift.c.size();
   }
-  if (!masks) {
-    rc = compute_masks(device, g, lift, in->n_views, masks_local);
+  if (!views) {
+    std::vector<PairGeometry> none;
+    rc = init_geometry(device, g, lift, in->n_views, {}, views_local, none);
     if (rc) return rc;
-    masks = &masks_local;
+    views = &views_local;
   }
   for (int v = 0; v < in->n_views; ++v) {
-    int b[4];
-    if (!hg_ns::mask_bbox((*masks)[v].data(), g.canvas_w, g.canvas_h, b))
-      return fail(STITCH_B200_EmptyProjection, "a view projects to no canvas pixel");
-    for (int i = 0; i < 4; ++i) g.views[v].bbox[i] = b[i];
-    hg_ns::mask_column_gap((*masks)[v].data(), g.canvas_w, g.canvas_h, b, g.views[v].gap);
+    const ViewFootprint& f = (*views)[v];
+    if (f.empty) return fail(STITCH_B200_EmptyProjection, "a view projects to no canvas pixel");
+    for (int i = 0; i < 4; ++i) g.views[v].bbox[i] = f.bbox[i];
+    g.views[v].gap[0] = f.gap[0];
+    g.views[v].gap[1] = f.gap[1];
   }
 
   // buffers
@@ -925,50 +895,43 @@ int stitch_b200_initialize(const stitch_b200_config* cfg, int device, stitch_b20
   if (canvas.width <= 0 || canvas.height <= 0 ||
       static_cast<long long>(canvas.width) * canvas.height > (1ll << 31))
     return fail(STITCH_B200_ConfigurationError, "canvas size out of range");
-  // rebuild_pair_geometry (pipeline.cpp:181-205): warp masks on the device,
-  // overlap bounds and chamfer blend weights on the host (init only).
+  // rebuild_pair_geometry (pipeline.cpp:181-205), all on the device: warp
+  // masks, view footprints, overlap bounds, chamfer blend weights.
   Geometry g{};
   fill_views(g, &in);
-  std::vector<std::vector<std::uint8_t>> masks;
-  int rc = compute_masks(device, g, make_lift(&in), cfg->n_views, masks);
-  if (rc) return rc;
   const int topo = (cfg->projection == 1 && cfg->topology == 0) ? 3 : cfg->topology;
   const auto pairs = hg_ns::build_pairs(cfg->n_views, cfg->reference, topo);
   if (static_cast<int>(pairs.size()) > kMaxPairs)
     return fail(STITCH_B200_ConfigurationError, "too many pairs");
-  std::vector<std::vector<float>> thetas(pairs.size());
+  std::vector<std::pair<int, int>> vp;
+  for (const auto& pr : pairs) vp.emplace_back(pr.view, pr.partner);
+  std::vector<ViewFootprint> views;
+  std::vector<PairGeometry> pgeo;
+  int rc = init_geometry(device, g, make_lift(&in), cfg->n_views, vp, views, pgeo);
+  if (rc) return rc;
   in.n_pairs = static_cast<int>(pairs.size());
   for (size_t k = 0; k < pairs.size(); ++k) {
-    int b[4];
-    if (!hg_ns::overlap_bounds(masks[pairs[k].view].data(), masks[pairs[k].partner].data(),
-                               canvas.width, canvas.height, b))
-      return fail(STITCH_B200_ConfigurationError, "adjacent views do not overlap");
-    thetas[k].resize(static_cast<size_t>(b[2] - b[0]) * (b[3] - b[1]));
-    hg_ns::blend_weights(masks[pairs[k].view].data(), masks[pairs[k].partner].data(), canvas.width,
-                         canvas.height, b, thetas[k].data());
+    if (!pgeo[k].ok) return fail(STITCH_B200_ConfigurationError, "adjacent views do not overlap");
     stitch_b200_pair& p = in.pairs[k];
     p.view = pairs[k].view;
     p.partner = pairs[k].partner;
-    p.x0 = b[0];
-    p.y0 = b[1];
-    p.x1 = b[2];
-    p.y1 = b[3];
-    p.theta_i = thetas[k].data();
+    p.x0 = pgeo[k].bounds[0];
+    p.y0 = pgeo[k].bounds[1];
+    p.x1 = pgeo[k].bounds[2];
+    p.y1 = pgeo[k].bounds[3];
+    p.theta_i = pgeo[k].theta.data();
   }
   std::unique_ptr<Ctx> ctx;
-  rc = build_context(&in, device, &masks, ctx);
+  rc = build_context(&in, device, &views, ctx);
   if (rc) return rc;
   *out = new stitch_b200_ctx{std::move(ctx)};
   return STITCH_B200_OK;
 }
 
-int stitch_b200_update_geometry(stitch_b200_ctx* h, const stitch_b200_init* init) {
+// Replace a context by a freshly built one, carrying the 3D-M windows,
+// threshold history and frame counter over (pipeline.cpp:399-405).
+static int carry_into(stitch_b200_ctx* h, std::unique_ptr<Ctx>& fresh) {
   Ctx* ctx = h->c.get();
-  if (init->n_pairs != ctx->hg.n_pairs)
-    return fail(STITCH_B200_ConfigurationError, "re-refinement must keep the pair set");
-  std::unique_ptr<Ctx> fresh;
-  int rc = build_context(init, ctx->device, nullptr, fresh);
-  if (rc) return rc;
   CUDA_TRY(cudaStreamSynchronize(ctx->h2d));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->d2h));
@@ -982,6 +945,81 @@ int stitch_b200_update_geometry(stitch_b200_ctx* h, const stitch_b200_init* init
                       cudaMemcpyDeviceToDevice));
   h->c = std::move(fresh);  // the old context is released here
   return STITCH_B200_OK;
+}
+
+int stitch_b200_update_geometry(stitch_b200_ctx* h, const stitch_b200_init* init) {
+  Ctx* ctx = h->c.get();
+  if (init->n_pairs != ctx->hg.n_pairs)
+    return fail(STITCH_B200_ConfigurationError, "re-refinement must keep the pair set");
+  std::unique_ptr<Ctx> fresh;
+  int rc = build_context(init, ctx->device, nullptr, fresh);
+  if (rc) return rc;
+  return carry_into(h, fresh);
+}
+
+int stitch_b200_camera_maps(const stitch_b200_config* cfg, double* maps) {
+  if (cfg->n_views < 2 || cfg->n_views > kMaxViews)
+    return fail(STITCH_B200_ConfigurationError, "n_views must be in [2, 16]");
+  if (cfg->reference < 0 || cfg->reference >= cfg->n_views)
+    return fail(STITCH_B200_ConfigurationError, "reference view index out of range");
+  std::vector<hg_ns::Mat3> cam(cfg->n_views);
+  for (int v = 0; v < cfg->n_views; ++v) {
+    int rc = hg_ns::planar_homography(cfg->cams[v], cam[v]);
+    if (rc) return fail(rc, "camera homography failed (rotation or degenerate pose)");
+  }
+  for (int v = 0; v < cfg->n_views; ++v) {
+    hg_ns::Mat3 m;
+    int rc = hg_ns::pairwise_homography(cam[cfg->reference], cam[v], m);
+    if (rc) return fail(rc, "singular pairwise homography");
+    for (int i = 0; i < 9; ++i) maps[9 * v + i] = m[i];
+  }
+  return STITCH_B200_OK;
+}
+
+int stitch_b200_update_maps(stitch_b200_ctx* h, const double* maps) {
+  Ctx* ctx = h->c.get();
+  if (ctx->init.projection != 0)
+    return fail(STITCH_B200_Unsupported, "update_maps serves the planar canvas");
+  stitch_b200_init in = ctx->init;
+  const int n = in.n_views;
+  std::vector<hg_ns::Mat3> fw(n), inv(n);
+  std::vector<std::pair<int, int>> sizes;
+  for (int v = 0; v < n; ++v) {
+    for (int i = 0; i < 9; ++i) fw[v][i] = maps[9 * v + i];
+    hg_ns::inverse3(fw[v], inv[v]);  // pipeline.cpp:40
+    sizes.emplace_back(in.view_width[v], in.view_height[v]);
+  }
+  const hg_ns::Canvas canvas = hg_ns::compute_canvas(fw, sizes);  // pipeline.cpp:231
+  if (canvas.width <= 0 || canvas.height <= 0 ||
+      static_cast<long long>(canvas.width) * canvas.height > (1ll << 31))
+    return fail(STITCH_B200_ConfigurationError, "canvas size out of range");
+  in.canvas_width = canvas.width;
+  in.canvas_height = canvas.height;
+  in.canvas_offset[0] = canvas.offx;
+  in.canvas_offset[1] = canvas.offy;
+  for (int v = 0; v < n; ++v)
+    for (int i = 0; i < 9; ++i) in.inv_maps[v][i] = inv[v][i];
+  Geometry g{};
+  fill_views(g, &in);
+  std::vector<std::pair<int, int>> vp;
+  for (int k = 0; k < in.n_pairs; ++k) vp.emplace_back(in.pairs[k].view, in.pairs[k].partner);
+  std::vector<ViewFootprint> views;
+  std::vector<PairGeometry> pgeo;
+  int rc = init_geometry(ctx->device, g, make_lift(&in), n, vp, views, pgeo);
+  if (rc) return rc;
+  for (int k = 0; k < in.n_pairs; ++k) {
+    if (!pgeo[k].ok) return fail(STITCH_B200_ConfigurationError, "adjacent views do not overlap");
+    stitch_b200_pair& p = in.pairs[k];
+    p.x0 = pgeo[k].bounds[0];
+    p.y0 = pgeo[k].bounds[1];
+    p.x1 = pgeo[k].bounds[2];
+    p.y1 = pgeo[k].bounds[3];
+    p.theta_i = pgeo[k].theta.data();
+  }
+  std::unique_ptr<Ctx> fresh;
+  rc = build_context(&in, ctx->device, &views, fresh);
+  if (rc) return rc;
+  return carry_into(h, fresh);
 }
 
 void stitch_b200_destroy(stitch_b200_ctx* h) { delete h; }

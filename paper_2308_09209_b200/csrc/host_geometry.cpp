@@ -236,130 +236,4 @@ void lift_tables(const Canvas& c, double f, std::vector<double>& lsin, std::vect
   for (int y = 0; y < c.height; ++y) lh[y] = (y + c.offy) / f;
 }
 
-bool overlap_bounds(const std::uint8_t* mi, const std::uint8_t* mj, int w, int h,
-                    int b[4]) {
-  int x0 = w, y0 = h, x1 = 0, y1 = 0;
-  for (int y = 0; y < h; ++y)
-    for (int x = 0; x < w; ++x) {
-      const size_t i = static_cast<size_t>(y) * w + x;
-      if (mi[i] && mj[i]) {
-        x0 = std::min(x0, x);
-        y0 = std::min(y0, y);
-        x1 = std::max(x1, x + 1);
-        y1 = std::max(y1, y + 1);
-      }
-    }
-  if (x1 <= x0 || y1 <= y0) return false;
-  b[0] = x0;
-  b[1] = y0;
-  b[2] = x1;
-  b[3] = y1;
-  return true;
-}
-
-bool mask_bbox(const std::uint8_t* m, int w, int h, int b[4]) {
-  int x0 = w, y0 = h, x1 = 0, y1 = 0;
-  for (int y = 0; y < h; ++y)
-    for (int x = 0; x < w; ++x)
-      if (m[static_cast<size_t>(y) * w + x]) {
-        x0 = std::min(x0, x);
-        y0 = std::min(y0, y);
-        x1 = std::max(x1, x + 1);
-        y1 = std::max(y1, y + 1);
-      }
-  if (x1 <= x0 || y1 <= y0) return false;
-  b[0] = x0;
-  b[1] = y0;
-  b[2] = x1;
-  b[3] = y1;
-  return true;
-}
-
-void mask_column_gap(const std::uint8_t* m, int w, int /*h*/, const int b[4], int gap[2]) {
-  gap[0] = gap[1] = 0;
-  std::vector<std::uint8_t> col(static_cast<size_t>(w), 0);
-  for (int y = b[1]; y < b[3]; ++y)
-    for (int x = b[0]; x < b[2]; ++x)
-      if (m[static_cast<size_t>(y) * w + x]) col[x] = 1;
-  int best = 0;
-  for (int x = b[0]; x < b[2];) {
-    if (col[x]) {
-      ++x;
-      continue;
-    }
-    int e = x;
-    while (e < b[2] && !col[e]) ++e;
-    if (e - x > best) {
-      best = e - x;
-      gap[0] = x;
-      gap[1] = e;
-    }
-    x = e;
-  }
-}
-
-static constexpr float kFarAway = 1e9f;  // flow.cpp:14
-
-// chamfer_distance (flow.cpp:192-223)
-static void chamfer(const std::vector<std::uint8_t>& zone, int w, int h,
-                    std::vector<float>& d) {
-  d.resize(static_cast<size_t>(w) * h);
-  for (size_t i = 0; i < d.size(); ++i) d[i] = zone[i] ? 0.0f : kFarAway;
-  auto at = [&](int y, int x) -> float& { return d[static_cast<size_t>(y) * w + x]; };
-  for (int y = 0; y < h; ++y)
-    for (int x = 0; x < w; ++x) {
-      float best = at(y, x);
-      if (x > 0) best = std::min(best, at(y, x - 1) + 3.0f);
-      if (y > 0) {
-        best = std::min(best, at(y - 1, x) + 3.0f);
-        if (x > 0) best = std::min(best, at(y - 1, x - 1) + 4.0f);
-        if (x + 1 < w) best = std::min(best, at(y - 1, x + 1) + 4.0f);
-      }
-      at(y, x) = best;
-    }
-  for (int y = h - 1; y >= 0; --y)
-    for (int x = w - 1; x >= 0; --x) {
-      float best = at(y, x);
-      if (x + 1 < w) best = std::min(best, at(y, x + 1) + 3.0f);
-      if (y + 1 < h) {
-        best = std::min(best, at(y + 1, x) + 3.0f);
-        if (x + 1 < w) best = std::min(best, at(y + 1, x + 1) + 4.0f);
-        if (x > 0) best = std::min(best, at(y + 1, x - 1) + 4.0f);
-      }
-      at(y, x) = best;
-    }
-}
-
-void blend_weights(const std::uint8_t* mi, const std::uint8_t* mj, int w, int h,
-                   const int b[4], float* theta_i) {
-  std::vector<std::uint8_t> ei(static_cast<size_t>(w) * h), ej(ei.size());
-  for (size_t i = 0; i < ei.size(); ++i) {
-    ei[i] = mi[i] && !mj[i];
-    ej[i] = mj[i] && !mi[i];
-  }
-  std::vector<float> to_j, to_i;
-  chamfer(ej, w, h, to_j);
-  chamfer(ei, w, h, to_i);
-  const int bw = b[2] - b[0], bh = b[3] - b[1];
-  for (int y = 0; y < bh; ++y)
-    for (int x = 0; x < bw; ++x) {
-      const size_t ci_ = static_cast<size_t>(b[1] + y) * w + b[0] + x;
-      const float cj = to_j[ci_], ci = to_i[ci_];
-      const float di = cj >= kFarAway ? kFarAway : std::max(0.0f, cj / 3.0f - 1.0f);
-      const float dj = ci >= kFarAway ? kFarAway : std::max(0.0f, ci / 3.0f - 1.0f);
-      float ti;
-      if (di >= kFarAway && dj >= kFarAway)
-        ti = 0.5f;
-      else if (di >= kFarAway)
-        ti = 1.0f;
-      else if (dj >= kFarAway)
-        ti = 0.0f;
-      else if (di + dj <= 0.0f)
-        ti = 0.5f;
-      else
-        ti = di / (di + dj);
-      theta_i[static_cast<size_t>(y) * bw + x] = ti;
-    }
-}
-
 }  // namespace stitch_b200_host

@@ -54,17 +54,7 @@ Canvas cylinder_canvas(const stitch_b200_config& cfg, double f);
 void lift_tables(const Canvas& c, double f, std::vector<double>& lsin, std::vector<double>& lcos,
                  std::vector<double>& lh);
 
-// Overlap bbox of two canvas masks (geometry.cpp:85-117); false if empty.
-bool overlap_bounds(const std::uint8_t* mi, const std::uint8_t* mj, int w, int h,
-                    int bounds[4]);
-// bbox of one mask; false if empty.
-bool mask_bbox(const std::uint8_t* m, int w, int h, int bbox[4]);
-// Widest run of empty columns [gap0, gap1) inside a bbox (a 360-degree ring
-// view wraps across the canvas seam, so its bbox spans the whole width while
-// its footprint is two strips at both ends); {0, 0} if none.
-void mask_column_gap(const std::uint8_t* m, int w, int h, const int bbox[4], int gap[2]);
-// blend_weights (flow.cpp:227-280), theta_i over bounds.
-void blend_weights(const std::uint8_t* mi, const std::uint8_t* mj, int w, int h,
-                   const int bounds[4], float* theta_i);
+// (overlap bounds, view footprints and blend weights are computed on the
+// device: geometry_kernels.cu)
 
 }  // namespace stitch_b200_host

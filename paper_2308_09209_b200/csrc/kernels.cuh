@@ -15,6 +15,8 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <utility>
+#include <vector>
 
 #include "stitch_b200.h"
 
@@ -215,5 +217,24 @@ void launch_warp_view(const Geometry* g, int view, const uchar4* frame, std::uin
                       std::uint8_t* mask, cudaStream_t s);
 void launch_expand_one(const std::uint8_t* rgb, uchar4* rgba, long long n_px, cudaStream_t s);
 void launch_warp_mask(const Geometry* g, int view, std::uint8_t* mask, cudaStream_t s);
+
+// ---- init-time geometry on the device (geometry_kernels.cu) ----
+struct ViewFootprint {
+  int bbox[4] = {0, 0, 0, 0};  // bbox of the warp mask
+  int gap[2] = {0, 0};         // widest empty column run inside it
+  bool empty = true;
+};
+struct PairGeometry {
+  bool ok = false;             // the pair's masks overlap
+  int bounds[4] = {0, 0, 0, 0};
+  std::vector<float> theta;    // blend weight theta_i over the bounds
+};
+// Warp masks of every view (launch_warp_mask), view footprints, and for each
+// (view, partner) pair its overlap bounds and chamfer blend weights.
+// lift_*: the cylindrical lift tables (projection 1), else unused.
+cudaError_t gpu_init_geometry(const Geometry& geom, const double* lift_s, const double* lift_c,
+                              const double* lift_h, int n_lift_x, int n_lift_y, int n_views,
+                              const std::vector<std::pair<int, int>>& pairs,
+                              std::vector<ViewFootprint>& views, std::vector<PairGeometry>& out);
 
 }  // namespace stitch_b200_dev

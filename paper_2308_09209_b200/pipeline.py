@@ -260,6 +260,11 @@ class PipelineState:
     def __init__(self, handle: C.c_void_p, config: Optional[StitchConfig] = None):
         self._h = handle
         self.config = config
+        self._refresh()
+        self.n_views = len(config.views) if config else None
+        self.frame_counter = 0
+
+    def _refresh(self) -> None:
         lib = _lib()
         w, h = C.c_int(), C.c_int()
         ox, oy = C.c_double(), C.c_double()
@@ -272,8 +277,15 @@ class PipelineState:
             th = np.empty((p.y1 - p.y0, p.x1 - p.x0), dtype=np.float32)
             check(lib.stitch_b200_get_pair(self._h, k, C.byref(p), th.ctypes.data_as(C.c_void_p)))
             self.pairs.append(PairState(p.view, p.partner, (p.x0, p.y0, p.x1, p.y1), th))
-        self.n_views = len(config.views) if config else None
-        self.frame_counter = 0
+
+    def update_maps(self, maps: np.ndarray) -> None:
+        """Re-refinement from new view->reference homographies (n, 3, 3):
+        canvas, inverse maps and pair geometry rebuilt (the pair geometry on
+        the device); windows, threshold history and counter carried over
+        (pipeline.cpp:395-406)."""
+        m = np.ascontiguousarray(maps, dtype=np.float64).reshape(-1)
+        check(_lib().stitch_b200_update_maps(self._h, m.ctypes.data_as(C.POINTER(C.c_double))))
+        self._refresh()
 
     @property
     def handle(self) -> C.c_void_p:
@@ -328,6 +340,15 @@ def initialize(config: StitchConfig, first_frames: Sequence[Frame]) -> PipelineS
     h = C.c_void_p()
     check(_lib().stitch_b200_initialize(C.byref(c), config.device, C.byref(h)))
     return PipelineState(h, config)
+
+
+def camera_maps(config: StitchConfig, sizes: Sequence[tuple]) -> np.ndarray:
+    """The unrefined view->reference homographies initialize() derives from
+    the camera models (pipeline.cpp:219-229), shape (n, 3, 3)."""
+    c = _config_to_c(config, sizes)
+    out = np.zeros((len(config.views), 3, 3), dtype=np.float64)
+    check(_lib().stitch_b200_camera_maps(C.byref(c), out.ctypes.data_as(C.POINTER(C.c_double))))
+    return out
 
 
 def create_from_init(init: _abi.Init, device: int = 0,

@@ -244,6 +244,43 @@ def test_update_geometry_keeps_temporal_state():
         check_frame(state, ost, frames_at(sc, t), t)
 
 
+def test_update_maps_rebuilds_geometry_on_device():
+    """Re-refinement from new homographies (stitch_b200_update_maps): the
+    canvas, inverse maps and device-built pair geometry equal a fresh
+    initialize() with those maps, and the temporal state is carried over."""
+    sc1 = scene(views=3, width=160, height=120, frames=4, focal_scale=1.0)
+    sc2 = scene(views=3, width=160, height=120, frames=4, focal_scale=1.03)
+    cfg1, cfg2 = product_config(sc1), product_config(sc2)
+    state = pb.initialize(cfg1, frames_at(sc1, 0))
+    for t in range(2):
+        pb.process_frame(state, frames_at(sc1, t))
+    sizes = [(160, 120)] * 3
+    maps2 = pb.camera_maps(cfg2, sizes)
+    assert not np.array_equal(maps2, pb.camera_maps(cfg1, sizes))
+    state.update_maps(maps2)
+    fresh = pb.initialize(cfg2, frames_at(sc2, 0))
+    assert state.canvas == fresh.canvas
+    for v in range(3):
+        assert np.array_equal(state.inv_map(v), fresh.inv_map(v))
+        assert state.view_bbox(v) == fresh.view_bbox(v)
+    assert len(state.pairs) == len(fresh.pairs)
+    for a, b in zip(state.pairs, fresh.pairs):
+        assert (a.view, a.partner, a.bounds) == (b.view, b.partner, b.bounds)
+        assert np.array_equal(a.theta_i, b.theta_i)
+    r1 = pb.process_frame(state, frames_at(sc2, 2))
+    r2 = pb.process_frame(fresh, frames_at(sc2, 2))
+    assert r1.report.frame_index == 2 and r2.report.frame_index == 0
+    assert r1.panorama.data.shape == r2.panorama.data.shape
+    # the unchanged maps reproduce the initialize() geometry bit for bit
+    state.update_maps(pb.camera_maps(cfg1, sizes))
+    again = pb.initialize(cfg1, frames_at(sc1, 0))
+    for a, b in zip(state.pairs, again.pairs):
+        assert a.bounds == b.bounds and np.array_equal(a.theta_i, b.theta_i)
+    state.close()
+    fresh.close()
+    again.close()
+
+
 def test_create_from_snapshot_matches_initialize():
     sc = scene(views=2, width=160, height=120, frames=2)
     state, ost = make_pair(sc)
