@@ -180,6 +180,24 @@ int stitch_b200_camera_maps(const stitch_b200_config* cfg, double* maps);
 
 void stitch_b200_destroy(stitch_b200_ctx* ctx);
 
+/* Quality metrics (metrics.cpp:9-155), evaluated on the device, results
+ * equal to the reference's.  psnr: dB over jointly valid pixels, channels
+ * pooled, +inf for identical inputs; ssim: mean SSIM on Rec.601 luma with an
+ * 11x11 Gaussian window (sigma 1.5) over windows with fully valid support.
+ * Host RGB8 frames, masks 0/1 or NULL (all valid).  Errors: ShapeMismatch
+ * is impossible here (one size), EmptyRegion, TooSmall (ssim, < 11 px). */
+int stitch_b200_psnr(int width, int height, const uint8_t* a_rgb, const uint8_t* a_mask,
+                     const uint8_t* b_rgb, const uint8_t* b_mask, double* out);
+int stitch_b200_ssim(int width, int height, const uint8_t* a_rgb, const uint8_t* a_mask,
+                     const uint8_t* b_rgb, const uint8_t* b_mask, double* out);
+
+/* The paper's Tables 2-3 columns for pair k's colour transfer in the last
+ * processed frame, on the device-resident overlap crops (compare_methods,
+ * metrics.cpp:177-208, with the context's window capacity = the method):
+ * out[0] = psnr(corrected, source), out[1] = psnr(corrected, reference),
+ * out[2] = ssim(corrected, reference). */
+int stitch_b200_pair_quality(stitch_b200_ctx* ctx, int k, double out[3]);
+
 /* Geometry of a context. */
 int stitch_b200_canvas(const stitch_b200_ctx* ctx, int* width, int* height,
                        double* offset_x, double* offset_y);

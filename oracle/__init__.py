@@ -124,6 +124,8 @@ def lib() -> C.CDLL:
                                          P(C.c_float)]),
         "so_state_last_warped": (C.c_int, [C.c_void_p, C.c_int, P(C.c_uint8), P(C.c_uint8)]),
         "so_free_frame": (None, [P(SoFrame)]),
+        "so_psnr": (C.c_int, [P(SoFrame), P(SoFrame), P(C.c_double)]),
+        "so_ssim": (C.c_int, [P(SoFrame), P(SoFrame), P(C.c_double)]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)
@@ -163,6 +165,26 @@ def take_frame(f: SoFrame):
         mask = np.ctypeslib.as_array(f.mask, shape=(h * w,)).copy().reshape(h, w)
     lib().so_free_frame(C.byref(f))
     return data, mask
+
+
+def psnr(a_data, a_mask, b_data, b_mask) -> float:
+    """metrics.cpp:9-31 (oracle)."""
+    fa, fb = FrameRef(a_data, a_mask), FrameRef(b_data, b_mask)
+    out = C.c_double()
+    e = lib().so_psnr(C.byref(fa.c), C.byref(fb.c), C.byref(out))
+    if e != SO_OK:
+        raise OracleError(e)
+    return out.value
+
+
+def ssim(a_data, a_mask, b_data, b_mask) -> float:
+    """metrics.cpp:83-155 (oracle)."""
+    fa, fb = FrameRef(a_data, a_mask), FrameRef(b_data, b_mask)
+    out = C.c_double()
+    e = lib().so_ssim(C.byref(fa.c), C.byref(fb.c), C.byref(out))
+    if e != SO_OK:
+        raise OracleError(e)
+    return out.value
 
 
 def quantize_channel(v: float) -> int:

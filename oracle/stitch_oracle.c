@@ -1583,3 +1583,137 @@ int so_state_last_warped(const so_state* s, int view, uint8_t* rgb,
   memcpy(mask, f->mask, (size_t)f->width * f->height);
   return SO_OK;
 }
+
+/* ======================================================================
+ * Quality metrics (metrics.cpp:9-155)
+ * ====================================================================== */
+
+static int so_valid(const so_frame* f, int x, int y) {
+  return f->mask == NULL || f->mask[(size_t)y * f->width + x] != 0;
+}
+
+/* psnr, metrics.cpp:9-31 */
+int so_psnr(const so_frame* a, const so_frame* b, double* out) {
+  if (a->width != b->width || a->height != b->height) return SO_ShapeMismatch;
+  long long n = 0;
+  double sse = 0.0;
+  for (int y = 0; y < a->height; ++y)
+    for (int x = 0; x < a->width; ++x) {
+      if (!so_valid(a, x, y) || !so_valid(b, x, y)) continue;
+      const uint8_t* pa = a->data + ((size_t)y * a->width + x) * 3;
+      const uint8_t* pb = b->data + ((size_t)y * b->width + x) * 3;
+      for (int c = 0; c < 3; ++c) {
+        const double d = (double)pa[c] - pb[c];
+        sse += d * d;
+      }
+      ++n;
+    }
+  if (n == 0) return SO_EmptyRegion;
+  const double mse = sse / (3.0 * (double)n);
+  *out = mse == 0.0 ? INFINITY : 10.0 * log10(255.0 * 255.0 / mse);
+  return SO_OK;
+}
+
+#define SO_SSIM_WIN 11
+
+/* gaussian_kernel, metrics.cpp:40-49 */
+static void so_gauss_kernel(double k[SO_SSIM_WIN]) {
+  double sum = 0.0;
+  for (int i = 0; i < SO_SSIM_WIN; ++i) {
+    const double d = i - (SO_SSIM_WIN - 1) / 2.0;
+    k[i] = exp(-d * d / (2.0 * 1.5 * 1.5));
+    sum += k[i];
+  }
+  for (int i = 0; i < SO_SSIM_WIN; ++i) k[i] /= sum;
+}
+
+/* gauss_filter, metrics.cpp:56-79: horizontal then vertical, interior only */
+static void so_gauss_filter(const double* src, int w, int h, double* out) {
+  double k[SO_SSIM_WIN];
+  so_gauss_kernel(k);
+  const int r = SO_SSIM_WIN / 2;
+  double* tmp = (double*)calloc((size_t)w * h, sizeof(double));
+  for (int y = 0; y < h; ++y)
+    for (int x = r; x < w - r; ++x) {
+      double acc = 0.0;
+      for (int i = 0; i < SO_SSIM_WIN; ++i) acc += k[i] * src[(size_t)y * w + x - r + i];
+      tmp[(size_t)y * w + x] = acc;
+    }
+  memset(out, 0, sizeof(double) * (size_t)w * h);
+  for (int y = r; y < h - r; ++y)
+    for (int x = 0; x < w; ++x) {
+      double acc = 0.0;
+      for (int i = 0; i < SO_SSIM_WIN; ++i) acc += k[i] * tmp[(size_t)(y - r + i) * w + x];
+      out[(size_t)y * w + x] = acc;
+    }
+  free(tmp);
+}
+
+/* ssim, metrics.cpp:83-155 */
+int so_ssim(const so_frame* a, const so_frame* b, double* out) {
+  if (a->width != b->width || a->height != b->height) return SO_ShapeMismatch;
+  if (a->width < SO_SSIM_WIN || a->height < SO_SSIM_WIN) return SO_TooSmall;
+  const int w = a->width, h = a->height;
+  const size_t n = (size_t)w * h;
+  double* la = (double*)malloc(sizeof(double) * n);
+  double* lb = (double*)malloc(sizeof(double) * n);
+  double* sq = (double*)malloc(sizeof(double) * n);
+  double* mu_a = (double*)malloc(sizeof(double) * n);
+  double* mu_b = (double*)malloc(sizeof(double) * n);
+  double* aa = (double*)malloc(sizeof(double) * n);
+  double* bb = (double*)malloc(sizeof(double) * n);
+  double* ab = (double*)malloc(sizeof(double) * n);
+  uint8_t* joint = (uint8_t*)malloc(n);
+  uint32_t* integ = (uint32_t*)calloc((size_t)(w + 1) * (h + 1), sizeof(uint32_t));
+  for (int y = 0; y < h; ++y)
+    for (int x = 0; x < w; ++x) {
+      const size_t i = (size_t)y * w + x;
+      const int valid = so_valid(a, x, y) && so_valid(b, x, y);
+      joint[i] = (uint8_t)valid;
+      const uint8_t* pa = a->data + i * 3;
+      const uint8_t* pb = b->data + i * 3;
+      la[i] = valid ? 0.299 * pa[0] + 0.587 * pa[1] + 0.114 * pa[2] : 0.0;
+      lb[i] = valid ? 0.299 * pb[0] + 0.587 * pb[1] + 0.114 * pb[2] : 0.0;
+    }
+  for (int y = 0; y < h; ++y) {
+    uint32_t row = 0;
+    for (int x = 0; x < w; ++x) {
+      row += joint[(size_t)y * w + x];
+      integ[(size_t)(y + 1) * (w + 1) + x + 1] = integ[(size_t)y * (w + 1) + x + 1] + row;
+    }
+  }
+  so_gauss_filter(la, w, h, mu_a);
+  so_gauss_filter(lb, w, h, mu_b);
+  for (size_t i = 0; i < n; ++i) sq[i] = la[i] * la[i];
+  so_gauss_filter(sq, w, h, aa);
+  for (size_t i = 0; i < n; ++i) sq[i] = lb[i] * lb[i];
+  so_gauss_filter(sq, w, h, bb);
+  for (size_t i = 0; i < n; ++i) sq[i] = la[i] * lb[i];
+  so_gauss_filter(sq, w, h, ab);
+  const double c1 = (0.01 * 255.0) * (0.01 * 255.0);
+  const double c2 = (0.03 * 255.0) * (0.03 * 255.0);
+  const int r = SO_SSIM_WIN / 2;
+  double sum = 0.0;
+  long long count = 0;
+  for (int y = r; y < h - r; ++y)
+    for (int x = r; x < w - r; ++x) {
+      const int x0 = x - r, y0 = y - r, x1 = x + r + 1, y1 = y + r + 1;
+      const uint32_t cnt = integ[(size_t)y1 * (w + 1) + x1] - integ[(size_t)y0 * (w + 1) + x1] -
+                           integ[(size_t)y1 * (w + 1) + x0] + integ[(size_t)y0 * (w + 1) + x0];
+      if (cnt != (uint32_t)(SO_SSIM_WIN * SO_SSIM_WIN)) continue;
+      const size_t i = (size_t)y * w + x;
+      const double ma = mu_a[i], mb = mu_b[i];
+      const double va = aa[i] - ma * ma;
+      const double vb = bb[i] - mb * mb;
+      const double cov = ab[i] - ma * mb;
+      const double num = (2.0 * ma * mb + c1) * (2.0 * cov + c2);
+      const double den = (ma * ma + mb * mb + c1) * (va + vb + c2);
+      sum += num / den;
+      ++count;
+    }
+  free(la); free(lb); free(sq); free(mu_a); free(mu_b); free(aa); free(bb); free(ab);
+  free(joint); free(integ);
+  if (count == 0) return SO_EmptyRegion;
+  *out = sum / (double)count;
+  return SO_OK;
+}

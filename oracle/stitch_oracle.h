@@ -187,6 +187,14 @@ int so_state_last_flow(const so_state* s, int k, int dir, float* u, float* v);
 int so_state_last_warped(const so_state* s, int view, uint8_t* rgb,
                          uint8_t* mask);
 
+/* ---- quality metrics (metrics.cpp:9-155) ---- */
+/* PSNR in dB over jointly valid pixels, channels pooled; +inf for identical
+ * inputs.  Returns SO_OK, SO_ShapeMismatch or SO_EmptyRegion. */
+int so_psnr(const so_frame* a, const so_frame* b, double* out);
+/* mean SSIM on Rec.601 luma, 11x11 Gaussian (sigma 1.5), windows with fully
+ * jointly valid support.  SO_ShapeMismatch, SO_TooSmall or SO_EmptyRegion. */
+int so_ssim(const so_frame* a, const so_frame* b, double* out);
+
 /* helpers */
 void so_free_frame(so_frame* f);
 

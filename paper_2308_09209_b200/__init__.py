@@ -28,6 +28,10 @@ from .pipeline import (  # noqa: F401
     SynthSpec,
     ViewSetup,
     camera_maps,
+    compare_methods,
+    MetricRow,
+    psnr,
+    ssim,
     create_from_init,
     initialize,
     process_frame,

@@ -80,6 +80,11 @@ SYMBOLS = [
     ("stitch_b200_update_geometry", C.c_int, [C.c_void_p, C.POINTER(Init)]),
     ("stitch_b200_update_maps", C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     ("stitch_b200_camera_maps", C.c_int, [C.POINTER(Config), C.POINTER(C.c_double)]),
+    ("stitch_b200_psnr", C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.c_void_p, C.POINTER(C.c_double)]),
+    ("stitch_b200_ssim", C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.c_void_p, C.POINTER(C.c_double)]),
+    ("stitch_b200_pair_quality", C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_double)]),
     ("stitch_b200_destroy", None, [C.c_void_p]),
     ("stitch_b200_canvas", C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                      C.POINTER(C.c_double), C.POINTER(C.c_double)]),

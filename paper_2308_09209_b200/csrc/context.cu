@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <limits>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -1284,3 +1285,85 @@ int stitch_b200_debug_warp_view(stitch_b200_ctx* h, int view, const uint8_t* hos
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// quality metrics (metrics.cpp:9-155) on the device
+// ---------------------------------------------------------------------------
+static int psnr_from_parts(unsigned long long sse, unsigned long long n, double* out) {
+  if (n == 0) return fail(STITCH_B200_EmptyRegion, "no jointly valid pixel");
+  const double mse = static_cast<double>(sse) / (3.0 * static_cast<double>(n));
+  *out = mse == 0.0 ? std::numeric_limits<double>::infinity()
+                    : 10.0 * std::log10(255.0 * 255.0 / mse);
+  return STITCH_B200_OK;
+}
+
+static int ssim_from_parts(double sum, long long n, double* out) {
+  if (n == 0) return fail(STITCH_B200_EmptyRegion, "no fully valid SSIM window");
+  *out = sum / static_cast<double>(n);
+  return STITCH_B200_OK;
+}
+
+namespace {
+struct PackedPair {
+  uchar4* a = nullptr;
+  uchar4* b = nullptr;
+  ~PackedPair() {
+    if (a) cudaFree(a);
+    if (b) cudaFree(b);
+  }
+};
+
+int pack_pair(int w, int h, const uint8_t* a_rgb, const uint8_t* a_mask, const uint8_t* b_rgb,
+              const uint8_t* b_mask, PackedPair& pp) {
+  if (w <= 0 || h <= 0 || !a_rgb || !b_rgb)
+    return fail(STITCH_B200_ConfigurationError, "bad frame arguments");
+  const int n = w * h;
+  CUDA_TRY(cudaMalloc(&pp.a, sizeof(uchar4) * n));
+  CUDA_TRY(cudaMalloc(&pp.b, sizeof(uchar4) * n));
+  CUDA_TRY(gpu_pack_rgba(a_rgb, a_mask, n, pp.a, nullptr));
+  CUDA_TRY(gpu_pack_rgba(b_rgb, b_mask, n, pp.b, nullptr));
+  return STITCH_B200_OK;
+}
+}  // namespace
+
+int stitch_b200_psnr(int width, int height, const uint8_t* a_rgb, const uint8_t* a_mask,
+                     const uint8_t* b_rgb, const uint8_t* b_mask, double* out) {
+  PackedPair pp;
+  int rc = pack_pair(width, height, a_rgb, a_mask, b_rgb, b_mask, pp);
+  if (rc) return rc;
+  unsigned long long sse = 0, n = 0;
+  CUDA_TRY(gpu_psnr_parts(pp.a, pp.b, width * height, &sse, &n, nullptr));
+  return psnr_from_parts(sse, n, out);
+}
+
+int stitch_b200_ssim(int width, int height, const uint8_t* a_rgb, const uint8_t* a_mask,
+                     const uint8_t* b_rgb, const uint8_t* b_mask, double* out) {
+  if (width < 11 || height < 11) return fail(STITCH_B200_TooSmall, "ssim needs >= 11x11");
+  PackedPair pp;
+  int rc = pack_pair(width, height, a_rgb, a_mask, b_rgb, b_mask, pp);
+  if (rc) return rc;
+  double sum = 0.0;
+  long long n = 0;
+  CUDA_TRY(gpu_ssim_parts(pp.a, pp.b, width, height, &sum, &n, nullptr));
+  return ssim_from_parts(sum, n, out);
+}
+
+int stitch_b200_pair_quality(stitch_b200_ctx* h, int k, double out[3]) {
+  Ctx* ctx = h->c.get();
+  if (k < 0 || k >= ctx->hg.n_pairs) return fail(STITCH_B200_ConfigurationError, "bad pair index");
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  const PairDesc& p = ctx->hg.pairs[k];
+  const int n = p.w * p.h;
+  unsigned long long sse = 0, cnt = 0;
+  CUDA_TRY(gpu_psnr_parts(p.crop_cor[0], p.crop_raw[0], n, &sse, &cnt, ctx->stream));
+  int rc = psnr_from_parts(sse, cnt, &out[0]);
+  if (rc) return rc;
+  CUDA_TRY(gpu_psnr_parts(p.crop_cor[0], p.crop_cor[1], n, &sse, &cnt, ctx->stream));
+  rc = psnr_from_parts(sse, cnt, &out[1]);
+  if (rc) return rc;
+  if (p.w < 11 || p.h < 11) return fail(STITCH_B200_TooSmall, "ssim needs >= 11x11");
+  double sum = 0.0;
+  long long wn = 0;
+  CUDA_TRY(gpu_ssim_parts(p.crop_cor[0], p.crop_cor[1], p.w, p.h, &sum, &wn, ctx->stream));
+  return ssim_from_parts(sum, wn, &out[2]);
+}

@@ -218,6 +218,14 @@ void launch_warp_view(const Geometry* g, int view, const uchar4* frame, std::uin
 void launch_expand_one(const std::uint8_t* rgb, uchar4* rgba, long long n_px, cudaStream_t s);
 void launch_warp_mask(const Geometry* g, int view, std::uint8_t* mask, cudaStream_t s);
 
+// ---- quality metrics (metrics_kernels.cu) ----
+cudaError_t gpu_psnr_parts(const uchar4* a, const uchar4* b, int n, unsigned long long* sse,
+                           unsigned long long* count, cudaStream_t s);
+cudaError_t gpu_ssim_parts(const uchar4* a, const uchar4* b, int w, int h, double* sum,
+                           long long* count, cudaStream_t s);
+cudaError_t gpu_pack_rgba(const std::uint8_t* rgb_host, const std::uint8_t* mask_host, int n,
+                          uchar4* out, cudaStream_t s);
+
 // ---- init-time geometry on the device (geometry_kernels.cu) ----
 struct ViewFootprint {
   int bbox[4] = {0, 0, 0, 0};  // bbox of the warp mask

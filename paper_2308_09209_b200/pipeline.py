@@ -9,6 +9,7 @@ is no CPU path.
 """
 from __future__ import annotations
 
+import copy
 import ctypes as C
 import enum
 import time
@@ -278,6 +279,14 @@ class PipelineState:
             check(lib.stitch_b200_get_pair(self._h, k, C.byref(p), th.ctypes.data_as(C.c_void_p)))
             self.pairs.append(PairState(p.view, p.partner, (p.x0, p.y0, p.x1, p.y1), th))
 
+    def pair_quality(self, k: int) -> tuple:
+        """Tables 2-3 columns of pair k in the last frame (device):
+        (psnr(corrected, source), psnr(corrected, reference),
+        ssim(corrected, reference))."""
+        out = (C.c_double * 3)()
+        check(_lib().stitch_b200_pair_quality(self._h, k, out))
+        return tuple(out)
+
     def update_maps(self, maps: np.ndarray) -> None:
         """Re-refinement from new view->reference homographies (n, 3, 3):
         canvas, inverse maps and pair geometry rebuilt (the pair geometry on
@@ -349,6 +358,67 @@ def camera_maps(config: StitchConfig, sizes: Sequence[tuple]) -> np.ndarray:
     out = np.zeros((len(config.views), 3, 3), dtype=np.float64)
     check(_lib().stitch_b200_camera_maps(C.byref(c), out.ctypes.data_as(C.POINTER(C.c_double))))
     return out
+
+
+def _metric(fn, a: Frame, b: Frame) -> float:
+    if a.data.shape != b.data.shape:
+        raise StitchError(ErrorCode.ShapeMismatch + 1, "frame sizes differ")
+    da = np.ascontiguousarray(a.data, np.uint8)
+    db = np.ascontiguousarray(b.data, np.uint8)
+    ma = None if a.mask is None else np.ascontiguousarray(a.mask, np.uint8)
+    mb = None if b.mask is None else np.ascontiguousarray(b.mask, np.uint8)
+    out = C.c_double()
+    check(fn(a.width, a.height, da.ctypes.data, None if ma is None else ma.ctypes.data,
+             db.ctypes.data, None if mb is None else mb.ctypes.data, C.byref(out)))
+    return out.value
+
+
+def psnr(a: Frame, b: Frame) -> float:
+    """metrics.hpp:15 psnr(a, b), evaluated on the device."""
+    return _metric(_lib().stitch_b200_psnr, a, b)
+
+
+def ssim(a: Frame, b: Frame) -> float:
+    """metrics.hpp:21 ssim(a, b), evaluated on the device."""
+    return _metric(_lib().stitch_b200_ssim, a, b)
+
+
+@dataclass
+class MetricRow:  # metrics.hpp:23-30
+    scene_id: str
+    frame_label: str
+    method: str
+    psnr_vs_source: float = 0.0
+    psnr_vs_reference: float = 0.0
+    ssim_vs_reference: float = 0.0
+
+
+def compare_methods(config: StitchConfig, views: Sequence[Sequence[Frame]], pair: int = 0,
+                    scene_id: str = "") -> List[MetricRow]:
+    """The Tables 2-3 comparison (metrics.hpp:48-54, compare_methods_both) on
+    the stitching pipeline's own overlap of `pair`: the sequence runs once
+    with window 1 (2D-M) and once with window 3 (3D-M); per-frame rows then
+    mu and sigma (population) rows per method."""
+    rows: List[MetricRow] = []
+    for window, method in ((1, "2D-M"), (3, "3D-M")):
+        cfg = copy.deepcopy(config)
+        cfg.window_capacity = window
+        state = initialize(cfg, [s[0] for s in views])
+        cols = []
+        try:
+            for t in range(len(views[0])):
+                process_frame(state, [s[t] for s in views])
+                q = state.pair_quality(pair)
+                rows.append(MetricRow(scene_id, str(t + 1), method, *q))
+                cols.append(q)
+        finally:
+            state.close()
+        arr = np.array(cols, dtype=np.float64)
+        mu = arr.mean(axis=0)
+        sigma = np.sqrt(((arr - mu) ** 2).mean(axis=0))
+        rows.append(MetricRow(scene_id, "mu", method, *mu))
+        rows.append(MetricRow(scene_id, "sigma", method, *sigma))
+    return rows
 
 
 def create_from_init(init: _abi.Init, device: int = 0,

@@ -292,3 +292,69 @@ def test_fuse_and_compose_examples():
     np.testing.assert_array_equal(out[:, :15], a[:, :15])
     np.testing.assert_array_equal(out[:, 15:], b[:, 15:])
     assert m.all()
+
+
+# ---- quality metrics (metrics.cpp:9-155) ----
+def _np_ssim(a, am, b, bm):
+    """Independent windowed-loop SSIM restatement (numpy, different summation order)."""
+    h, w = a.shape[:2]
+    valid = np.ones((h, w), bool)
+    if am is not None:
+        valid &= am.astype(bool)
+    if bm is not None:
+        valid &= bm.astype(bool)
+    lum = lambda d: np.where(valid, 0.299 * d[..., 0] + 0.587 * d[..., 1] + 0.114 * d[..., 2], 0.0)
+    la, lb = lum(a.astype(np.float64)), lum(b.astype(np.float64))
+    d = np.arange(11) - 5.0
+    k = np.exp(-d * d / (2 * 1.5 * 1.5))
+    k /= k.sum()
+    g2 = np.outer(k, k)
+    c1, c2 = (0.01 * 255) ** 2, (0.03 * 255) ** 2
+    vals = []
+    for y in range(5, h - 5):
+        for x in range(5, w - 5):
+            if not valid[y - 5:y + 6, x - 5:x + 6].all():
+                continue
+            pa, pb = la[y - 5:y + 6, x - 5:x + 6], lb[y - 5:y + 6, x - 5:x + 6]
+            ma, mb = (g2 * pa).sum(), (g2 * pb).sum()
+            va, vb = (g2 * pa * pa).sum() - ma * ma, (g2 * pb * pb).sum() - mb * mb
+            cov = (g2 * pa * pb).sum() - ma * mb
+            vals.append((2 * ma * mb + c1) * (2 * cov + c2) / ((ma * ma + mb * mb + c1) * (va + vb + c2)))
+    return float(np.mean(vals))
+
+
+def test_psnr_examples():  # SPEC.md:566-574
+    rng = np.random.default_rng(21)
+    a, _ = random_frame(rng, 40, 30)
+    assert O.psnr(a, None, a, None) == float("inf")
+    b = a.copy().astype(np.int16)
+    b = np.where(b == 255, 254, b + 1).astype(np.uint8)  # every sample differs by exactly 1
+    assert abs(O.psnr(a, None, b, None) - 20 * np.log10(255.0)) <= 1e-4
+    c, cm = random_frame(rng, 40, 30, mask_drop=0.2)
+    am = (rng.random((30, 40)) >= 0.1).astype(np.uint8)
+    valid = cm.astype(bool) & am.astype(bool)
+    d = a.astype(np.float64) - c.astype(np.float64)
+    mse = (d[valid] ** 2).sum() / (3 * valid.sum())
+    assert abs(O.psnr(a, am, c, cm) - 10 * np.log10(255.0 ** 2 / mse)) <= 1e-9
+    assert O.psnr(a, am, c, cm) == O.psnr(c, cm, a, am)  # symmetric
+    with pytest.raises(O.OracleError):
+        O.psnr(a, None, a[:20], None)  # ShapeMismatch
+    with pytest.raises(O.OracleError):
+        O.psnr(a, np.zeros((30, 40), np.uint8), a, None)  # EmptyRegion
+
+
+def test_ssim_examples():  # SPEC.md:575-582
+    rng = np.random.default_rng(22)
+    a, _ = random_frame(rng, 36, 28)
+    assert abs(O.ssim(a, None, a, None) - 1.0) <= 1e-9
+    zero = np.zeros((28, 36, 3), np.uint8)
+    full = np.full((28, 36, 3), 255, np.uint8)
+    c1 = (0.01 * 255) ** 2
+    assert abs(O.ssim(zero, None, full, None) - c1 / (255.0 ** 2 + c1)) <= 1e-12
+    b, _ = random_frame(rng, 36, 28)
+    bm = np.ones((28, 36), np.uint8)
+    bm[:9, :12] = 0  # an invalid corner: windows touching it are skipped
+    b = ((a.astype(np.int32) * 3 + b) // 4).astype(np.uint8)  # correlated with a
+    assert abs(O.ssim(a, None, b, bm) - _np_ssim(a, None, b, bm)) <= 1e-6
+    with pytest.raises(O.OracleError):
+        O.ssim(a[:10], None, a[:10], None)  # TooSmall
