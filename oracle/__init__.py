@@ -53,7 +53,26 @@ class SoConfig(C.Structure):
                 ("flow_levels", C.c_int), ("flow_iterations", C.c_int),
                 ("smoothness", C.c_double), ("window_capacity", C.c_int),
                 ("fuse_weighting", C.c_int), ("topology", C.c_int), ("threads", C.c_int),
-                ("keep_debug", C.c_int), ("projection", C.c_int), ("cyl_focal", C.c_double)]
+                ("keep_debug", C.c_int), ("projection", C.c_int), ("cyl_focal", C.c_double),
+                ("refine_enabled", C.c_int), ("refine_margin", C.c_double),
+                ("ransac_iters", C.c_int), ("inlier_px", C.c_double),
+                ("detect_threshold", C.c_double), ("match_ratio", C.c_double),
+                ("seed", C.c_ulonglong)]
+
+
+class SoKeypoint(C.Structure):
+    _fields_ = [("x", C.c_double), ("y", C.c_double), ("scale", C.c_double),
+                ("response", C.c_double)]
+
+
+class SoMatchPair(C.Structure):
+    _fields_ = [("index_a", C.c_int), ("index_b", C.c_int), ("distance", C.c_double),
+                ("ax", C.c_double), ("ay", C.c_double), ("bx", C.c_double), ("by", C.c_double)]
+
+
+class SoSimilarity(C.Structure):
+    _fields_ = [("s_x", C.c_double), ("s_y", C.c_double), ("t_x", C.c_double),
+                ("t_y", C.c_double)]
 
 
 class SoReport(C.Structure):
@@ -125,6 +144,14 @@ def lib() -> C.CDLL:
         "so_state_last_warped": (C.c_int, [C.c_void_p, C.c_int, P(C.c_uint8), P(C.c_uint8)]),
         "so_free_frame": (None, [P(SoFrame)]),
         "so_psnr": (C.c_int, [P(SoFrame), P(SoFrame), P(C.c_double)]),
+        "so_detect": (C.c_int, [P(SoFrame), SoRegion, C.c_double, P(P(SoKeypoint)), P(C.c_int)]),
+        "so_describe": (None, [P(SoFrame), P(SoKeypoint), C.c_int, P(C.c_float)]),
+        "so_match": (C.c_int, [P(C.c_float), C.c_int, P(C.c_float), C.c_int, P(SoKeypoint),
+                               P(SoKeypoint), C.c_double, P(SoMatchPair)]),
+        "so_ransac": (C.c_int, [P(SoMatchPair), C.c_int, C.c_int, C.c_double, C.c_double,
+                                C.c_double, C.c_ulonglong, P(SoSimilarity)]),
+        "so_initialize_frames": (C.c_void_p, [P(SoConfig), P(SoFrame), P(C.c_int)]),
+        "so_state_refine_warning": (C.c_int, [C.c_void_p, C.c_int]),
         "so_ssim": (C.c_int, [P(SoFrame), P(SoFrame), P(C.c_double)]),
     }
     for name, (res, args) in sigs.items():
@@ -185,6 +212,63 @@ def ssim(a_data, a_mask, b_data, b_mask) -> float:
     if e != SO_OK:
         raise OracleError(e)
     return out.value
+
+
+def detect(data, mask, region, threshold=2e-4):
+    """features.cpp:52-118 -> list of (x, y, scale, response)."""
+    fr = FrameRef(data, mask)
+    out = C.POINTER(SoKeypoint)()
+    n = C.c_int()
+    e = lib().so_detect(C.byref(fr.c), SoRegion(*region), threshold, C.byref(out), C.byref(n))
+    if e != SO_OK:
+        raise OracleError(e)
+    kps = [(out[i].x, out[i].y, out[i].scale, out[i].response) for i in range(n.value)]
+    if n.value:
+        C.CDLL(None).free(out)
+    return kps
+
+
+def _kp_array(kps):
+    arr = (SoKeypoint * max(1, len(kps)))()
+    for i, k in enumerate(kps):
+        arr[i] = SoKeypoint(*k)
+    return arr
+
+
+def describe(data, mask, kps):
+    """features.cpp:139-179 -> (n, 64) float32."""
+    fr = FrameRef(data, mask)
+    out = np.zeros((max(1, len(kps)), 64), np.float32)
+    lib().so_describe(C.byref(fr.c), _kp_array(kps), len(kps),
+                      out.ctypes.data_as(C.POINTER(C.c_float)))
+    return out[:len(kps)]
+
+
+def match(da, db, ka, kb, ratio=0.8):
+    """features.cpp:181-234 -> list of (a, b, distance, ax, ay, bx, by)."""
+    da = np.ascontiguousarray(da, np.float32)
+    db = np.ascontiguousarray(db, np.float32)
+    out = (SoMatchPair * max(1, len(ka)))()
+    n = lib().so_match(da.ctypes.data_as(C.POINTER(C.c_float)), len(ka),
+                       db.ctypes.data_as(C.POINTER(C.c_float)), len(kb), _kp_array(ka),
+                       _kp_array(kb), ratio, out)
+    return [(out[i].index_a, out[i].index_b, out[i].distance, out[i].ax, out[i].ay, out[i].bx,
+             out[i].by) for i in range(n)]
+
+
+def ransac(matches, iterations=500, inlier_px=2.0, min_scale=0.5, max_scale=2.0, seed=0):
+    """features.cpp:282-354 on (ax, ay, bx, by[, distance]) -> (s_x, s_y, t_x, t_y)."""
+    arr = (SoMatchPair * max(1, len(matches)))()
+    for i, m in enumerate(matches):
+        ax, ay, bx, by = m[:4]
+        d = m[4] if len(m) > 4 else 0.0
+        arr[i] = SoMatchPair(i, i, d, ax, ay, bx, by)
+    out = SoSimilarity()
+    e = lib().so_ransac(arr, len(matches), iterations, inlier_px, min_scale, max_scale, seed,
+                        C.byref(out))
+    if e != SO_OK:
+        raise OracleError(e)
+    return (out.s_x, out.s_y, out.t_x, out.t_y)
 
 
 def quantize_channel(v: float) -> int:
@@ -353,7 +437,8 @@ def blend_weights(mask_i, mask_j, region):
 def make_config(n_views, reference, sizes, cams, *, lam=0.05, gamma_dark=1.5, gamma_bright=1.5,
                 target_black=0, target_white=255, levels=4, iterations=50, smoothness=15.0,
                 window=3, weighting=0, topology=0, threads=1, keep_debug=0, projection=0,
-                cyl_focal=0.0) -> SoConfig:
+                cyl_focal=0.0, refine=False, refine_margin=0.15, ransac_iters=500,
+                inlier_px=2.0, detect_threshold=2e-4, match_ratio=0.8, seed=0) -> SoConfig:
     """cams: list of (fx, fy, cx, cy, R[9] row-major, t[3])."""
     c = SoConfig()
     c.n_views = n_views
@@ -377,16 +462,24 @@ def make_config(n_views, reference, sizes, cams, *, lam=0.05, gamma_dark=1.5, ga
     c.keep_debug = keep_debug
     c.projection = projection
     c.cyl_focal = cyl_focal
+    c.refine_enabled = 1 if refine else 0
+    c.refine_margin, c.ransac_iters, c.inlier_px = refine_margin, ransac_iters, inlier_px
+    c.detect_threshold, c.match_ratio, c.seed = detect_threshold, match_ratio, seed
     return c
 
 
 class OracleState:
     """so_state: the oracle's PipelineState (initialize + process_frame)."""
 
-    def __init__(self, cfg: SoConfig):
+    def __init__(self, cfg: SoConfig, first_frames=None):
         self.cfg = cfg
         err = C.c_int(SO_OK)
-        self._h = lib().so_initialize(C.byref(cfg), C.byref(err))
+        if first_frames is not None:
+            refs = [FrameRef(f) for f in first_frames]
+            arr = (SoFrame * len(refs))(*[r.c for r in refs])
+            self._h = lib().so_initialize_frames(C.byref(cfg), arr, C.byref(err))
+        else:
+            self._h = lib().so_initialize(C.byref(cfg), C.byref(err))
         if not self._h:
             raise OracleError(err.value)
         w, h, ox, oy = C.c_int(), C.c_int(), C.c_double(), C.c_double()
@@ -411,6 +504,9 @@ class OracleState:
         r = SoRegion()
         lib().so_state_view_bbox(self._h, v, C.byref(r))
         return (r.x0, r.y0, r.x1, r.y1)
+
+    def refine_warning(self, k) -> bool:
+        return bool(lib().so_state_refine_warning(self._h, k))
 
     def maps(self, v):
         h = (C.c_double * 9)()

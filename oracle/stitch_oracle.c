@@ -1178,6 +1178,7 @@ struct so_state {
   /* debug intermediates of the last frame */
   so_frame dbg_warped[SO_MAX_VIEWS];
   float* dbg_flow[SO_MAX_VIEWS][2][2];
+  int refine_warning[SO_MAX_VIEWS];
 };
 
 static int effective_topology(const so_config* c) {
@@ -1229,6 +1230,47 @@ static void build_pairs(so_state* s) {
 /* initialize, pipeline.cpp:209-257, with refinement disabled (the
  * per-frame path's configs use fixed/coarse homographies).  Masks depend
  * only on geometry for unmasked inputs, so a zero frame is warped. */
+/* rebuild_pair_geometry (pipeline.cpp:181-205): warp masks (geometry only:
+ * the warped pixel values are not needed), view footprints, overlap bounds
+ * and blend weights of every pair. */
+static int rebuild_pair_geometry(so_state* s) {
+  const so_config* cfg = &s->cfg;
+  so_frame warped[SO_MAX_VIEWS];
+  for (int v = 0; v < cfg->n_views; ++v) {
+    so_frame zero;
+    frame_alloc(&zero, cfg->width[v], cfg->height[v], 0, 0);
+    int e = so_warp_frame_lift(&zero, s->inv[v], s->canvas_w, s->canvas_h, s->offx,
+                               s->offy, s->lsin, s->lcos, s->lh, cfg->threads, &warped[v]);
+    so_free_frame(&zero);
+    if (e != SO_OK) {
+      for (int u = 0; u < v; ++u) so_free_frame(&warped[u]);
+      return e;
+    }
+    mask_bbox(&warped[v], &s->view_bbox[v]);
+  }
+  for (int k = 0; k < s->n_pairs; ++k) {
+    so_pair* p = &s->pairs[k];
+    int e = overlap_bounds(&warped[p->view], &warped[p->partner], &p->bounds);
+    if (e != SO_OK) {
+      for (int u = 0; u < cfg->n_views; ++u) so_free_frame(&warped[u]);
+      for (int q = 0; q < k; ++q) {
+        free(s->pairs[q].theta_i);
+        free(s->pairs[q].theta_j);
+        s->pairs[q].theta_i = s->pairs[q].theta_j = NULL;
+      }
+      return (e == SO_NoOverlap) ? SO_ConfigurationError : e;
+    }
+    const size_t n = (size_t)(p->bounds.x1 - p->bounds.x0) *
+                     (p->bounds.y1 - p->bounds.y0);
+    p->theta_i = (float*)malloc(sizeof(float) * n);
+    p->theta_j = (float*)malloc(sizeof(float) * n);
+    so_blend_weights(&warped[p->view], &warped[p->partner], p->bounds,
+                     p->theta_i, p->theta_j);
+  }
+  for (int v = 0; v < cfg->n_views; ++v) so_free_frame(&warped[v]);
+  return SO_OK;
+}
+
 so_state* so_initialize(const so_config* cfg, int* err) {
   *err = SO_OK;
   if (cfg->n_views < 2 || cfg->n_views > SO_MAX_VIEWS || cfg->reference < 0 ||
@@ -1332,45 +1374,148 @@ so_state* so_initialize(const so_config* cfg, int* err) {
     s->pairs[k].window.capacity = wc;
     s->pairs[k].window.size = 0;
   }
-  /* rebuild_pair_geometry, pipeline.cpp:181-205 */
-  so_frame warped[SO_MAX_VIEWS];
-  for (int v = 0; v < cfg->n_views; ++v) {
-    so_frame zero;
-    frame_alloc(&zero, cfg->width[v], cfg->height[v], 0, 0);
-    int e = so_warp_frame_lift(&zero, s->inv[v], s->canvas_w, s->canvas_h, s->offx,
-                               s->offy, s->lsin, s->lcos, s->lh, cfg->threads, &warped[v]);
-    so_free_frame(&zero);
-    if (e != SO_OK) {
-      *err = e;
-      for (int u = 0; u <= v; ++u) so_free_frame(&warped[u]);
-      free(s);
-      return NULL;
-    }
-    mask_bbox(&warped[v], &s->view_bbox[v]);
+  int e = rebuild_pair_geometry(s);
+  if (e != SO_OK) {
+    *err = e;
+    free(s->lsin);
+    free(s->lcos);
+    free(s->lh);
+    free(s);
+    return NULL;
   }
-  for (int k = 0; k < s->n_pairs; ++k) {
-    so_pair* p = &s->pairs[k];
-    int e = overlap_bounds(&warped[p->view], &warped[p->partner], &p->bounds);
-    if (e != SO_OK) {
-      *err = (e == SO_NoOverlap) ? SO_ConfigurationError : e;
-      for (int u = 0; u < cfg->n_views; ++u) so_free_frame(&warped[u]);
-      for (int q = 0; q < k; ++q) {
-        free(s->pairs[q].theta_i);
-        free(s->pairs[q].theta_j);
-      }
-      free(s);
-      return NULL;
-    }
-    const size_t n = (size_t)(p->bounds.x1 - p->bounds.x0) *
-                     (p->bounds.y1 - p->bounds.y0);
-    p->theta_i = (float*)malloc(sizeof(float) * n);
-    p->theta_j = (float*)malloc(sizeof(float) * n);
-    so_blend_weights(&warped[p->view], &warped[p->partner], p->bounds,
-                     p->theta_i, p->theta_j);
-  }
-  for (int v = 0; v < cfg->n_views; ++v) so_free_frame(&warped[v]);
   return s;
 }
+
+/* Homography::apply with hnormalized (geometry.cpp:33-36) */
+static void h_apply(const double* h, double x, double y, double* ox, double* oy) {
+  const double q0 = (h[0] * x + h[1] * y) + h[2];
+  const double q1 = (h[3] * x + h[4] * y) + h[5];
+  const double q2 = (h[6] * x + h[7] * y) + h[8];
+  *ox = q0 / q2;
+  *oy = q1 / q2;
+}
+
+/* broaden (geometry.cpp:119-133) */
+static so_region broaden(so_region r, double margin, so_region b) {
+  const int mx = (int)lround(margin * (r.x1 - r.x0));
+  const int my = (int)lround(margin * (r.y1 - r.y0));
+  so_region o;
+  o.x0 = r.x0 - mx > b.x0 ? r.x0 - mx : b.x0;
+  o.y0 = r.y0 - my > b.y0 ? r.y0 - my : b.y0;
+  o.x1 = r.x1 + mx < b.x1 ? r.x1 + mx : b.x1;
+  o.y1 = r.y1 + my < b.y1 ? r.y1 + my : b.y1;
+  return o;
+}
+
+/* refine_pair (pipeline.cpp:114-179) against the pair's partner (the
+ * reference for the star topology): detect / describe / match on the
+ * broadened overlap of the warped first frames, matches back-projected to
+ * the view's source plane, RANSAC scale + translation, translation carried
+ * to the plane with the local Jacobian, map := T * H * S. */
+static void refine_pair(so_state* s, const so_frame* warped, int k) {
+  const so_config* cfg = &s->cfg;
+  so_pair* p = &s->pairs[k];
+  s->refine_warning[k] = 1;
+  const so_region canvas_r = {0, 0, s->canvas_w, s->canvas_h};
+  const so_region search = broaden(p->bounds, cfg->refine_margin, canvas_r);
+  so_keypoint *kv = NULL, *kr = NULL;
+  int nv = 0, nr = 0;
+  if (so_detect(&warped[p->view], search, cfg->detect_threshold, &kv, &nv) != SO_OK ||
+      so_detect(&warped[p->partner], search, cfg->detect_threshold, &kr, &nr) != SO_OK ||
+      nv == 0 || nr == 0) {
+    free(kv);
+    free(kr);
+    return;
+  }
+  float* dv = (float*)malloc(sizeof(float) * 64 * nv);
+  float* dr = (float*)malloc(sizeof(float) * 64 * nr);
+  so_describe(&warped[p->view], kv, nv, dv);
+  so_describe(&warped[p->partner], kr, nr, dr);
+  so_match_pair* m = (so_match_pair*)malloc(sizeof(so_match_pair) * (nv > 0 ? nv : 1));
+  const int nm = so_match(dv, nv, dr, nr, kv, kr, cfg->match_ratio, m);
+  const double* map = s->maps[p->view];
+  double inv_raw[9], inv[9];
+  so_inverse3(map, inv_raw);
+  homography_from_matrix(inv_raw, inv); /* Homography::inverse, geometry.cpp:29-31 */
+  for (int i = 0; i < nm; ++i) {
+    double qx, qy, px, py;
+    h_apply(inv, m[i].ax + s->offx, m[i].ay + s->offy, &qx, &qy);
+    h_apply(inv, m[i].bx + s->offx, m[i].by + s->offy, &px, &py);
+    m[i].ax = qx;
+    m[i].ay = qy;
+    m[i].bx = px;
+    m[i].by = py;
+  }
+  so_similarity fit;
+  const int e = so_ransac(m, nm, cfg->ransac_iters, cfg->inlier_px, 0.5, 2.0,
+                          cfg->seed + (unsigned long long)p->view, &fit);
+  free(kv);
+  free(kr);
+  free(dv);
+  free(dr);
+  free(m);
+  if (e != SO_OK) return; /* NoConsensus / InsufficientMatches: keep the map */
+  /* centre of the overlap and local_jacobian (pipeline.cpp:98-112) */
+  const double cx = s->offx + p->bounds.x0 + (p->bounds.x1 - p->bounds.x0) / 2.0;
+  const double cy = s->offy + p->bounds.y0 + (p->bounds.y1 - p->bounds.y0) / 2.0;
+  double ax, ay;
+  h_apply(inv, cx, cy, &ax, &ay);
+  const double eps = 1e-4;
+  double xp0, yp0, xm0, ym0, xp1, yp1, xm1, ym1;
+  h_apply(map, ax + eps, ay, &xp0, &yp0);
+  h_apply(map, ax - eps, ay, &xm0, &ym0);
+  h_apply(map, ax, ay + eps, &xp1, &yp1);
+  h_apply(map, ax, ay - eps, &xm1, &ym1);
+  const double j00 = (xp0 - xm0) / (2 * eps), j10 = (yp0 - ym0) / (2 * eps);
+  const double j01 = (xp1 - xm1) / (2 * eps), j11 = (yp1 - ym1) / (2 * eps);
+  const double tx = j00 * fit.t_x + j01 * fit.t_y;
+  const double ty = j10 * fit.t_x + j11 * fit.t_y;
+  /* refine_homography (geometry.cpp:135-145): T(tx, ty) * H * S(sx, sy) */
+  const double t[9] = {1, 0, tx, 0, 1, ty, 0, 0, 1};
+  const double sc[9] = {fit.s_x, 0, 0, 0, fit.s_y, 0, 0, 0, 1};
+  double th[9], ths[9];
+  mul3(t, map, th);
+  mul3(th, sc, ths);
+  double refined[9];
+  if (homography_from_matrix(ths, refined) != SO_OK) return;
+  memcpy(s->maps[p->view], refined, sizeof(refined));
+  so_inverse3(s->maps[p->view], s->inv[p->view]); /* pipeline.cpp:40 */
+  s->refine_warning[k] = 0;
+}
+
+so_state* so_initialize_frames(const so_config* cfg, const so_frame* first, int* err) {
+  so_state* s = so_initialize(cfg, err);
+  if (!s || !cfg->refine_enabled || !first) return s;
+  if (cfg->projection == 1) return s; /* refinement serves the planar canvas */
+  so_frame warped[SO_MAX_VIEWS];
+  for (int v = 0; v < cfg->n_views; ++v) {
+    const int e = so_warp_frame(&first[v], s->inv[v], s->canvas_w, s->canvas_h, s->offx, s->offy,
+                                cfg->threads, &warped[v]);
+    if (e != SO_OK) {
+      for (int u = 0; u < v; ++u) so_free_frame(&warped[u]);
+      so_destroy(s);
+      *err = e;
+      return NULL;
+    }
+  }
+  for (int k = 0; k < s->n_pairs; ++k) refine_pair(s, warped, k);
+  for (int v = 0; v < cfg->n_views; ++v) so_free_frame(&warped[v]);
+  /* refinement moved the maps: bounds and weights shift (pipeline.cpp:254) */
+  for (int k = 0; k < s->n_pairs; ++k) {
+    free(s->pairs[k].theta_i);
+    free(s->pairs[k].theta_j);
+    s->pairs[k].theta_i = s->pairs[k].theta_j = NULL;
+  }
+  const int e = rebuild_pair_geometry(s);
+  if (e != SO_OK) {
+    so_destroy(s);
+    *err = e;
+    return NULL;
+  }
+  return s;
+}
+
+int so_state_refine_warning(const so_state* s, int k) { return s->refine_warning[k]; }
 
 void so_destroy(so_state* s) {
   if (!s) return;

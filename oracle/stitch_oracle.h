@@ -100,6 +100,15 @@ typedef struct {
    * (sin t, h, cos t); samples behind the camera are invalid) */
   int projection;
   double cyl_focal;   /* pixels per radian; 0 = reference fx */
+  /* RefineOptions (pipeline.hpp:23-31) + StitchConfig.seed; refinement runs
+   * in so_initialize_frames only (it needs the first frames) */
+  int refine_enabled;
+  double refine_margin;
+  int ransac_iters;
+  double inlier_px;
+  double detect_threshold;
+  double match_ratio;
+  unsigned long long seed;
 } so_config;
 
 typedef struct {
@@ -167,8 +176,34 @@ int so_compose_panorama(const so_frame* wi, const so_frame* wj,
                         const so_frame* fused, so_region overlap,
                         so_frame* out);
 
+/* ---- feature refinement (features.cpp, features_oracle.cpp) ---- */
+typedef struct {
+  double x, y, scale, response;
+} so_keypoint;
+typedef struct {
+  int index_a, index_b;
+  double distance, ax, ay, bx, by;
+} so_match_pair;
+typedef struct {
+  double s_x, s_y, t_x, t_y;
+} so_similarity;
+/* *out is malloc'ed (free()); SO_RegionTooSmall below 32x32 */
+int so_detect(const so_frame* f, so_region r, double threshold, so_keypoint** out, int* n_out);
+void so_describe(const so_frame* f, const so_keypoint* kps, int n, float* desc /* n*64 */);
+/* out: capacity na; returns the match count */
+int so_match(const float* da, int na, const float* db, int nb, const so_keypoint* ka,
+             const so_keypoint* kb, double ratio, so_match_pair* out);
+int so_ransac(const so_match_pair* m, int n, int iterations, double inlier_px, double min_scale,
+              double max_scale, unsigned long long seed, so_similarity* out);
+
 /* ---- pipeline (pipeline.cpp:209-360) ---- */
 so_state* so_initialize(const so_config* cfg, int* err);
+/* initialize() with the first frames: feature refinement when
+ * cfg->refine_enabled (pipeline.cpp:241-255, refine_pair :114-179) */
+so_state* so_initialize_frames(const so_config* cfg, const so_frame* first_frames, int* err);
+/* the (possibly refined) view->reference maps and whether pair k's
+ * refinement was kept (0) or fell back to the unrefined map (1) */
+int so_state_refine_warning(const so_state* s, int k);
 void so_destroy(so_state* s);
 int so_process_frame(so_state* s, const so_frame* frames, so_frame* pano,
                      so_report* rep);

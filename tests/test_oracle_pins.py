@@ -358,3 +358,61 @@ def test_ssim_examples():
     assert abs(O.ssim(a, None, b, bm) - _np_ssim(a, None, b, bm)) <= 1e-6
     with pytest.raises(O.OracleError):
         O.ssim(a[:10], None, a[:10], None)  # TooSmall
+
+
+# ---- feature refinement (features.cpp) ----
+def _disc(h=96, w=96, cx=40, cy=48, r=8):
+    yy, xx = np.mgrid[:h, :w]
+    img = np.full((h, w, 3), 255, np.uint8)
+    img[(yy - cy) ** 2 + (xx - cx) ** 2 <= r * r] = 0
+    return img
+
+
+def test_detect_examples():
+    flat = np.full((64, 64, 3), 128, np.uint8)
+    assert O.detect(flat, None, (0, 0, 64, 64)) == []
+    img = _disc()
+    kps = O.detect(img, None, (0, 0, 96, 96))
+    assert kps and abs(kps[0][0] - 40) <= 2 and abs(kps[0][1] - 48) <= 2
+    assert 8 / 2.5 <= kps[0][2] <= 8 * 2  # detection sigma of the strongest blob vs radius 8
+    assert kps == O.detect(img, None, (0, 0, 96, 96))  # deterministic
+    resp = [k[3] for k in kps]
+    assert resp == sorted(resp, reverse=True)
+    with pytest.raises(O.OracleError):
+        O.detect(img, None, (0, 0, 31, 96))  # RegionTooSmall
+
+
+def test_describe_and_match_examples():
+    rng = np.random.default_rng(31)
+    img = (rng.random((120, 160, 3)) * 255).astype(np.uint8)
+    img = np.repeat(np.repeat(img[::4, ::4], 4, axis=0), 4, axis=1)  # blocky texture
+    kps = O.detect(img, None, (0, 0, 160, 120))
+    d = O.describe(img, None, kps)
+    assert np.allclose(np.linalg.norm(d, axis=1), 1.0, atol=1e-5)
+    np.testing.assert_array_equal(d, O.describe(img.copy(), None, kps))
+    m = O.match(d, d, kps, kps)
+    assert len(m) == len(kps) and all(a == b for a, b, *_ in m)  # identity matching
+    dup = np.concatenate([d, d[:1]])  # a duplicated descriptor fails the ratio test
+    m2 = O.match(d[:1], dup, kps[:1], kps + kps[:1])
+    assert m2 == []
+
+
+def test_ransac_examples():
+    rng = np.random.default_rng(32)
+    pts = rng.random((60, 2)) * 600
+    exact = [(x, y, 1.1 * x + 4, 1.0 * y - 2) for x, y in pts]
+    sx, sy, tx, ty = O.ransac(exact, seed=7)
+    assert abs(sx - 1.1) <= 1e-9 and abs(sy - 1.0) <= 1e-9
+    assert abs(tx - 4) <= 1e-6 and abs(ty + 2) <= 1e-6
+    noisy = list(exact)
+    for i in range(0, 60, 5):  # 40 % uniform outliers
+        noisy[i] = (pts[i][0], pts[i][1], rng.random() * 600, rng.random() * 600)
+    for i in range(1, 60, 5):
+        noisy[i] = (pts[i][0], pts[i][1], rng.random() * 600, rng.random() * 600)
+    sx, sy, tx, ty = O.ransac(noisy, seed=7)
+    assert abs(sx - 1.1) <= 0.01 and abs(sy - 1.0) <= 0.01
+    assert abs(tx - 4) <= 0.5 and abs(ty + 2) <= 0.5
+    perm = [noisy[i] for i in rng.permutation(60)]
+    assert O.ransac(perm, seed=7) == O.ransac(noisy, seed=7)  # canonical order
+    with pytest.raises(O.OracleError):
+        O.ransac(exact[:1])  # InsufficientMatches
