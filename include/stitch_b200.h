@@ -60,10 +60,9 @@ typedef struct {
   double translation[3];
 } stitch_b200_camera;
 
-/* StitchConfig (pipeline.hpp:33-44) restricted to what the per-frame path
- * consumes.  refine_enabled must be 0: feature refinement is init-only and
- * out of scope; pass refined maps through
- * stitch_b200_create() instead. */
+/* StitchConfig (pipeline.hpp:33-44).  Feature refinement (refine_enabled,
+ * RefineOptions pipeline.hpp:23-31) runs in stitch_b200_initialize_frames,
+ * which receives the first frames it needs (planar canvas only). */
 typedef struct {
   int n_views;
   int reference;
@@ -81,13 +80,20 @@ typedef struct {
   int fuse_weighting;  /* 0 = own (OwnWeightOnOwnFlow), 1 = cross */
   int topology;        /* 0 = auto (star <= 3 views, chain beyond), 1 star, 2 chain,
                           3 ring chain (360 degree rigs) */
-  int refine_enabled;  /* must be 0 */
+  int refine_enabled;  /* 1: refine_pair at init (stitch_b200_initialize_frames) */
   /* Extension (not in the reference, which is planar only): 0 = planar
    * canvas (the reference's world plane), 1 = cylindrical 360-degree canvas
    * around the reference camera, cyl_focal pixels per radian (0: the
    * reference camera's fx).  Cameras must share their centre. */
   int projection;
   double cyl_focal;
+  /* RefineOptions (pipeline.hpp:23-31) and StitchConfig.seed */
+  double refine_margin;     /* 0.15 */
+  int ransac_iters;         /* 500 */
+  double inlier_px;         /* 2.0 */
+  double detect_threshold;  /* 2e-4 */
+  double match_ratio;       /* 0.8 */
+  unsigned long long seed;  /* RANSAC seed base (+ view index) */
 } stitch_b200_config;
 
 /* Fill a config with the reference defaults (pipeline.hpp:23-44,
@@ -160,6 +166,20 @@ int stitch_b200_create(const stitch_b200_init* init, int device,
 int stitch_b200_initialize(const stitch_b200_config* cfg, int device,
                            stitch_b200_ctx** out);
 
+/* initialize() with the first frames (host RGB8, one per view): with
+ * cfg->refine_enabled the maps are refined from feature matches on the
+ * warped first frames (refine_pair, pipeline.cpp:114-179: detection,
+ * description and matching on the device, RANSAC on the host with the
+ * reference's std::mt19937_64 stream), then the pair geometry is rebuilt on
+ * the device (pipeline.cpp:241-255). */
+int stitch_b200_initialize_frames(const stitch_b200_config* cfg,
+                                  const uint8_t* const* frames, int device,
+                                  stitch_b200_ctx** out);
+
+/* 1 when pair k's refinement fell back to the unrefined map
+ * (PairState::refine_warning: too few keypoints / matches, no consensus). */
+int stitch_b200_refine_warning(const stitch_b200_ctx* ctx, int k);
+
 /* Re-upload geometry (re-refinement, pipeline.cpp:395-406): the 3D-M
  * windows, threshold history and frame counter are kept. */
 int stitch_b200_update_geometry(stitch_b200_ctx* ctx,
@@ -197,6 +217,17 @@ int stitch_b200_ssim(int width, int height, const uint8_t* a_rgb, const uint8_t*
  * out[0] = psnr(corrected, source), out[1] = psnr(corrected, reference),
  * out[2] = ssim(corrected, reference). */
 int stitch_b200_pair_quality(stitch_b200_ctx* ctx, int k, double out[3]);
+
+/* Feature-path diagnostics (the device kernels of stitch_b200_initialize_frames
+ * on one host RGB8 frame, for parity tests): detect over region
+ * {x0, y0, x1, y1} + describe; kp gets 4 doubles (x, y, scale, response) and
+ * desc 64 floats per keypoint, at most max_kp.  Returns the keypoint count,
+ * or minus an error code.  debug_match: the device matching of two
+ * descriptor sets (best_b[a] = ratio-tested nearest b or -1, best_a[b]). */
+int stitch_b200_debug_detect(int width, int height, const uint8_t* rgb, const int region[4],
+                             double threshold, int max_kp, double* kp, float* desc);
+int stitch_b200_debug_match(const float* da, int na, const float* db, int nb, double ratio,
+                            int* best_b, double* best_dist, int* best_a);
 
 /* Geometry of a context. */
 int stitch_b200_canvas(const stitch_b200_ctx* ctx, int* width, int* height,

@@ -130,10 +130,9 @@ struct ViewSetup {
 };
 
 struct RefineOptions {
-  // Feature refinement is init-only and outside the per-frame B200 path;
-  // refined maps enter through the C ABI's stitch_b200_create().  The mirror
-  // defaults it off (the reference defaults it on) and initialize() throws
-  // Unsupported when it is requested.
+  // Feature refinement at initialize(): detection / description / matching on
+  // the device, RANSAC on the host (stitch_b200_initialize_frames).  The
+  // mirror defaults it off (the reference defaults it on).
   bool enabled = false;
   double margin = 0.15;
   int ransac_iters = 500;
@@ -268,10 +267,17 @@ inline stitch_b200_config to_c(const StitchConfig& config, const std::vector<Fra
   c.fuse_weighting = config.fuse_weighting == FuseWeighting::CrossWeightOnOwnFlow ? 1 : 0;
   c.topology = config.topology;
   c.refine_enabled = config.refine.enabled ? 1 : 0;
+  c.refine_margin = config.refine.margin;
+  c.ransac_iters = config.refine.ransac_iters;
+  c.inlier_px = config.refine.inlier_px;
+  c.detect_threshold = config.refine.detect_threshold;
+  c.match_ratio = config.refine.match_ratio;
+  c.seed = config.seed;
   return c;
 }
 
-// initialize (pipeline.hpp:73-74), refinement off.
+// initialize (pipeline.hpp:73-74); with refine.enabled the first frames feed
+// the feature refinement (pipeline.cpp:241-255).
 inline PipelineState initialize(const StitchConfig& config, const std::vector<Frame>& first_frames) {
   const int n = static_cast<int>(config.views.size());
   if (n < 2 || n > STITCH_B200_MAX_VIEWS)
@@ -280,7 +286,13 @@ inline PipelineState initialize(const StitchConfig& config, const std::vector<Fr
     throw StitchError(ErrorCode::ConfigurationError, "frame count does not match configured views");
   stitch_b200_config c = to_c(config, first_frames);
   stitch_b200_ctx* ctx = nullptr;
-  check(stitch_b200_initialize(&c, config.device, &ctx));
+  if (config.refine.enabled) {
+    std::vector<const std::uint8_t*> ptrs;
+    for (const Frame& f : first_frames) ptrs.push_back(f.data.data());
+    check(stitch_b200_initialize_frames(&c, ptrs.data(), config.device, &ctx));
+  } else {
+    check(stitch_b200_initialize(&c, config.device, &ctx));
+  }
   return PipelineState(ctx, config);
 }
 

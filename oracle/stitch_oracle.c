@@ -1412,7 +1412,7 @@ static so_region broaden(so_region r, double margin, so_region b) {
  * broadened overlap of the warped first frames, matches back-projected to
  * the view's source plane, RANSAC scale + translation, translation carried
  * to the plane with the local Jacobian, map := T * H * S. */
-static void refine_pair(so_state* s, const so_frame* warped, int k) {
+static int refine_pair(so_state* s, const so_frame* warped, int k) {
   const so_config* cfg = &s->cfg;
   so_pair* p = &s->pairs[k];
   s->refine_warning[k] = 1;
@@ -1425,7 +1425,7 @@ static void refine_pair(so_state* s, const so_frame* warped, int k) {
       nv == 0 || nr == 0) {
     free(kv);
     free(kr);
-    return;
+    return SO_OK;
   }
   float* dv = (float*)malloc(sizeof(float) * 64 * nv);
   float* dr = (float*)malloc(sizeof(float) * 64 * nr);
@@ -1454,7 +1454,7 @@ static void refine_pair(so_state* s, const so_frame* warped, int k) {
   free(dv);
   free(dr);
   free(m);
-  if (e != SO_OK) return; /* NoConsensus / InsufficientMatches: keep the map */
+  if (e != SO_OK) return SO_OK; /* NoConsensus / InsufficientMatches: keep the map */
   /* centre of the overlap and local_jacobian (pipeline.cpp:98-112) */
   const double cx = s->offx + p->bounds.x0 + (p->bounds.x1 - p->bounds.x0) / 2.0;
   const double cy = s->offy + p->bounds.y0 + (p->bounds.y1 - p->bounds.y0) / 2.0;
@@ -1477,10 +1477,12 @@ static void refine_pair(so_state* s, const so_frame* warped, int k) {
   mul3(t, map, th);
   mul3(th, sc, ths);
   double refined[9];
-  if (homography_from_matrix(ths, refined) != SO_OK) return;
+  const int fe = homography_from_matrix(ths, refined);
+  if (fe != SO_OK) return fe; /* SingularHomography propagates (pipeline.cpp:171-177) */
   memcpy(s->maps[p->view], refined, sizeof(refined));
   so_inverse3(s->maps[p->view], s->inv[p->view]); /* pipeline.cpp:40 */
   s->refine_warning[k] = 0;
+  return SO_OK;
 }
 
 so_state* so_initialize_frames(const so_config* cfg, const so_frame* first, int* err) {
@@ -1498,8 +1500,14 @@ so_state* so_initialize_frames(const so_config* cfg, const so_frame* first, int*
       return NULL;
     }
   }
-  for (int k = 0; k < s->n_pairs; ++k) refine_pair(s, warped, k);
+  int re = SO_OK;
+  for (int k = 0; k < s->n_pairs && re == SO_OK; ++k) re = refine_pair(s, warped, k);
   for (int v = 0; v < cfg->n_views; ++v) so_free_frame(&warped[v]);
+  if (re != SO_OK) {
+    so_destroy(s);
+    *err = re;
+    return NULL;
+  }
   /* refinement moved the maps: bounds and weights shift (pipeline.cpp:254) */
   for (int k = 0; k < s->n_pairs; ++k) {
     free(s->pairs[k].theta_i);

@@ -25,7 +25,10 @@ class Config(C.Structure):
                 ("flow_levels", C.c_int), ("flow_iterations", C.c_int),
                 ("smoothness", C.c_double), ("window_capacity", C.c_int),
                 ("fuse_weighting", C.c_int), ("topology", C.c_int), ("refine_enabled", C.c_int),
-                ("projection", C.c_int), ("cyl_focal", C.c_double)]
+                ("projection", C.c_int), ("cyl_focal", C.c_double),
+                ("refine_margin", C.c_double), ("ransac_iters", C.c_int),
+                ("inlier_px", C.c_double), ("detect_threshold", C.c_double),
+                ("match_ratio", C.c_double), ("seed", C.c_ulonglong)]
 
 
 class Pair(C.Structure):
@@ -79,6 +82,13 @@ SYMBOLS = [
     ("stitch_b200_initialize", C.c_int, [C.POINTER(Config), C.c_int, C.POINTER(C.c_void_p)]),
     ("stitch_b200_update_geometry", C.c_int, [C.c_void_p, C.POINTER(Init)]),
     ("stitch_b200_update_maps", C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
+    ("stitch_b200_initialize_frames", C.c_int, [C.POINTER(Config), C.c_void_p, C.c_int,
+                                                C.POINTER(C.c_void_p)]),
+    ("stitch_b200_refine_warning", C.c_int, [C.c_void_p, C.c_int]),
+    ("stitch_b200_debug_detect", C.c_int, [C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_int),
+                                           C.c_double, C.c_int, C.c_void_p, C.c_void_p]),
+    ("stitch_b200_debug_match", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_double,
+                                          C.c_void_p, C.c_void_p, C.c_void_p]),
     ("stitch_b200_camera_maps", C.c_int, [C.POINTER(Config), C.POINTER(C.c_double)]),
     ("stitch_b200_psnr", C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_void_p, C.POINTER(C.c_double)]),

@@ -57,6 +57,7 @@ struct Ctx {
   DevState* dst = nullptr;
   stitch_b200_init init{};  // copy (theta pointers re-pointed at host copies)
   std::vector<std::vector<float>> theta_host;
+  std::vector<int> refine_warning;  // per pair (initialize_frames with refinement)
   std::vector<void*> allocs;
   std::uint8_t* d_frames[kMaxViews] = {};
   size_t frame_bytes[kMaxViews] = {};
@@ -820,6 +821,12 @@ void stitch_b200_config_defaults(stitch_b200_config* c) {
   c->refine_enabled = 0;
   c->projection = 0;
   c->cyl_focal = 0.0;
+  c->refine_margin = 0.15;  // RefineOptions defaults (pipeline.hpp:23-31)
+  c->ransac_iters = 500;
+  c->inlier_px = 2.0;
+  c->detect_threshold = 2e-4;
+  c->match_ratio = 0.8;
+  c->seed = 0;
   for (int v = 0; v < STITCH_B200_MAX_VIEWS; ++v) {
     c->cams[v].fx = c->cams[v].fy = 1.0;
     c->cams[v].rotation[0] = c->cams[v].rotation[4] = c->cams[v].rotation[8] = 1.0;
@@ -835,12 +842,136 @@ int stitch_b200_create(const stitch_b200_init* init, int device, stitch_b200_ctx
   return STITCH_B200_OK;
 }
 
-int stitch_b200_initialize(const stitch_b200_config* cfg, int device, stitch_b200_ctx** out) {
+// refine_pair (pipeline.cpp:114-179) for every pair, on the first frames
+// warped with the unrefined maps: detection, description and matching on
+// the device (features_kernels.cu), back-projection, RANSAC, the Jacobian
+// transport and refine_homography on the host.  maps / invs of refined views
+// are replaced; warn[k] = PairState::refine_warning.
+static int refine_maps(int device, const stitch_b200_config* cfg, const uint8_t* const* frames,
+                       const Geometry& geom, const std::vector<PairGeometry>& pgeo,
+                       const std::vector<hg_ns::PairSpec>& pairs, std::vector<hg_ns::Mat3>& maps,
+                       std::vector<hg_ns::Mat3>& invs, std::vector<int>& warn) {
+  CUDA_TRY(cudaSetDevice(device));
+  const int cw = geom.canvas_w, ch = geom.canvas_h;
+  if (ch >= (1 << 13) || cw >= (1 << 15))
+    return fail(STITCH_B200_Unsupported, "refinement supports canvases below 32768 x 8192");
+  cudaStream_t s = nullptr;
+  CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  struct Guard {
+    cudaStream_t s;
+    std::vector<void*> p;
+    ~Guard() {
+      for (void* q : p) cudaFree(q);
+      cudaStreamDestroy(s);
+    }
+  } gd{s, {}};
+  auto dalloc = [&](void** q, size_t n) -> cudaError_t {
+    cudaError_t e = cudaMalloc(q, n + 16);
+    if (e == cudaSuccess) gd.p.push_back(*q);
+    return e;
+  };
+  void* dg = nullptr;
+  CUDA_TRY(dalloc(&dg, sizeof(Geometry)));
+  CUDA_TRY(cudaMemcpyAsync(dg, &geom, sizeof(Geometry), cudaMemcpyHostToDevice, s));
+  const size_t P = static_cast<size_t>(cw) * ch;
+  void *wrgb = nullptr, *wmask = nullptr;
+  CUDA_TRY(dalloc(&wrgb, 3 * P));
+  CUDA_TRY(dalloc(&wmask, P));
+  // warp_frame of the first frames (the per-frame sampler's arithmetic) and
+  // the integral image of each warped view taking part in a pair
+  std::vector<std::unique_ptr<FeatView>> fv(cfg->n_views);
+  for (const auto& pr : pairs)
+    for (int v : {pr.view, pr.partner}) {
+      if (fv[v]) continue;
+      const size_t npx = static_cast<size_t>(cfg->width[v]) * cfg->height[v];
+      void *src = nullptr, *rgba = nullptr;
+      CUDA_TRY(dalloc(&src, 3 * npx));
+      CUDA_TRY(dalloc(&rgba, 4 * npx));
+      CUDA_TRY(cudaMemcpyAsync(src, frames[v], 3 * npx, cudaMemcpyHostToDevice, s));
+      launch_expand_one(static_cast<const std::uint8_t*>(src), static_cast<uchar4*>(rgba),
+                        static_cast<long long>(npx), s);
+      launch_warp_view(static_cast<const Geometry*>(dg), v, static_cast<const uchar4*>(rgba),
+                       static_cast<std::uint8_t*>(wrgb), static_cast<std::uint8_t*>(wmask), s);
+      CUDA_TRY(cudaGetLastError());
+      fv[v].reset(new FeatView());
+      CUDA_TRY(fv[v]->build(static_cast<const std::uint8_t*>(wrgb), cw, ch, s));
+    }
+  const int canvas_r[4] = {0, 0, cw, ch};
+  warn.assign(pairs.size(), 1);
+  for (size_t k = 0; k < pairs.size(); ++k) {
+    const int view = pairs[k].view, partner = pairs[k].partner;
+    int search[4];
+    hg_ns::broaden(pgeo[k].bounds, cfg->refine_margin, canvas_r, search);
+    if (search[2] - search[0] < 32 || search[3] - search[1] < 32) continue;  // RegionTooSmall
+    std::vector<FeatPoint> kv, kr;
+    std::vector<float> dv, dr;
+    CUDA_TRY(fv[view]->detect_describe(search[0], search[1], search[2], search[3],
+                                       cfg->detect_threshold, kv, dv, s));
+    CUDA_TRY(fv[partner]->detect_describe(search[0], search[1], search[2], search[3],
+                                          cfg->detect_threshold, kr, dr, s));
+    if (kv.empty() || kr.empty()) continue;
+    std::vector<int> best_b, best_a;
+    std::vector<double> best_dist;
+    CUDA_TRY(feat_match(dv, dr, static_cast<int>(kv.size()), static_cast<int>(kr.size()),
+                        cfg->match_ratio, best_b, best_dist, best_a, s));
+    const hg_ns::Mat3 map = maps[view];
+    hg_ns::Mat3 inv;
+    int rc = hg_ns::homography_inverse(map, inv);  // Homography::inverse
+    if (rc) return fail(rc, "singular map during refinement");
+    std::vector<hg_ns::MatchPt> m;
+    for (size_t a = 0; a < kv.size(); ++a) {
+      const int b = best_b[a];
+      if (b < 0 || best_a[b] != static_cast<int>(a)) continue;  // cross-check
+      hg_ns::MatchPt mp;
+      hg_ns::homography_apply(inv, kv[a].x + geom.offx, kv[a].y + geom.offy, mp.ax, mp.ay);
+      hg_ns::homography_apply(inv, kr[b].x + geom.offx, kr[b].y + geom.offy, mp.bx, mp.by);
+      mp.distance = best_dist[a];
+      m.push_back(mp);
+    }
+    hg_ns::ScaleShift fit;
+    rc = hg_ns::ransac_scale_translation(m, cfg->ransac_iters, cfg->inlier_px, 0.5, 2.0,
+                                         cfg->seed + static_cast<std::uint64_t>(view), fit);
+    if (rc) continue;  // InsufficientMatches / NoConsensus: keep the unrefined map
+    // translation carried to the plane with the local Jacobian at the
+    // overlap centre (pipeline.cpp:98-112, 160-170)
+    const int* bb = pgeo[k].bounds;
+    const double cx = geom.offx + bb[0] + (bb[2] - bb[0]) / 2.0;
+    const double cy = geom.offy + bb[1] + (bb[3] - bb[1]) / 2.0;
+    double ax, ay;
+    hg_ns::homography_apply(inv, cx, cy, ax, ay);
+    const double eps = 1e-4;
+    double xp0, yp0, xm0, ym0, xp1, yp1, xm1, ym1;
+    hg_ns::homography_apply(map, ax + eps, ay, xp0, yp0);
+    hg_ns::homography_apply(map, ax - eps, ay, xm0, ym0);
+    hg_ns::homography_apply(map, ax, ay + eps, xp1, yp1);
+    hg_ns::homography_apply(map, ax, ay - eps, xm1, ym1);
+    const double j00 = (xp0 - xm0) / (2 * eps), j10 = (yp0 - ym0) / (2 * eps);
+    const double j01 = (xp1 - xm1) / (2 * eps), j11 = (yp1 - ym1) / (2 * eps);
+    const double tx = j00 * fit.t_x + j01 * fit.t_y;
+    const double ty = j10 * fit.t_x + j11 * fit.t_y;
+    // refine_homography (geometry.cpp:135-145): T(tx, ty) * H * S(sx, sy)
+    const hg_ns::Mat3 t = {1, 0, tx, 0, 1, ty, 0, 0, 1};
+    const hg_ns::Mat3 sc = {fit.s_x, 0, 0, 0, fit.s_y, 0, 0, 0, 1};
+    hg_ns::Mat3 th, ths, refined;
+    hg_ns::mul3(t, map, th);
+    hg_ns::mul3(th, sc, ths);
+    rc = hg_ns::homography_from_matrix(ths, refined);
+    if (rc) return fail(rc, "refinement produced a singular map");
+    maps[view] = refined;
+    hg_ns::inverse3(refined, invs[view]);  // pipeline.cpp:40
+    warn[k] = 0;
+  }
+  return STITCH_B200_OK;
+}
+
+static int initialize_impl(const stitch_b200_config* cfg, const uint8_t* const* frames, int device,
+                           stitch_b200_ctx** out) {
   *out = nullptr;
-  if (cfg->refine_enabled)
-    return fail(STITCH_B200_Unsupported,
-                "feature refinement is init-only and not part of the B200 path; pass refined "
-                "maps through stitch_b200_create");
+  if (cfg->refine_enabled && !frames)
+    return fail(STITCH_B200_ConfigurationError,
+                "feature refinement needs the first frames: use stitch_b200_initialize_frames");
+  if (cfg->refine_enabled && cfg->projection == 1)
+    return fail(STITCH_B200_Unsupported, "feature refinement serves the planar canvas");
   if (cfg->n_views < 2 || cfg->n_views > kMaxViews)
     return fail(STITCH_B200_ConfigurationError, "n_views must be in [2, 16]");
   if (cfg->reference < 0 || cfg->reference >= cfg->n_views)
@@ -910,6 +1041,20 @@ int stitch_b200_initialize(const stitch_b200_config* cfg, int device, stitch_b20
   std::vector<PairGeometry> pgeo;
   int rc = init_geometry(device, g, make_lift(&in), cfg->n_views, vp, views, pgeo);
   if (rc) return rc;
+  std::vector<int> warn(pairs.size(), 0);
+  if (cfg->refine_enabled) {
+    for (size_t k = 0; k < pairs.size(); ++k)
+      if (!pgeo[k].ok) return fail(STITCH_B200_ConfigurationError, "adjacent views do not overlap");
+    rc = refine_maps(device, cfg, frames, g, pgeo, pairs, maps, invs, warn);
+    if (rc) return rc;
+    // refinement moved the maps: bounds and weights shift (pipeline.cpp:254);
+    // the canvas is kept (the reference computes it before refining)
+    for (int v = 0; v < cfg->n_views; ++v)
+      for (int i = 0; i < 9; ++i) in.inv_maps[v][i] = invs[v][i];
+    fill_views(g, &in);
+    rc = init_geometry(device, g, make_lift(&in), cfg->n_views, vp, views, pgeo);
+    if (rc) return rc;
+  }
   in.n_pairs = static_cast<int>(pairs.size());
   for (size_t k = 0; k < pairs.size(); ++k) {
     if (!pgeo[k].ok) return fail(STITCH_B200_ConfigurationError, "adjacent views do not overlap");
@@ -925,8 +1070,25 @@ int stitch_b200_initialize(const stitch_b200_config* cfg, int device, stitch_b20
   std::unique_ptr<Ctx> ctx;
   rc = build_context(&in, device, &views, ctx);
   if (rc) return rc;
+  ctx->refine_warning = warn;
   *out = new stitch_b200_ctx{std::move(ctx)};
   return STITCH_B200_OK;
+}
+
+int stitch_b200_initialize(const stitch_b200_config* cfg, int device, stitch_b200_ctx** out) {
+  return initialize_impl(cfg, nullptr, device, out);
+}
+
+int stitch_b200_initialize_frames(const stitch_b200_config* cfg, const uint8_t* const* frames,
+                                  int device, stitch_b200_ctx** out) {
+  if (!frames) return fail(STITCH_B200_ConfigurationError, "frames must not be NULL");
+  return initialize_impl(cfg, frames, device, out);
+}
+
+int stitch_b200_refine_warning(const stitch_b200_ctx* h, int k) {
+  const Ctx* ctx = h->c.get();
+  if (k < 0 || k >= ctx->hg.n_pairs) return 0;
+  return k < static_cast<int>(ctx->refine_warning.size()) ? ctx->refine_warning[k] : 0;
 }
 
 // Replace a context by a freshly built one, carrying the 3D-M windows,
@@ -1366,4 +1528,50 @@ int stitch_b200_pair_quality(stitch_b200_ctx* h, int k, double out[3]) {
   long long wn = 0;
   CUDA_TRY(gpu_ssim_parts(p.crop_cor[0], p.crop_cor[1], p.w, p.h, &sum, &wn, ctx->stream));
   return ssim_from_parts(sum, wn, &out[2]);
+}
+
+// ---------------------------------------------------------------------------
+// feature-path diagnostics
+// ---------------------------------------------------------------------------
+int stitch_b200_debug_detect(int width, int height, const uint8_t* rgb, const int region[4],
+                             double threshold, int max_kp, double* kp, float* desc) {
+  if (width <= 0 || height <= 0 || !rgb || !region)
+    return -fail(STITCH_B200_ConfigurationError, "bad frame arguments");
+  if (region[2] - region[0] < 32 || region[3] - region[1] < 32)
+    return -fail(STITCH_B200_RegionTooSmall, "detection region must be at least 32x32");
+  const size_t n = static_cast<size_t>(width) * height * 3;
+  void* d = nullptr;
+  if (cudaMalloc(&d, n) != cudaSuccess) return -fail(STITCH_B200_CudaError, "cudaMalloc");
+  std::unique_ptr<void, cudaError_t (*)(void*)> guard(d, cudaFree);
+  if (cudaMemcpy(d, rgb, n, cudaMemcpyHostToDevice) != cudaSuccess)
+    return -fail(STITCH_B200_CudaError, "cudaMemcpy");
+  FeatView fv;
+  std::vector<FeatPoint> kps;
+  std::vector<float> ds;
+  cudaError_t e = fv.build(static_cast<const std::uint8_t*>(d), width, height, nullptr);
+  if (e == cudaSuccess)
+    e = fv.detect_describe(region[0], region[1], region[2], region[3], threshold, kps, ds, nullptr);
+  if (e != cudaSuccess) return -fail(STITCH_B200_CudaError, cudaGetErrorString(e));
+  const int m = std::min<int>(max_kp, static_cast<int>(kps.size()));
+  for (int i = 0; i < m; ++i) {
+    kp[4 * i + 0] = kps[i].x;
+    kp[4 * i + 1] = kps[i].y;
+    kp[4 * i + 2] = kps[i].scale;
+    kp[4 * i + 3] = kps[i].response;
+    std::memcpy(desc + 64 * static_cast<size_t>(i), ds.data() + 64 * static_cast<size_t>(i),
+                64 * sizeof(float));
+  }
+  return static_cast<int>(kps.size());
+}
+
+int stitch_b200_debug_match(const float* da, int na, const float* db, int nb, double ratio,
+                            int* best_b, double* best_dist, int* best_a) {
+  std::vector<float> a(da, da + 64 * static_cast<size_t>(na)), b(db, db + 64 * static_cast<size_t>(nb));
+  std::vector<int> bb, ba;
+  std::vector<double> bd;
+  CUDA_TRY(feat_match(a, b, na, nb, ratio, bb, bd, ba, nullptr));
+  std::copy(bb.begin(), bb.end(), best_b);
+  std::copy(bd.begin(), bd.end(), best_dist);
+  std::copy(ba.begin(), ba.end(), best_a);
+  return STITCH_B200_OK;
 }

@@ -7,6 +7,8 @@
 #include <cmath>
 #include <cstdlib>
 #include <limits>
+#include <random>
+#include <tuple>
 
 namespace stitch_b200_host {
 
@@ -234,6 +236,108 @@ void lift_tables(const Canvas& c, double f, std::vector<double>& lsin, std::vect
     lcos[x] = std::cos(t);
   }
   for (int y = 0; y < c.height; ++y) lh[y] = (y + c.offy) / f;
+}
+
+// ---------------------------------------------------------------------------
+// feature refinement, host part
+// ---------------------------------------------------------------------------
+static int count_inliers(const std::vector<MatchPt>& m, const ScaleShift& p, double inlier_px,
+                         std::vector<int>* idx, double* sse) {
+  int count = 0;
+  if (sse) *sse = 0.0;
+  for (size_t i = 0; i < m.size(); ++i) {
+    const double ex = p.s_x * m[i].ax + p.t_x - m[i].bx;
+    const double ey = p.s_y * m[i].ay + p.t_y - m[i].by;
+    const double e2 = ex * ex + ey * ey;
+    if (e2 <= inlier_px * inlier_px) {
+      ++count;
+      if (idx) idx->push_back(static_cast<int>(i));
+      if (sse) *sse += e2;
+    }
+  }
+  return count;
+}
+
+// 1-D least squares b = s a + t over the inliers (features.cpp:260-278)
+static bool fit_axis(const std::vector<MatchPt>& m, const std::vector<int>& idx, bool x_axis,
+                     double& s, double& t) {
+  double sa = 0, sb = 0, saa = 0, sab = 0;
+  const double n = static_cast<double>(idx.size());
+  for (int i : idx) {
+    const double a = x_axis ? m[i].ax : m[i].ay;
+    const double b = x_axis ? m[i].bx : m[i].by;
+    sa += a;
+    sb += b;
+    saa += a * a;
+    sab += a * b;
+  }
+  const double det = n * saa - sa * sa;
+  if (std::abs(det) < 1e-9) return false;
+  s = (n * sab - sa * sb) / det;
+  t = (sb * saa - sa * sab) / det;
+  return true;
+}
+
+int ransac_scale_translation(std::vector<MatchPt> m, int iterations, double inlier_px,
+                             double min_scale, double max_scale, std::uint64_t seed,
+                             ScaleShift& out) {
+  if (m.size() < 2) return STITCH_B200_InsufficientMatches;
+  // canonical order: the fit depends on the set and the seed only
+  std::sort(m.begin(), m.end(), [](const MatchPt& a, const MatchPt& b) {
+    return std::tie(a.ax, a.ay, a.bx, a.by, a.distance) <
+           std::tie(b.ax, b.ay, b.bx, b.by, b.distance);
+  });
+  std::mt19937_64 rng(seed);
+  std::uniform_int_distribution<std::size_t> pick(0, m.size() - 1);
+  ScaleShift best;
+  int best_count = -1;
+  double best_sse = std::numeric_limits<double>::max();
+  for (int it = 0; it < iterations; ++it) {
+    const std::size_t i = pick(rng);
+    const std::size_t j = pick(rng);
+    if (i == j) continue;
+    const double dax = m[j].ax - m[i].ax;
+    const double day = m[j].ay - m[i].ay;
+    if (std::abs(dax) < 1e-9 || std::abs(day) < 1e-9) continue;
+    ScaleShift p;
+    p.s_x = (m[j].bx - m[i].bx) / dax;
+    p.s_y = (m[j].by - m[i].by) / day;
+    p.t_x = m[i].bx - p.s_x * m[i].ax;
+    p.t_y = m[i].by - p.s_y * m[i].ay;
+    if (p.s_x < min_scale || p.s_x > max_scale || p.s_y < min_scale || p.s_y > max_scale) continue;
+    double sse = 0.0;
+    const int count = count_inliers(m, p, inlier_px, nullptr, &sse);
+    if (count > best_count || (count == best_count && sse < best_sse)) {
+      best = p;
+      best_count = count;
+      best_sse = sse;
+    }
+  }
+  std::vector<int> inl;
+  if (best_count > 0) count_inliers(m, best, inlier_px, &inl, nullptr);
+  if (!(best_count >= 0 && (inl.size() * 2 >= m.size() || inl.size() >= 8)))
+    return STITCH_B200_NoConsensus;
+  ScaleShift refit = best;
+  double s, t;
+  if (fit_axis(m, inl, true, s, t)) {
+    refit.s_x = s;
+    refit.t_x = t;
+  }
+  if (fit_axis(m, inl, false, s, t)) {
+    refit.s_y = s;
+    refit.t_y = t;
+  }
+  out = refit;
+  return STITCH_B200_OK;
+}
+
+void broaden(const int r[4], double margin, const int b[4], int out[4]) {
+  const int mx = static_cast<int>(std::lround(margin * (r[2] - r[0])));
+  const int my = static_cast<int>(std::lround(margin * (r[3] - r[1])));
+  out[0] = std::max(b[0], r[0] - mx);
+  out[1] = std::max(b[1], r[1] - my);
+  out[2] = std::min(b[2], r[2] + mx);
+  out[3] = std::min(b[3], r[3] + my);
 }
 
 }  // namespace stitch_b200_host

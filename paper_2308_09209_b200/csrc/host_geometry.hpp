@@ -54,6 +54,22 @@ Canvas cylinder_canvas(const stitch_b200_config& cfg, double f);
 void lift_tables(const Canvas& c, double f, std::vector<double>& lsin, std::vector<double>& lcos,
                  std::vector<double>& lh);
 
+// ---- feature refinement, host part (features.cpp:236-354, geometry.cpp) ----
+struct MatchPt {
+  double ax, ay, bx, by, distance;
+};
+struct ScaleShift {
+  double s_x = 1.0, s_y = 1.0, t_x = 0.0, t_y = 0.0;
+};
+// ransac_scale_translation over (ax, ay) -> (bx, by): STITCH_B200_OK,
+// InsufficientMatches or NoConsensus; the reference's std::mt19937_64 and
+// std::uniform_int_distribution<std::size_t> stream.
+int ransac_scale_translation(std::vector<MatchPt> m, int iterations, double inlier_px,
+                             double min_scale, double max_scale, std::uint64_t seed,
+                             ScaleShift& out);
+// broaden (geometry.cpp:119-133)
+void broaden(const int r[4], double margin, const int b[4], int out[4]);
+
 // (overlap bounds, view footprints and blend weights are computed on the
 // device: geometry_kernels.cu)
 

@@ -218,6 +218,34 @@ void launch_warp_view(const Geometry* g, int view, const uchar4* frame, std::uin
 void launch_expand_one(const std::uint8_t* rgb, uchar4* rgba, long long n_px, cudaStream_t s);
 void launch_warp_mask(const Geometry* g, int view, std::uint8_t* mask, cudaStream_t s);
 
+// ---- feature refinement image work (features_kernels.cu) ----
+struct FeatPoint {
+  double x, y, scale, response;  // Keypoint (features.hpp)
+};
+// One warped view: the integral image of its quantized gray, then
+// detect + describe over a search region (keypoints in the reference's
+// order, 64 floats per descriptor).
+class FeatView {
+ public:
+  FeatView();
+  ~FeatView();
+  FeatView(const FeatView&) = delete;
+  FeatView& operator=(const FeatView&) = delete;
+  cudaError_t build(const std::uint8_t* d_rgb, int w, int h, cudaStream_t s);
+  cudaError_t detect_describe(int rx0, int ry0, int rx1, int ry1, double threshold,
+                              std::vector<FeatPoint>& kps, std::vector<float>& desc,
+                              cudaStream_t s) const;
+
+ private:
+  struct Impl;
+  Impl* impl;
+};
+// match (features.cpp:181-234) on the device: per a the ratio-tested
+// nearest b (-1 when rejected) and its distance, per b the nearest a.
+cudaError_t feat_match(const std::vector<float>& da, const std::vector<float>& db, int na, int nb,
+                       double ratio, std::vector<int>& best_b, std::vector<double>& best_dist,
+                       std::vector<int>& best_a, cudaStream_t s);
+
 // ---- quality metrics (metrics_kernels.cu) ----
 cudaError_t gpu_psnr_parts(const uchar4* a, const uchar4* b, int n, unsigned long long* sse,
                            unsigned long long* count, cudaStream_t s);

@@ -123,8 +123,10 @@ class FlowOptions:  # flow.hpp:29-34
 
 @dataclass
 class RefineOptions:  # pipeline.hpp:23-31
-    # Feature refinement is init-only and outside the B200 path; the mirror
-    # defaults it off (the reference defaults it on).
+    # Feature refinement runs at initialize() (detect / describe / match on
+    # the device, RANSAC on the host); the mirror defaults it off (the
+    # reference defaults it on) so that contexts built from a config alone
+    # need no first frames.
     enabled: bool = False
     margin: float = 0.15
     ransac_iters: int = 500
@@ -183,6 +185,12 @@ def _config_to_c(cfg: StitchConfig, sizes: Sequence[tuple]) -> _abi.Config:
     c.projection = 1 if cfg.projection == "cylindrical" else 0
     c.cyl_focal = cfg.cyl_focal
     c.refine_enabled = 1 if cfg.refine.enabled else 0
+    c.refine_margin = cfg.refine.margin
+    c.ransac_iters = cfg.refine.ransac_iters
+    c.inlier_px = cfg.refine.inlier_px
+    c.detect_threshold = cfg.refine.detect_threshold
+    c.match_ratio = cfg.refine.match_ratio
+    c.seed = int(cfg.seed) & 0xFFFFFFFFFFFFFFFF
     return c
 
 
@@ -252,6 +260,7 @@ class PairState:
     partner: int
     bounds: tuple  # (x0, y0, x1, y1)
     theta_i: np.ndarray
+    refine_warning: bool = False  # refinement fell back to the unrefined map
 
 
 class PipelineState:
@@ -347,8 +356,15 @@ def initialize(config: StitchConfig, first_frames: Sequence[Frame]) -> PipelineS
     sizes = [(f.width, f.height) for f in first_frames]
     c = _config_to_c(config, sizes)
     h = C.c_void_p()
-    check(_lib().stitch_b200_initialize(C.byref(c), config.device, C.byref(h)))
-    return PipelineState(h, config)
+    if config.refine.enabled:
+        arrs, ptrs = _frame_ptrs(first_frames, len(config.views))
+        check(_lib().stitch_b200_initialize_frames(C.byref(c), ptrs, config.device, C.byref(h)))
+    else:
+        check(_lib().stitch_b200_initialize(C.byref(c), config.device, C.byref(h)))
+    state = PipelineState(h, config)
+    for k, p in enumerate(state.pairs):
+        p.refine_warning = bool(_lib().stitch_b200_refine_warning(h, k))
+    return state
 
 
 def camera_maps(config: StitchConfig, sizes: Sequence[tuple]) -> np.ndarray:

@@ -22,7 +22,8 @@ def scene(views=2, width=160, height=120, frames=4, seed=1, overlap=0.3, casts=N
 
 def oracle_config(sc: pb.SynthScene, *, threads=4, keep_debug=1, window=3, weighting=0,
                   topology=0, levels=4, iterations=50, smoothness=15.0, lam=0.05,
-                  gamma_dark=1.5, gamma_bright=1.5, target_black=0, target_white=255):
+                  gamma_dark=1.5, gamma_bright=1.5, target_black=0, target_white=255,
+                  refine=False, seed=0):
     import oracle as O
 
     c = sc.config_c()
@@ -35,13 +36,15 @@ def oracle_config(sc: pb.SynthScene, *, threads=4, keep_debug=1, window=3, weigh
                          smoothness=smoothness, window=window, weighting=weighting,
                          topology=topology if topology else c.topology, threads=threads,
                          keep_debug=keep_debug, projection=c.projection,
-                         cyl_focal=c.cyl_focal)
+                         cyl_focal=c.cyl_focal, refine=refine, seed=seed)
 
 
 def product_config(sc: pb.SynthScene, *, window=3, weighting=0, topology=0, levels=4,
                    iterations=50, smoothness=15.0, lam=0.05, gamma_dark=1.5, gamma_bright=1.5,
-                   target_black=0, target_white=255) -> pb.StitchConfig:
+                   target_black=0, target_white=255, refine=False, seed=0) -> pb.StitchConfig:
     cfg = sc.config()
+    cfg.refine.enabled = refine
+    cfg.seed = seed
     cfg.window_capacity = window
     cfg.fuse_weighting = "cross" if weighting else "own"
     if topology:

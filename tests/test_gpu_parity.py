@@ -197,6 +197,7 @@ def test_errors_fail_loudly():
     sc = scene(views=2, width=120, height=90)
     cfg = product_config(sc)
     cfg.refine.enabled = True
+    cfg.projection = "cylindrical"  # refinement serves the planar canvas only
     with pytest.raises(pb.StitchError):
         pb.initialize(cfg, frames_at(sc, 0))
     cfg = product_config(sc, lam=0.7)
