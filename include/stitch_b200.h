@@ -176,6 +176,13 @@ int stitch_b200_initialize_frames(const stitch_b200_config* cfg,
                                   const uint8_t* const* frames, int device,
                                   stitch_b200_ctx** out);
 
+/* run_sequence's re-refinement branch (pipeline.cpp:395-406): a fresh
+ * initialize(config, current frames) (with refinement when enabled) replaces
+ * the context's geometry; the 3D-M windows, threshold history and frame
+ * counter are carried over.  The pair set must not change. */
+int stitch_b200_rerefine(stitch_b200_ctx* ctx, const stitch_b200_config* cfg,
+                         const uint8_t* const* frames);
+
 /* 1 when pair k's refinement fell back to the unrefined map
  * (PairState::refine_warning: too few keypoints / matches, no consensus). */
 int stitch_b200_refine_warning(const stitch_b200_ctx* ctx, int k);

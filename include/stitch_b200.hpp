@@ -338,7 +338,7 @@ struct RunResult {
 };
 
 // run_sequence (pipeline.hpp:90-92, pipeline.cpp:362-420); periodic
-// re-refinement is not part of the B200 path.
+// re-refinement (refine.rerefine_every) runs through stitch_b200_rerefine.
 inline RunResult run_sequence(const StitchConfig& config, const std::vector<std::vector<Frame>>& views,
                               const std::function<void(long, const Frame&)>& sink = {}) {
   if (views.size() != config.views.size())
@@ -356,9 +356,18 @@ inline RunResult run_sequence(const StitchConfig& config, const std::vector<std:
   result.report.scene_id = config.scene_id;
   result.report.threads = config.threads;
   result.report.frames = static_cast<long>(frames);
+  const int every = config.refine.rerefine_every;
   for (std::size_t t = 0; t < frames; ++t) {
     std::vector<Frame> set;
     for (const auto& s : views) set.push_back(s[t]);
+    if (every > 0 && t > 0 && t % static_cast<std::size_t>(every) == 0) {
+      // re-refinement (pipeline.cpp:395-406): fresh initialize() on the
+      // current frames, windows / history / counter carried over
+      stitch_b200_config c = to_c(config, set);
+      std::vector<const std::uint8_t*> ptrs;
+      for (const Frame& f : set) ptrs.push_back(f.data.data());
+      check(stitch_b200_rerefine(state.handle(), &c, ptrs.data()));
+    }
     ProcessResult pr = process_frame(state, set);
     result.report.totals += pr.report.times;
     result.report.per_frame.push_back(pr.report);

@@ -85,6 +85,7 @@ SYMBOLS = [
     ("stitch_b200_initialize_frames", C.c_int, [C.POINTER(Config), C.c_void_p, C.c_int,
                                                 C.POINTER(C.c_void_p)]),
     ("stitch_b200_refine_warning", C.c_int, [C.c_void_p, C.c_int]),
+    ("stitch_b200_rerefine", C.c_int, [C.c_void_p, C.POINTER(Config), C.c_void_p]),
     ("stitch_b200_debug_detect", C.c_int, [C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_int),
                                            C.c_double, C.c_int, C.c_void_p, C.c_void_p]),
     ("stitch_b200_debug_match", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_double,

@@ -1085,6 +1085,21 @@ int stitch_b200_initialize_frames(const stitch_b200_config* cfg, const uint8_t* 
   return initialize_impl(cfg, frames, device, out);
 }
 
+static int carry_into(stitch_b200_ctx* h, std::unique_ptr<Ctx>& fresh);
+
+int stitch_b200_rerefine(stitch_b200_ctx* h, const stitch_b200_config* cfg,
+                         const uint8_t* const* frames) {
+  if (!frames) return fail(STITCH_B200_ConfigurationError, "frames must not be NULL");
+  stitch_b200_ctx* fresh = nullptr;
+  int rc = initialize_impl(cfg, frames, h->c->device, &fresh);
+  if (rc) return rc;
+  std::unique_ptr<stitch_b200_ctx> guard(fresh);
+  if (fresh->c->hg.n_pairs != h->c->hg.n_pairs)
+    return fail(STITCH_B200_ConfigurationError, "re-refinement must keep the pair set");
+  std::unique_ptr<Ctx> f = std::move(fresh->c);
+  return carry_into(h, f);
+}
+
 int stitch_b200_refine_warning(const stitch_b200_ctx* h, int k) {
   const Ctx* ctx = h->c.get();
   if (k < 0 || k >= ctx->hg.n_pairs) return 0;

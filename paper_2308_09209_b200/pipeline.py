@@ -296,6 +296,16 @@ class PipelineState:
         check(_lib().stitch_b200_pair_quality(self._h, k, out))
         return tuple(out)
 
+    def rerefine(self, config: StitchConfig, frames: Sequence[Frame]) -> None:
+        """run_sequence's re-refinement (pipeline.cpp:395-406): a fresh
+        initialize() on `frames` with the temporal state carried over."""
+        c = _config_to_c(config, [(f.width, f.height) for f in frames])
+        arrs, ptrs = _frame_ptrs(frames, len(config.views))
+        check(_lib().stitch_b200_rerefine(self._h, C.byref(c), ptrs))
+        self._refresh()
+        for k, p in enumerate(self.pairs):
+            p.refine_warning = bool(_lib().stitch_b200_refine_warning(self._h, k))
+
     def update_maps(self, maps: np.ndarray) -> None:
         """Re-refinement from new view->reference homographies (n, 3, 3):
         canvas, inverse maps and pair geometry rebuilt (the pair geometry on
@@ -481,7 +491,8 @@ class RunResult:
 
 def run_sequence(config: StitchConfig, views: Sequence[Sequence[Frame]],
                  sink: Optional[Callable[[int, Frame], None]] = None) -> RunResult:
-    """pipeline.hpp:90-92 / pipeline.cpp:362-420 (re-refinement unsupported)."""
+    """pipeline.hpp:90-92 / pipeline.cpp:362-420, including the re-refinement
+    branch (refine.rerefine_every > 0)."""
     if len(views) != len(config.views):
         raise StitchError(ErrorCode.ConfigurationError + 1,
                           "stream count does not match configured views")
@@ -495,7 +506,10 @@ def run_sequence(config: StitchConfig, views: Sequence[Sequence[Frame]],
     result = RunResult([], RunReport(scene_id=config.scene_id, threads=config.threads,
                                      frames=frames))
     try:
+        every = config.refine.rerefine_every
         for t in range(frames):
+            if every > 0 and t > 0 and t % every == 0:
+                state.rerefine(config, [s[t] for s in views])
             pr = process_frame(state, [s[t] for s in views])
             for i in range(4):
                 result.report.totals[i] += pr.report.times[i]

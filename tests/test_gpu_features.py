@@ -108,3 +108,29 @@ def test_refine_needs_frames():
     h = C.c_void_p()
     rc = _lib().stitch_b200_initialize(C.byref(c), 0, C.byref(h))
     assert rc == pb.ErrorCode.ConfigurationError + 1
+
+
+def test_run_sequence_rerefines():
+    """refine.rerefine_every: the state is re-initialized from the current
+    frames (pipeline.cpp:395-406) while the frame counter carries on; the
+    re-refined geometry equals a fresh refined initialize() on those frames."""
+    sc = scene(views=2, width=320, height=240, frames=4, focal_scale=1.03)
+    cfg = product_config(sc, refine=True, seed=3)
+    cfg.refine.rerefine_every = 2
+    views = [[sc.render_view(v, t) for t in range(4)] for v in range(2)]
+    res = pb.run_sequence(cfg, views)
+    assert [r.frame_index for r in res.report.per_frame] == [0, 1, 2, 3]
+    state = pb.initialize(cfg, [s[0] for s in views])
+    for t in range(2):
+        pb.process_frame(state, [s[t] for s in views])
+    state.rerefine(cfg, [s[2] for s in views])
+    fresh = pb.initialize(cfg, [s[2] for s in views])
+    for v in range(2):
+        np.testing.assert_array_equal(state.inv_map(v), fresh.inv_map(v))
+    for a, b in zip(state.pairs, fresh.pairs):
+        assert a.bounds == b.bounds and a.refine_warning == b.refine_warning
+    r = pb.process_frame(state, [s[2] for s in views])
+    assert r.report.frame_index == 2
+    np.testing.assert_array_equal(r.panorama.data, res.panoramas[2].data)
+    state.close()
+    fresh.close()
