@@ -307,10 +307,12 @@ __device__ __forceinline__ uchar4 canvas_pixel(const CanvasParams& P,
   return pv;
 }
 
+constexpr int kCanvasCtasPerSm = 4;  // resident CTAs per SM (register budget; 5 spills)
+
 // Every canvas pixel once (64 x 4 tiles, grid-stride), per-CTA histogram
 // flushed to the frame histogram; the last CTA builds the balance LUT.
 template <bool CYL>
-__global__ void __launch_bounds__(256, 4) k_canvas(const __grid_constant__ CanvasParams P,
+__global__ void __launch_bounds__(256, kCanvasCtasPerSm) k_canvas(const __grid_constant__ CanvasParams P,
                                                    const Geometry* __restrict__ g,
                                                    DevState* __restrict__ st,
                                                    uchar4* __restrict__ pano) {
@@ -489,7 +491,7 @@ void launch_crop_warp(const CanvasParams& P, int max_w, int max_h, cudaStream_t 
 void launch_canvas(const CanvasParams& P, const Geometry* g, DevState* st, uchar4* pano,
                    int num_sms, cudaStream_t s) {
   const long long tiles = static_cast<long long>((P.cw + 63) / 64) * ((P.ch + 3) / 4);
-  const long long b = std::min<long long>(static_cast<long long>(num_sms) * 4, tiles);
+  const long long b = std::min<long long>(static_cast<long long>(num_sms) * kCanvasCtasPerSm, tiles);
   const int blocks = static_cast<int>(b < 1 ? 1 : b);
   if (P.projection == 1)
     k_canvas<true><<<blocks, 256, 0, s>>>(P, g, st, pano);
