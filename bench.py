@@ -265,14 +265,18 @@ def run_b200(args, rank, world, local_rank):
             torch.distributed.barrier()
 
     def step_all(i):
+        # pipelined device-resident frames (two slots per context, ordered
+        # only where the temporal state requires it); joined below
         for j, h in enumerate(hs_):
-            pb.pipeline.check(lib.stitch_b200_process_device(h, dev_sets[(i + j) % F], None))
+            pb.pipeline.check(lib.stitch_b200_process_device_async(h, dev_sets[(i + j) % F]))
 
     clocks = ClockSampler(local_rank)
     clocks.start()
     # ---- warm-up ----
     for i in range(args.warmup):
         step_all(i)
+    for h in hs_:
+        pb.pipeline.check(lib.stitch_b200_synchronize(h))
     torch.cuda.synchronize()
     # ---- timed: device-resident inputs; all streams of this rank ----
     barrier()
@@ -283,8 +287,12 @@ def run_b200(args, rank, world, local_rank):
     e0.record(main)
     for cs in cstreams:
         cs.wait_event(e0)
+    for h in hs_:
+        pb.pipeline.check(lib.stitch_b200_fork(h))
     for i in range(args.steps):
         step_all(i)
+    for h in hs_:
+        pb.pipeline.check(lib.stitch_b200_join(h))
     for cs in cstreams:
         ev = torch.cuda.Event()
         ev.record(cs)

@@ -272,11 +272,26 @@ int stitch_b200_wait(stitch_b200_ctx* ctx, long long ticket,
                      stitch_b200_report* report);
 
 /* Device-resident variant: frames[v] are device pointers; outputs stay in
- * the context (see stitch_b200_device_pano).  Enqueued on the context's
- * stream; returns without synchronising unless report != NULL. */
+ * the context (see stitch_b200_device_pano).  Ordered on the context's API
+ * stream (stitch_b200_stream): inputs written there before the call are
+ * seen, work enqueued there after it sees the outputs.  Returns without
+ * synchronising unless report != NULL. */
 int stitch_b200_process_device(stitch_b200_ctx* ctx,
                                const uint8_t* const* dev_frames,
                                stitch_b200_report* report);
+
+/* Pipelined device-resident frames.  A context runs two pipeline slots on
+ * their own streams; consecutive frames overlap except at the points where
+ * the reference's temporal state orders them (the 3D-M window update, the
+ * threshold history), which the slots chain in frame order.
+ * process_device_async enqueues a frame without ordering against the API
+ * stream; stitch_b200_fork makes subsequently enqueued frames wait for the
+ * API stream's work so far, stitch_b200_join makes the API stream wait for
+ * every frame enqueued so far.  The outputs of frame t stay valid until
+ * frame t + 2 is enqueued. */
+int stitch_b200_process_device_async(stitch_b200_ctx* ctx, const uint8_t* const* dev_frames);
+int stitch_b200_fork(stitch_b200_ctx* ctx);
+int stitch_b200_join(stitch_b200_ctx* ctx);
 
 /* Device pointers of the context's last panorama (rgb w*h*3, mask w*h). */
 int stitch_b200_device_pano(const stitch_b200_ctx* ctx, uint8_t** rgb,

@@ -86,6 +86,9 @@ SYMBOLS = [
                                                 C.POINTER(C.c_void_p)]),
     ("stitch_b200_refine_warning", C.c_int, [C.c_void_p, C.c_int]),
     ("stitch_b200_rerefine", C.c_int, [C.c_void_p, C.POINTER(Config), C.c_void_p]),
+    ("stitch_b200_process_device_async", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("stitch_b200_fork", C.c_int, [C.c_void_p]),
+    ("stitch_b200_join", C.c_int, [C.c_void_p]),
     ("stitch_b200_debug_detect", C.c_int, [C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_int),
                                            C.c_double, C.c_int, C.c_void_p, C.c_void_p]),
     ("stitch_b200_debug_match", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_double,

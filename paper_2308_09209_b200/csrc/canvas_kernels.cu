@@ -175,9 +175,9 @@ __device__ void balance_lut(const Geometry* __restrict__ g, DevState* __restrict
   __syncthreads();
   if (v == 0) {
     ok = 0;
-    st->report.frame_index = st->frame_counter;
+    st->report.frame_index = *st->frame_counter;
     if (tot != 0) {
-      BalanceState& bs = st->balance;
+      BalanceState& bs = *st->balance;
       if (bs.n == 3) {
         for (int i = 0; i < 2; ++i)
           for (int c = 0; c < 3; ++c) {
@@ -219,7 +219,7 @@ __device__ void balance_lut(const Geometry* __restrict__ g, DevState* __restrict
       st->report.m1[c] = ok ? sm1[c] : 0;
       st->report.m2[c] = ok ? sm2[c] : 0;
     }
-    st->frame_counter++;
+    ++*st->frame_counter;
   }
   __syncthreads();
   for (int c = 0; c < 3; ++c) {

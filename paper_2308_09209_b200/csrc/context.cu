@@ -48,22 +48,43 @@ struct Op {
 
 }  // namespace
 
+// One pipeline slot: the buffers a frame writes (RGBA views, crops,
+// pyramids, flows, panorama), its device geometry / frame state / task
+// tables, its compute stream and its graphs.  Two slots let consecutive
+// frames overlap; the temporal state is shared and updated in frame order.
+struct SlotRes {
+  Geometry hg{};           // host mirror (this slot's buffer pointers)
+  Geometry* dg = nullptr;  // device geometry
+  DevState* dst = nullptr;
+  uchar4* d_pano = nullptr;
+  CanvasParams cparams{};
+  HsTask* d_hs = nullptr;
+  PrepTask* d_hp = nullptr;
+  PyrTask* d_pyr = nullptr;
+  cudaStream_t cs = nullptr;
+  // the frame as 4 graphs: front (expand, crops), colour (3D-M solves, in
+  // frame order across slots), mid (flow), back (canvas + balance, in frame
+  // order across slots; tone)
+  static constexpr int kSegs = 4;
+  cudaGraph_t graph[kSegs] = {};
+  cudaGraphExec_t exec[kSegs] = {};
+};
+
 struct Ctx {
   int device = 0;
   int num_sms = 148;
-  cudaStream_t stream = nullptr;
-  Geometry hg{};           // host mirror of the device geometry
-  Geometry* dg = nullptr;  // device geometry
-  DevState* dst = nullptr;
+  cudaStream_t stream = nullptr;  // the API stream (process_device, profile, debug)
+  static constexpr int kSlots = 2;
+  SlotRes slot[kSlots];
+  Geometry hg{};  // metadata (slot 0's mirror; buffers: use slot[s].hg)
+  TemporalState* dtemp = nullptr;
   stitch_b200_init init{};  // copy (theta pointers re-pointed at host copies)
   std::vector<std::vector<float>> theta_host;
   std::vector<int> refine_warning;  // per pair (initialize_frames with refinement)
   std::vector<void*> allocs;
   std::uint8_t* d_frames[kMaxViews] = {};
   size_t frame_bytes[kMaxViews] = {};
-  uchar4* d_pano = nullptr;
-  // two pipeline slots: inputs, outputs, graph, stage events, report
-  static constexpr int kSlots = 2;
+  // per slot: inputs, outputs, stage events, report
   std::uint8_t* d_in[kSlots][kMaxViews] = {};
   std::uint8_t* d_out_rgb[kSlots] = {};
   std::uint8_t* d_out_mask[kSlots] = {};
@@ -75,19 +96,19 @@ struct Ctx {
   float alpha2 = 225.0f;
   int n_levels_max = 0;
   std::vector<Op> plan;
-  HsTask* d_hs = nullptr;
-  PrepTask* d_hp = nullptr;
-  PyrTask* d_pyr = nullptr;
+  int seg_begin[SlotRes::kSegs + 1] = {};  // plan index ranges of the segments
   int* d_lists = nullptr;
-  cudaGraph_t graph[kSlots] = {};
-  cudaGraphExec_t exec[kSlots] = {};
   int launches = 0;
   cudaEvent_t ev[kSlots][6] = {};
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t h2d_done[kSlots] = {}, comp_done[kSlots] = {}, d2h_done[kSlots] = {};
+  // frame-order points between slots: colour solves done, canvas done
+  cudaEvent_t color_done[kSlots] = {}, canvas_done[kSlots] = {};
+  cudaEvent_t fork_ev = nullptr;
   long long seq = 0;                       // frames submitted (any API)
   long long slot_ticket[kSlots] = {-1, -1};  // ticket occupying each slot
   bool slot_pending[kSlots] = {false, false};
+  bool slot_joined[kSlots] = {true, true};  // the API stream waited for the slot's frame
   std::vector<std::pair<long long, stitch_b200_report>> done_reports;
   int last_slot = 0;
   // pinned ring for device-frame pointer tables
@@ -97,20 +118,25 @@ struct Ctx {
   DevReport* h_report = nullptr;  // one per slot (pinned)
   std::vector<int> pair_levels;
   float2* d_zero = nullptr;
-  CanvasParams cparams{};
 
   ~Ctx() {
     if (stream) cudaStreamSynchronize(stream);
+    for (auto& S : slot)
+      if (S.cs) cudaStreamSynchronize(S.cs);
     if (h2d) cudaStreamSynchronize(h2d);
     if (d2h) cudaStreamSynchronize(d2h);
     for (int s = 0; s < kSlots; ++s) {
-      if (exec[s]) cudaGraphExecDestroy(exec[s]);
-      if (graph[s]) cudaGraphDestroy(graph[s]);
+      for (int g = 0; g < SlotRes::kSegs; ++g) {
+        if (slot[s].exec[g]) cudaGraphExecDestroy(slot[s].exec[g]);
+        if (slot[s].graph[g]) cudaGraphDestroy(slot[s].graph[g]);
+      }
       for (auto& e : ev[s])
         if (e) cudaEventDestroy(e);
-      for (cudaEvent_t e : {h2d_done[s], comp_done[s], d2h_done[s]})
+      for (cudaEvent_t e : {h2d_done[s], comp_done[s], d2h_done[s], color_done[s], canvas_done[s]})
         if (e) cudaEventDestroy(e);
+      if (slot[s].cs) cudaStreamDestroy(slot[s].cs);
     }
+    if (fork_ev) cudaEventDestroy(fork_ev);
     if (h2d) cudaStreamDestroy(h2d);
     if (d2h) cudaStreamDestroy(d2h);
     for (auto& e : ring_ev)
@@ -225,36 +251,37 @@ void fill_views(Geometry& g, const stitch_b200_init* in) {
 
 int enqueue_op(Ctx* ctx, const Op& op, cudaStream_t s, int slot = 0) {
   const Geometry& g = ctx->hg;
+  const SlotRes& S = ctx->slot[slot];
   switch (op.kind) {
     case OP_EXPAND:
-      launch_expand(ctx->dg, g.n_views, ctx->max_view_px, s);
+      launch_expand(S.dg, g.n_views, ctx->max_view_px, s);
       return 1;
     case OP_CROP:
       if (!g.n_pairs) return 0;
-      launch_crop_warp(ctx->cparams, ctx->max_crop_w, ctx->max_crop_h, s);
+      launch_crop_warp(S.cparams, ctx->max_crop_w, ctx->max_crop_h, s);
       return 1;
     case OP_STATS:
-      launch_pair_color(ctx->dg, ctx->dst, ctx->d_lists + op.offset, op.count, ctx->max_crop_px, s);
+      launch_pair_color(S.dg, S.dst, ctx->d_lists + op.offset, op.count, ctx->max_crop_px, s);
       return 1;
     case OP_PREP:
       if (!g.n_pairs) return 0;
-      launch_flow_prepare(ctx->dg, ctx->dst, g.n_pairs, ctx->max_crop_px, s);
+      launch_flow_prepare(S.dg, S.dst, g.n_pairs, ctx->max_crop_px, s);
       return 1;
     case OP_PYR:
-      launch_pyr_down(ctx->d_pyr + op.offset, op.count, op.max_px, s);
+      launch_pyr_down(S.d_pyr + op.offset, op.count, op.max_px, s);
       return 1;
     case OP_HSPREP:
-      launch_hs_prepare(ctx->d_hp + op.offset, op.count, op.max_w, op.max_h, ctx->alpha2, s);
+      launch_hs_prepare(S.d_hp + op.offset, op.count, op.max_w, op.max_h, ctx->alpha2, s);
       return 1;
     case OP_HS:
-      launch_hs_iter(ctx->d_hs + op.offset, op.count, op.max_w, op.max_h, op.sweeps, op.fuse,
+      launch_hs_iter(S.d_hs + op.offset, op.count, op.max_w, op.max_h, op.sweeps, op.fuse,
                      ctx->alpha2, s);
       return 1;
     case OP_CANVAS:
-      launch_canvas(ctx->cparams, ctx->dg, ctx->dst, ctx->d_pano, ctx->num_sms, s);
+      launch_canvas(S.cparams, S.dg, S.dst, S.d_pano, ctx->num_sms, s);
       return 1;
     case OP_TONE:
-      launch_tone(ctx->dst, ctx->d_pano, ctx->n_px, ctx->d_out_rgb[slot], ctx->d_out_mask[slot], s);
+      launch_tone(S.dst, S.d_pano, ctx->n_px, ctx->d_out_rgb[slot], ctx->d_out_mask[slot], s);
       return 1;
     default:
       return 0;
@@ -319,325 +346,351 @@ int build_context(const stitch_b200_init* in, int device,
     g.views[v].gap[1] = f.gap[1];
   }
 
-  // buffers
-  for (int v = 0; v < in->n_views; ++v) {
-    ctx->frame_bytes[v] = static_cast<size_t>(in->view_width[v]) * in->view_height[v] * 3;
-    CUDA_TRY(ctx->alloc(&ctx->d_frames[v], ctx->frame_bytes[v]));
-    g.frames[v] = ctx->d_frames[v];
-    ctx->d_in[0][v] = ctx->d_frames[v];
-    for (int sl = 1; sl < Ctx::kSlots; ++sl) CUDA_TRY(ctx->alloc(&ctx->d_in[sl][v], ctx->frame_bytes[v]));
-    const long long vpx = static_cast<long long>(in->view_width[v]) * in->view_height[v];
-    CUDA_TRY(ctx->alloc(&g.rgba[v], vpx));
-    ctx->max_view_px = std::max(ctx->max_view_px, vpx);
-  }
-  ctx->n_px = static_cast<long long>(g.canvas_w) * g.canvas_h;
-  CUDA_TRY(ctx->alloc(&ctx->d_pano, static_cast<size_t>(ctx->n_px) + 4));
-  for (int sl = 0; sl < Ctx::kSlots; ++sl) {
-    CUDA_TRY(ctx->alloc(&ctx->d_out_rgb[sl], static_cast<size_t>(ctx->n_px) * 3 + 16));
-    CUDA_TRY(ctx->alloc(&ctx->d_out_mask[sl], static_cast<size_t>(ctx->n_px) + 16));
-  }
-
-  ctx->sweeps = std::max(1, in->flow_iterations / 5);  // flow.cpp:79-80
-  ctx->alpha2 = static_cast<float>(in->smoothness * in->smoothness);
-  ctx->theta_host.resize(in->n_pairs);
-  int max_zero = 16;
-  for (int k = 0; k < in->n_pairs; ++k) {
-    const stitch_b200_pair& sp = in->pairs[k];
-    PairDesc& p = g.pairs[k];
-    p.view = sp.view;
-    p.partner = sp.partner;
-    p.x0 = sp.x0;
-    p.y0 = sp.y0;
-    p.w = sp.x1 - sp.x0;
-    p.h = sp.y1 - sp.y0;
-    const int n = p.w * p.h;
-    ctx->max_crop_px = std::max(ctx->max_crop_px, n);
-    ctx->max_crop_w = std::max(ctx->max_crop_w, p.w);
-    ctx->max_crop_h = std::max(ctx->max_crop_h, p.h);
-    max_zero = std::max(max_zero, n);
-    ctx->theta_host[k].assign(sp.theta_i, sp.theta_i + n);
-    ctx->init.pairs[k].theta_i = ctx->theta_host[k].data();
-    float* th;
-    CUDA_TRY(ctx->alloc(&th, n));
-    CUDA_TRY(cudaMemcpy(th, sp.theta_i, sizeof(float) * n, cudaMemcpyHostToDevice));
-    p.theta_i = th;
-    for (int s = 0; s < 2; ++s) {
-      CUDA_TRY(ctx->alloc(&p.crop_raw[s], n));
-      CUDA_TRY(ctx->alloc(&p.crop_cor[s], n));
-    }
-    // dense_flow requires >= 16x16 (flow.cpp:146-148), else zero flow
-    p.flow_ok = (p.w >= 16 && p.h >= 16) ? 1 : 0;
-  }
-  CUDA_TRY(ctx->alloc(&ctx->d_zero, max_zero));
-
-  // pair depth (distance from the reference through partners)
-  std::vector<int> depth(in->n_pairs, 1);
-  int max_depth = 0;
-  for (int k = 0; k < in->n_pairs; ++k) {
-    const int partner = in->pairs[k].partner;
-    if (partner != in->reference)
-      for (int j = 0; j < k; ++j)
-        if (in->pairs[j].view == partner) depth[k] = depth[j] + 1;
-    g.pair_depth[k] = depth[k];
-    max_depth = std::max(max_depth, depth[k]);
-  }
-
-  // ---- flow plan: pyramids (flow.cpp:152-156), per-level tasks ----
-  struct TaskState {
-    int k, dir, L;
-    int dims[kMaxLevels][2];
-    float2* UV[2];  // (u, v) ping-pong
-    float4* KQ;  // (gx, gy, c, denom) per pixel of the current warp iteration
-    int cur;
-  };
-  std::vector<TaskState> tasks;
-  ctx->pair_levels.assign(in->n_pairs, 0);
-  int Lmax = 0;
-  for (int k = 0; k < in->n_pairs; ++k) {
-    PairDesc& p = g.pairs[k];
-    if (!p.flow_ok) {
-      for (int d = 0; d < 2; ++d) {
-        p.flow_uv[d] = ctx->d_zero;
-      }
-      continue;
-    }
-    int dims[kMaxLevels][2];
-    int L = 1;
-    dims[0][0] = p.w;
-    dims[0][1] = p.h;
-    for (int l = 1; l < in->flow_levels && l < kMaxLevels; ++l) {
-      if (dims[l - 1][0] < 16 || dims[l - 1][1] < 16) break;
-      dims[l][0] = std::max(1, dims[l - 1][0] / 2);
-      dims[l][1] = std::max(1, dims[l - 1][1] / 2);
-      ++L;
-    }
-    ctx->pair_levels[k] = L;
-    Lmax = std::max(Lmax, L);
-    for (int s = 0; s < 2; ++s)
-      for (int l = 0; l < L; ++l) CUDA_TRY(ctx->alloc(&p.pyr[s][l], dims[l][0] * dims[l][1]));
-    for (int d = 0; d < 2; ++d) {
-      TaskState t{};
-      t.k = k;
-      t.dir = d;
-      t.L = L;
-      std::memcpy(t.dims, dims, sizeof(dims));
-      for (int b = 0; b < 2; ++b) {
-        CUDA_TRY(ctx->alloc(&t.UV[b], p.w * p.h));
-      }
-      CUDA_TRY(ctx->alloc(&t.KQ, p.w * p.h));
-      t.cur = 0;
-      tasks.push_back(t);
-    }
-  }
-  ctx->n_levels_max = Lmax;
-
-  std::vector<HsTask> hs_table;
-  std::vector<PrepTask> hp_table;
-  std::vector<PyrTask> pyr_table;
-  std::vector<int> lists;
-  std::vector<Op>& plan = ctx->plan;
-  plan.push_back({OP_EVENT, 0, 0, 0, 0, 0, 0});
-  plan.push_back({OP_EXPAND});
-  plan.push_back({OP_CROP});
-  plan.push_back({OP_EVENT, 0, 0, 0, 0, 0, 1});
-  for (int d = 1; d <= max_depth; ++d) {
-    Op op{OP_STATS};
-    op.offset = static_cast<int>(lists.size());
-    for (int k = 0; k < in->n_pairs; ++k)
-      if (depth[k] == d) lists.push_back(k);
-    op.count = static_cast<int>(lists.size()) - op.offset;
-    plan.push_back(op);
-  }
-  plan.push_back({OP_PREP});
-  plan.push_back({OP_EVENT, 0, 0, 0, 0, 0, 2});
-
-  for (int l = 1; l < Lmax; ++l) {
-    Op op{OP_PYR};
-    op.offset = static_cast<int>(pyr_table.size());
-    for (int k = 0; k < in->n_pairs; ++k) {
-      if (ctx->pair_levels[k] <= l) continue;
-      const PairDesc& p = g.pairs[k];
-      // recompute dims
-      int w = p.w, h = p.h;
-      for (int i = 0; i < l - 1; ++i) {
-        w = std::max(1, w / 2);
-        h = std::max(1, h / 2);
-      }
-      const int w2 = std::max(1, w / 2), h2 = std::max(1, h / 2);
-      for (int s = 0; s < 2; ++s) {
-        pyr_table.push_back({p.pyr[s][l - 1], w, h, p.pyr[s][l], w2, h2});
-        op.max_px = std::max(op.max_px, w2 * h2);
-      }
-    }
-    op.count = static_cast<int>(pyr_table.size()) - op.offset;
-    if (op.count) plan.push_back(op);
-  }
-  // Each warp iteration (5 per level, flow.cpp:78) is a linearisation (the
-  // constants planes) followed by its `sweeps` Jacobi sweeps as nseg
-  // launches (segments), ping-ponging two flow buffers per task.  The
-  // linearisation is fused into the first segment on the levels where the
-  // sweep launcher says it pays (hs_fuse_wanted), else it is a launch of its
-  // own.
-  const int nseg = hs_segments(ctx->sweeps);
-  std::vector<int> seg_len(nseg, ctx->sweeps / nseg);
-  for (int j = 0; j < ctx->sweeps % nseg; ++j) seg_len[j]++;
-  for (int l = Lmax - 1; l >= 0; --l) {
-    int n_l = 0, w_l = 0, h_l = 0;
-    for (const auto& t : tasks)
-      if (l < t.L) {
-        ++n_l;
-        w_l = std::max(w_l, t.dims[l][0]);
-        h_l = std::max(h_l, t.dims[l][1]);
-      }
-    const bool fuse = n_l > 0 && hs_fuse_wanted(n_l, w_l, h_l, seg_len[0]);
-    for (int it = 0; it < 5; ++it) {
-      // u0: zero at the coarsest level's first warp, the coarser flow
-      // upsampled at a finer level's first warp, else the previous warp's
-      auto lin_mode = [&](const TaskState& t) {
-        return (l == t.L - 1 && it == 0) ? 0 : (it == 0 ? 2 : 1);
-      };
-      if (!fuse) {
-        Op pop{OP_HSPREP};
-        pop.offset = static_cast<int>(hp_table.size());
-        for (auto& t : tasks) {
-          if (l >= t.L) continue;
-          const PairDesc& p = g.pairs[t.k];
-          const int sa = t.dir == 0 ? 0 : 1, sb = 1 - sa;
-          PrepTask q{};
-          q.a = p.pyr[sa][l];
-          q.b = p.pyr[sb][l];
-          q.mode = lin_mode(t);
-          q.uv_in = t.UV[t.cur];
-          q.wc = q.mode == 2 ? t.dims[l + 1][0] : 0;
-          q.hc = q.mode == 2 ? t.dims[l + 1][1] : 0;
-          q.w = t.dims[l][0];
-          q.h = t.dims[l][1];
-          q.kq = t.KQ;
-          if (q.mode != 1) {
-            q.uv0_out = t.UV[1 - t.cur];
-            t.cur ^= 1;
-          }
-          hp_table.push_back(q);
-          pop.max_w = std::max(pop.max_w, q.w);
-          pop.max_h = std::max(pop.max_h, q.h);
-        }
-        pop.count = static_cast<int>(hp_table.size()) - pop.offset;
-        if (pop.count) plan.push_back(pop);
-      }
-      for (int j = 0; j < nseg; ++j) {
-        Op op{OP_HS};
-        op.sweeps = seg_len[j];
-        op.fuse = (fuse && j == 0) ? 1 : 0;
-        op.offset = static_cast<int>(hs_table.size());
-        for (auto& t : tasks) {
-          if (l >= t.L) continue;
-          const PairDesc& p = g.pairs[t.k];
-          const int sa = t.dir == 0 ? 0 : 1, sb = 1 - sa;
-          HsTask h{};
-          h.kq = t.KQ;
-          h.uv_in = t.UV[t.cur];
-          h.uv_out = t.UV[1 - t.cur];
-          h.w = t.dims[l][0];
-          h.h = t.dims[l][1];
-          if (op.fuse) {
-            h.lin_a = p.pyr[sa][l];
-            h.lin_b = p.pyr[sb][l];
-            h.lin_mode = lin_mode(t);
-            h.wc = h.lin_mode == 2 ? t.dims[l + 1][0] : 0;
-            h.hc = h.lin_mode == 2 ? t.dims[l + 1][1] : 0;
-          }
-          t.cur ^= 1;
-          hs_table.push_back(h);
-          op.max_w = std::max(op.max_w, h.w);
-          op.max_h = std::max(op.max_h, h.h);
-        }
-        op.count = static_cast<int>(hs_table.size()) - op.offset;
-        if (op.count) plan.push_back(op);
-      }
-    }
-  }
-  for (auto& t : tasks) {
-    PairDesc& p = g.pairs[t.k];
-    p.flow_uv[t.dir] = t.UV[t.cur];
-  }
-  plan.push_back({OP_EVENT, 0, 0, 0, 0, 0, 3});
-  plan.push_back({OP_CANVAS});
-  plan.push_back({OP_EVENT, 0, 0, 0, 0, 0, 4});
-  plan.push_back({OP_TONE});
-  plan.push_back({OP_EVENT, 0, 0, 0, 0, 0, 5});
-
-  // upload tables + geometry + state
-  CUDA_TRY(ctx->alloc(&ctx->d_hs, hs_table.size() + 1));
-  CUDA_TRY(ctx->alloc(&ctx->d_hp, hp_table.size() + 1));
-  CUDA_TRY(ctx->alloc(&ctx->d_pyr, pyr_table.size() + 1));
-  CUDA_TRY(ctx->alloc(&ctx->d_lists, lists.size() + 1));
-  if (!hs_table.empty())
-    CUDA_TRY(cudaMemcpy(ctx->d_hs, hs_table.data(), hs_table.size() * sizeof(HsTask),
-                        cudaMemcpyHostToDevice));
-  if (!hp_table.empty())
-    CUDA_TRY(cudaMemcpy(ctx->d_hp, hp_table.data(), hp_table.size() * sizeof(PrepTask),
-                        cudaMemcpyHostToDevice));
-  if (!pyr_table.empty())
-    CUDA_TRY(cudaMemcpy(ctx->d_pyr, pyr_table.data(), pyr_table.size() * sizeof(PyrTask),
-                        cudaMemcpyHostToDevice));
-  if (!lists.empty())
-    CUDA_TRY(cudaMemcpy(ctx->d_lists, lists.data(), lists.size() * sizeof(int),
-                        cudaMemcpyHostToDevice));
-  {
-    CanvasParams& P = ctx->cparams;
-    P.cw = g.canvas_w;
-    P.ch = g.canvas_h;
-    P.ref = g.reference;
-    P.np = g.n_pairs;
-    P.weighting = g.weighting;
-    P.offx = g.offx;
-    P.offy = g.offy;
-    P.projection = g.projection;
-    P.lift_sin = g.lift_sin;
-    P.lift_cos = g.lift_cos;
-    P.lift_h = g.lift_h;
-    for (int v = 0; v < g.n_views; ++v) {
-      for (int i = 0; i < 9; ++i) P.views[v].inv[i] = g.views[v].inv[i];
-      P.views[v].rgba = g.rgba[v];
-      P.views[v].w = g.views[v].width;
-      P.views[v].h = g.views[v].height;
-      for (int i = 0; i < 4; ++i) P.views[v].bbox[i] = g.views[v].bbox[i];
-      P.views[v].gap[0] = g.views[v].gap[0];
-      P.views[v].gap[1] = g.views[v].gap[1];
-    }
-    for (int k = 0; k < g.n_pairs; ++k) {
-      const PairDesc& p = g.pairs[k];
-      CanvasPair& q = P.pairs[k];
-      q.view = p.view;
-      q.partner = p.partner;
-      q.x0 = p.x0;
-      q.y0 = p.y0;
-      q.w = p.w;
-      q.h = p.h;
-      q.theta = p.theta_i;
-      for (int s2 = 0; s2 < 2; ++s2) {
-        q.crop_raw[s2] = p.crop_raw[s2];
-        q.crop_cor[s2] = p.crop_cor[s2];
-        q.fuv[s2] = p.flow_uv[s2];
-      }
-    }
-  }
-  CUDA_TRY(ctx->alloc(&ctx->dg, 1));
-  CUDA_TRY(cudaMemcpy(ctx->dg, &g, sizeof(Geometry), cudaMemcpyHostToDevice));
-  CUDA_TRY(ctx->alloc(&ctx->dst, 1));
+  // ---- per-slot buffers, geometry and task tables (the plan is identical
+  // for every slot; the temporal state is shared) ----
+  CUDA_TRY(ctx->alloc(&ctx->dtemp, 1));
   {
     // window capacity (TransferWindow clamps to 1..3, color_transfer.cpp:8-11)
-    // and identity matrices for every view
-    std::unique_ptr<DevState> hs(new DevState());
-    std::memset(hs.get(), 0, sizeof(DevState));
+    std::unique_ptr<TemporalState> ts(new TemporalState());
+    std::memset(ts.get(), 0, sizeof(TemporalState));
     const int cap = std::min(3, std::max(1, in->window_capacity));
-    for (int k = 0; k < kMaxPairs; ++k) hs->windows[k].capacity = cap;
-    for (int v = 0; v < kMaxViews; ++v)
-      for (int i = 0; i < 9; ++i) hs->mview[v][i] = (i % 4 == 0) ? 1.0 : 0.0;
-    for (int c = 0; c < 3; ++c)
-      for (int v = 0; v < 256; ++v) hs->lut[c][v] = static_cast<unsigned char>(v);
-    CUDA_TRY(cudaMemcpy(ctx->dst, hs.get(), sizeof(DevState), cudaMemcpyHostToDevice));
+    for (int k = 0; k < kMaxPairs; ++k) ts->windows[k].capacity = cap;
+    CUDA_TRY(cudaMemcpy(ctx->dtemp, ts.get(), sizeof(TemporalState), cudaMemcpyHostToDevice));
   }
+  const Geometry base = g;
+  std::vector<float*> theta_dev(in->n_pairs, nullptr);
+  for (int sl = 0; sl < Ctx::kSlots; ++sl) {
+    SlotRes& S = ctx->slot[sl];
+    Geometry& g = S.hg;
+    g = base;
+    // buffers
+    for (int v = 0; v < in->n_views; ++v) {
+      ctx->frame_bytes[v] = static_cast<size_t>(in->view_width[v]) * in->view_height[v] * 3;
+      if (sl == 0) {
+        CUDA_TRY(ctx->alloc(&ctx->d_frames[v], ctx->frame_bytes[v]));
+        ctx->d_in[0][v] = ctx->d_frames[v];
+        for (int s2 = 1; s2 < Ctx::kSlots; ++s2)
+          CUDA_TRY(ctx->alloc(&ctx->d_in[s2][v], ctx->frame_bytes[v]));
+      }
+      g.frames[v] = ctx->d_in[sl][v];
+      const long long vpx = static_cast<long long>(in->view_width[v]) * in->view_height[v];
+      CUDA_TRY(ctx->alloc(&g.rgba[v], vpx));
+      ctx->max_view_px = std::max(ctx->max_view_px, vpx);
+    }
+    ctx->n_px = static_cast<long long>(g.canvas_w) * g.canvas_h;
+    CUDA_TRY(ctx->alloc(&S.d_pano, static_cast<size_t>(ctx->n_px) + 4));
+    CUDA_TRY(ctx->alloc(&ctx->d_out_rgb[sl], static_cast<size_t>(ctx->n_px) * 3 + 16));
+    CUDA_TRY(ctx->alloc(&ctx->d_out_mask[sl], static_cast<size_t>(ctx->n_px) + 16));
+
+    ctx->sweeps = std::max(1, in->flow_iterations / 5);  // flow.cpp:79-80
+    ctx->alpha2 = static_cast<float>(in->smoothness * in->smoothness);
+    ctx->theta_host.resize(in->n_pairs);
+    int max_zero = 16;
+    for (int k = 0; k < in->n_pairs; ++k) {
+      const stitch_b200_pair& sp = in->pairs[k];
+      PairDesc& p = g.pairs[k];
+      p.view = sp.view;
+      p.partner = sp.partner;
+      p.x0 = sp.x0;
+      p.y0 = sp.y0;
+      p.w = sp.x1 - sp.x0;
+      p.h = sp.y1 - sp.y0;
+      const int n = p.w * p.h;
+      ctx->max_crop_px = std::max(ctx->max_crop_px, n);
+      ctx->max_crop_w = std::max(ctx->max_crop_w, p.w);
+      ctx->max_crop_h = std::max(ctx->max_crop_h, p.h);
+      max_zero = std::max(max_zero, n);
+      ctx->theta_host[k].assign(sp.theta_i, sp.theta_i + n);
+      ctx->init.pairs[k].theta_i = ctx->theta_host[k].data();
+      if (!theta_dev[k]) {  // constant: shared by the slots
+        CUDA_TRY(ctx->alloc(&theta_dev[k], n));
+        CUDA_TRY(cudaMemcpy(theta_dev[k], sp.theta_i, sizeof(float) * n, cudaMemcpyHostToDevice));
+      }
+      p.theta_i = theta_dev[k];
+      for (int s = 0; s < 2; ++s) {
+        CUDA_TRY(ctx->alloc(&p.crop_raw[s], n));
+        CUDA_TRY(ctx->alloc(&p.crop_cor[s], n));
+      }
+      // dense_flow requires >= 16x16 (flow.cpp:146-148), else zero flow
+      p.flow_ok = (p.w >= 16 && p.h >= 16) ? 1 : 0;
+    }
+    if (sl == 0) CUDA_TRY(ctx->alloc(&ctx->d_zero, max_zero));
+
+    // pair depth (distance from the reference through partners)
+    std::vector<int> depth(in->n_pairs, 1);
+    int max_depth = 0;
+    for (int k = 0; k < in->n_pairs; ++k) {
+      const int partner = in->pairs[k].partner;
+      if (partner != in->reference)
+        for (int j = 0; j < k; ++j)
+          if (in->pairs[j].view == partner) depth[k] = depth[j] + 1;
+      g.pair_depth[k] = depth[k];
+      max_depth = std::max(max_depth, depth[k]);
+    }
+
+    // ---- flow plan: pyramids (flow.cpp:152-156), per-level tasks ----
+    struct TaskState {
+      int k, dir, L;
+      int dims[kMaxLevels][2];
+      float2* UV[2];  // (u, v) ping-pong
+      float4* KQ;  // (gx, gy, c, denom) per pixel of the current warp iteration
+      int cur;
+    };
+    std::vector<TaskState> tasks;
+    ctx->pair_levels.assign(in->n_pairs, 0);
+    int Lmax = 0;
+    for (int k = 0; k < in->n_pairs; ++k) {
+      PairDesc& p = g.pairs[k];
+      if (!p.flow_ok) {
+        for (int d = 0; d < 2; ++d) {
+          p.flow_uv[d] = ctx->d_zero;
+        }
+        continue;
+      }
+      int dims[kMaxLevels][2];
+      int L = 1;
+      dims[0][0] = p.w;
+      dims[0][1] = p.h;
+      for (int l = 1; l < in->flow_levels && l < kMaxLevels; ++l) {
+        if (dims[l - 1][0] < 16 || dims[l - 1][1] < 16) break;
+        dims[l][0] = std::max(1, dims[l - 1][0] / 2);
+        dims[l][1] = std::max(1, dims[l - 1][1] / 2);
+        ++L;
+      }
+      ctx->pair_levels[k] = L;
+      Lmax = std::max(Lmax, L);
+      for (int s = 0; s < 2; ++s)
+        for (int l = 0; l < L; ++l) CUDA_TRY(ctx->alloc(&p.pyr[s][l], dims[l][0] * dims[l][1]));
+      for (int d = 0; d < 2; ++d) {
+        TaskState t{};
+        t.k = k;
+        t.dir = d;
+        t.L = L;
+        std::memcpy(t.dims, dims, sizeof(dims));
+        for (int b = 0; b < 2; ++b) {
+          CUDA_TRY(ctx->alloc(&t.UV[b], p.w * p.h));
+        }
+        CUDA_TRY(ctx->alloc(&t.KQ, p.w * p.h));
+        t.cur = 0;
+        tasks.push_back(t);
+      }
+    }
+    ctx->n_levels_max = Lmax;
+
+    std::vector<HsTask> hs_table;
+    std::vector<PrepTask> hp_table;
+    std::vector<PyrTask> pyr_table;
+    std::vector<int> lists;
+    std::vector<Op> plan_scratch;  // the plan is the same for every slot
+    std::vector<Op>& plan = sl == 0 ? ctx->plan : plan_scratch;
+    plan.push_back({OP_EVENT, 0, 0, 0, 0, 0, 0});
+    plan.push_back({OP_EXPAND});
+    plan.push_back({OP_CROP});
+    plan.push_back({OP_EVENT, 0, 0, 0, 0, 0, 1});
+    for (int d = 1; d <= max_depth; ++d) {
+      Op op{OP_STATS};
+      op.offset = static_cast<int>(lists.size());
+      for (int k = 0; k < in->n_pairs; ++k)
+        if (depth[k] == d) lists.push_back(k);
+      op.count = static_cast<int>(lists.size()) - op.offset;
+      plan.push_back(op);
+    }
+    plan.push_back({OP_PREP});
+    plan.push_back({OP_EVENT, 0, 0, 0, 0, 0, 2});
+
+    for (int l = 1; l < Lmax; ++l) {
+      Op op{OP_PYR};
+      op.offset = static_cast<int>(pyr_table.size());
+      for (int k = 0; k < in->n_pairs; ++k) {
+        if (ctx->pair_levels[k] <= l) continue;
+        const PairDesc& p = g.pairs[k];
+        // recompute dims
+        int w = p.w, h = p.h;
+        for (int i = 0; i < l - 1; ++i) {
+          w = std::max(1, w / 2);
+          h = std::max(1, h / 2);
+        }
+        const int w2 = std::max(1, w / 2), h2 = std::max(1, h / 2);
+        for (int s = 0; s < 2; ++s) {
+          pyr_table.push_back({p.pyr[s][l - 1], w, h, p.pyr[s][l], w2, h2});
+          op.max_px = std::max(op.max_px, w2 * h2);
+        }
+      }
+      op.count = static_cast<int>(pyr_table.size()) - op.offset;
+      if (op.count) plan.push_back(op);
+    }
+    // Each warp iteration (5 per level, flow.cpp:78) is a linearisation (the
+    // constants planes) followed by its `sweeps` Jacobi sweeps as nseg
+    // launches (segments), ping-ponging two flow buffers per task.  The
+    // linearisation is fused into the first segment on the levels where the
+    // sweep launcher says it pays (hs_fuse_wanted), else it is a launch of its
+    // own.
+    const int nseg = hs_segments(ctx->sweeps);
+    std::vector<int> seg_len(nseg, ctx->sweeps / nseg);
+    for (int j = 0; j < ctx->sweeps % nseg; ++j) seg_len[j]++;
+    for (int l = Lmax - 1; l >= 0; --l) {
+      int n_l = 0, w_l = 0, h_l = 0;
+      for (const auto& t : tasks)
+        if (l < t.L) {
+          ++n_l;
+          w_l = std::max(w_l, t.dims[l][0]);
+          h_l = std::max(h_l, t.dims[l][1]);
+        }
+      const bool fuse = n_l > 0 && hs_fuse_wanted(n_l, w_l, h_l, seg_len[0]);
+      for (int it = 0; it < 5; ++it) {
+        // u0: zero at the coarsest level's first warp, the coarser flow
+        // upsampled at a finer level's first warp, else the previous warp's
+        auto lin_mode = [&](const TaskState& t) {
+          return (l == t.L - 1 && it == 0) ? 0 : (it == 0 ? 2 : 1);
+        };
+        if (!fuse) {
+          Op pop{OP_HSPREP};
+          pop.offset = static_cast<int>(hp_table.size());
+          for (auto& t : tasks) {
+            if (l >= t.L) continue;
+            const PairDesc& p = g.pairs[t.k];
+            const int sa = t.dir == 0 ? 0 : 1, sb = 1 - sa;
+            PrepTask q{};
+            q.a = p.pyr[sa][l];
+            q.b = p.pyr[sb][l];
+            q.mode = lin_mode(t);
+            q.uv_in = t.UV[t.cur];
+            q.wc = q.mode == 2 ? t.dims[l + 1][0] : 0;
+            q.hc = q.mode == 2 ? t.dims[l + 1][1] : 0;
+            q.w = t.dims[l][0];
+            q.h = t.dims[l][1];
+            q.kq = t.KQ;
+            if (q.mode != 1) {
+              q.uv0_out = t.UV[1 - t.cur];
+              t.cur ^= 1;
+            }
+            hp_table.push_back(q);
+            pop.max_w = std::max(pop.max_w, q.w);
+            pop.max_h = std::max(pop.max_h, q.h);
+          }
+          pop.count = static_cast<int>(hp_table.size()) - pop.offset;
+          if (pop.count) plan.push_back(pop);
+        }
+        for (int j = 0; j < nseg; ++j) {
+          Op op{OP_HS};
+          op.sweeps = seg_len[j];
+          op.fuse = (fuse && j == 0) ? 1 : 0;
+          op.offset = static_cast<int>(hs_table.size());
+          for (auto& t : tasks) {
+            if (l >= t.L) continue;
+            const PairDesc& p = g.pairs[t.k];
+            const int sa = t.dir == 0 ? 0 : 1, sb = 1 - sa;
+            HsTask h{};
+            h.kq = t.KQ;
+            h.uv_in = t.UV[t.cur];
+            h.uv_out = t.UV[1 - t.cur];
+            h.w = t.dims[l][0];
+            h.h = t.dims[l][1];
+            if (op.fuse) {
+              h.lin_a = p.pyr[sa][l];
+              h.lin_b = p.pyr[sb][l];
+              h.lin_mode = lin_mode(t);
+              h.wc = h.lin_mode == 2 ? t.dims[l + 1][0] : 0;
+              h.hc = h.lin_mode == 2 ? t.dims[l + 1][1] : 0;
+            }
+            t.cur ^= 1;
+            hs_table.push_back(h);
+            op.max_w = std::max(op.max_w, h.w);
+            op.max_h = std::max(op.max_h, h.h);
+          }
+          op.count = static_cast<int>(hs_table.size()) - op.offset;
+          if (op.count) plan.push_back(op);
+        }
+      }
+    }
+    for (auto& t : tasks) {
+      PairDesc& p = g.pairs[t.k];
+      p.flow_uv[t.dir] = t.UV[t.cur];
+    }
+    plan.push_back({OP_EVENT, 0, 0, 0, 0, 0, 3});
+    plan.push_back({OP_CANVAS});
+    plan.push_back({OP_EVENT, 0, 0, 0, 0, 0, 4});
+    plan.push_back({OP_TONE});
+    plan.push_back({OP_EVENT, 0, 0, 0, 0, 0, 5});
+
+    // upload tables + geometry + state
+    CUDA_TRY(ctx->alloc(&S.d_hs, hs_table.size() + 1));
+    CUDA_TRY(ctx->alloc(&S.d_hp, hp_table.size() + 1));
+    CUDA_TRY(ctx->alloc(&S.d_pyr, pyr_table.size() + 1));
+    if (!hs_table.empty())
+      CUDA_TRY(cudaMemcpy(S.d_hs, hs_table.data(), hs_table.size() * sizeof(HsTask),
+                          cudaMemcpyHostToDevice));
+    if (!hp_table.empty())
+      CUDA_TRY(cudaMemcpy(S.d_hp, hp_table.data(), hp_table.size() * sizeof(PrepTask),
+                          cudaMemcpyHostToDevice));
+    if (!pyr_table.empty())
+      CUDA_TRY(cudaMemcpy(S.d_pyr, pyr_table.data(), pyr_table.size() * sizeof(PyrTask),
+                          cudaMemcpyHostToDevice));
+    if (sl == 0) {
+      CUDA_TRY(ctx->alloc(&ctx->d_lists, lists.size() + 1));
+      if (!lists.empty())
+        CUDA_TRY(cudaMemcpy(ctx->d_lists, lists.data(), lists.size() * sizeof(int),
+                            cudaMemcpyHostToDevice));
+    }
+    {
+      CanvasParams& P = S.cparams;
+      P.cw = g.canvas_w;
+      P.ch = g.canvas_h;
+      P.ref = g.reference;
+      P.np = g.n_pairs;
+      P.weighting = g.weighting;
+      P.offx = g.offx;
+      P.offy = g.offy;
+      P.projection = g.projection;
+      P.lift_sin = g.lift_sin;
+      P.lift_cos = g.lift_cos;
+      P.lift_h = g.lift_h;
+      for (int v = 0; v < g.n_views; ++v) {
+        for (int i = 0; i < 9; ++i) P.views[v].inv[i] = g.views[v].inv[i];
+        P.views[v].rgba = g.rgba[v];
+        P.views[v].w = g.views[v].width;
+        P.views[v].h = g.views[v].height;
+        for (int i = 0; i < 4; ++i) P.views[v].bbox[i] = g.views[v].bbox[i];
+        P.views[v].gap[0] = g.views[v].gap[0];
+        P.views[v].gap[1] = g.views[v].gap[1];
+      }
+      for (int k = 0; k < g.n_pairs; ++k) {
+        const PairDesc& p = g.pairs[k];
+        CanvasPair& q = P.pairs[k];
+        q.view = p.view;
+        q.partner = p.partner;
+        q.x0 = p.x0;
+        q.y0 = p.y0;
+        q.w = p.w;
+        q.h = p.h;
+        q.theta = p.theta_i;
+        for (int s2 = 0; s2 < 2; ++s2) {
+          q.crop_raw[s2] = p.crop_raw[s2];
+          q.crop_cor[s2] = p.crop_cor[s2];
+          q.fuv[s2] = p.flow_uv[s2];
+        }
+      }
+    }
+    CUDA_TRY(ctx->alloc(&S.dg, 1));
+    CUDA_TRY(cudaMemcpy(S.dg, &g, sizeof(Geometry), cudaMemcpyHostToDevice));
+    CUDA_TRY(ctx->alloc(&S.dst, 1));
+    {
+      // identity matrices for every view; the temporal state lives in the
+      // shared TemporalState
+      std::unique_ptr<DevState> hs(new DevState());
+      std::memset(hs.get(), 0, sizeof(DevState));
+      char* tbase = reinterpret_cast<char*>(ctx->dtemp);
+      hs->windows = reinterpret_cast<PairWindow*>(tbase + offsetof(TemporalState, windows));
+      hs->balance = reinterpret_cast<BalanceState*>(tbase + offsetof(TemporalState, balance));
+      hs->frame_counter = reinterpret_cast<long long*>(tbase + offsetof(TemporalState, frame_counter));
+      for (int v = 0; v < kMaxViews; ++v)
+        for (int i = 0; i < 9; ++i) hs->mview[v][i] = (i % 4 == 0) ? 1.0 : 0.0;
+      for (int c = 0; c < 3; ++c)
+        for (int v = 0; v < 256; ++v) hs->lut[c][v] = static_cast<unsigned char>(v);
+      CUDA_TRY(cudaMemcpy(S.dst, hs.get(), sizeof(DevState), cudaMemcpyHostToDevice));
+    }
+  }
+  ctx->hg = ctx->slot[0].hg;
   CUDA_TRY(prepare_hs(ctx->sweeps));
   for (int j = 1; j <= ctx->sweeps; ++j) CUDA_TRY(prepare_hs(j));
   for (int sl = 0; sl < Ctx::kSlots; ++sl) {
@@ -645,7 +698,11 @@ int build_context(const stitch_b200_init* in, int device,
     CUDA_TRY(cudaEventCreateWithFlags(&ctx->h2d_done[sl], cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&ctx->comp_done[sl], cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&ctx->d2h_done[sl], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&ctx->color_done[sl], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&ctx->canvas_done[sl], cudaEventDisableTiming));
+    CUDA_TRY(cudaStreamCreateWithFlags(&ctx->slot[sl].cs, cudaStreamNonBlocking));
   }
+  CUDA_TRY(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
   CUDA_TRY(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
   CUDA_TRY(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
   for (auto& e : ctx->ring_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -654,39 +711,65 @@ int build_context(const stitch_b200_init* in, int device,
   CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_report),
                          sizeof(DevReport) * Ctx::kSlots, cudaHostAllocDefault));
 
-  // ---- capture the per-frame launch sequence once per pipeline slot ----
-  cudaStream_t s = ctx->stream;
+  // ---- the plan's four segments: front | colour | mid (flow) | back ----
+  {
+    const auto& pl = ctx->plan;
+    const int n = static_cast<int>(pl.size());
+    int b1 = -1, b2 = -1, b3 = -1;
+    for (int i = 0; i < n; ++i) {
+      if (b1 < 0 && pl[i].kind == OP_STATS) b1 = i;
+      if (b2 < 0 && pl[i].kind == OP_PREP) b2 = i;
+      if (b3 < 0 && pl[i].kind == OP_CANVAS) b3 = i > 0 && pl[i - 1].kind == OP_EVENT ? i - 1 : i;
+    }
+    if (b2 < 0) b2 = b3;
+    if (b1 < 0) b1 = b2;
+    ctx->seg_begin[0] = 0;
+    ctx->seg_begin[1] = b1;
+    ctx->seg_begin[2] = b2;
+    ctx->seg_begin[3] = b3;
+    ctx->seg_begin[4] = n;
+  }
+  // ---- capture each slot's segments once ----
   int launches = 0;
   for (int sl = 0; sl < Ctx::kSlots; ++sl) {
-    CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    SlotRes& S = ctx->slot[sl];
+    cudaStream_t s = S.cs;
     launches = 0;
-    for (const Op& op : plan) {
-      if (op.kind == OP_EVENT)
-        cudaEventRecordWithFlags(ctx->ev[sl][op.event], s, cudaEventRecordExternal);
-      else
-        launches += enqueue_op(ctx.get(), op, s, sl);
+    for (int seg = 0; seg < SlotRes::kSegs; ++seg) {
+      if (ctx->seg_begin[seg] == ctx->seg_begin[seg + 1]) continue;
+      CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      for (int i = ctx->seg_begin[seg]; i < ctx->seg_begin[seg + 1]; ++i) {
+        const Op& op = ctx->plan[i];
+        if (op.kind == OP_EVENT)
+          cudaEventRecordWithFlags(ctx->ev[sl][op.event], s, cudaEventRecordExternal);
+        else
+          launches += enqueue_op(ctx.get(), op, s, sl);
+      }
+      cudaError_t cap_err = cudaStreamEndCapture(s, &S.graph[seg]);
+      if (cap_err != cudaSuccess)
+        return fail(STITCH_B200_CudaError,
+                    std::string("graph capture: ") + cudaGetErrorString(cap_err));
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaGraphInstantiate(&S.exec[seg], S.graph[seg], 0));
     }
-    cudaError_t cap_err = cudaStreamEndCapture(s, &ctx->graph[sl]);
-    if (cap_err != cudaSuccess)
-      return fail(STITCH_B200_CudaError,
-                  std::string("graph capture: ") + cudaGetErrorString(cap_err));
-    CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaGraphInstantiate(&ctx->exec[sl], ctx->graph[sl], 0));
   }
   ctx->launches = launches;
   out = std::move(ctx);
   return STITCH_B200_OK;
 }
 
-int set_frame_pointers(Ctx* ctx, const std::uint8_t* const* ptrs) {
-  const int slot = ctx->ring_pos;
+// Point the slot's frame table at this frame's device inputs (pinned ring
+// of pointer tables, copied on the slot's stream).
+int set_frame_pointers(Ctx* ctx, int slot, const std::uint8_t* const* ptrs) {
+  const int r = ctx->ring_pos;
   ctx->ring_pos = (ctx->ring_pos + 1) % 16;
-  CUDA_TRY(cudaEventSynchronize(ctx->ring_ev[slot]));
-  const std::uint8_t** h = ctx->h_ptr_ring + slot * kMaxViews;
+  CUDA_TRY(cudaEventSynchronize(ctx->ring_ev[r]));
+  const std::uint8_t** h = ctx->h_ptr_ring + r * kMaxViews;
   for (int v = 0; v < ctx->hg.n_views; ++v) h[v] = ptrs[v];
-  CUDA_TRY(cudaMemcpyAsync(ctx->dg->frames, h, sizeof(void*) * ctx->hg.n_views,
-                           cudaMemcpyHostToDevice, ctx->stream));
-  CUDA_TRY(cudaEventRecord(ctx->ring_ev[slot], ctx->stream));
+  cudaStream_t cs = ctx->slot[slot].cs;
+  CUDA_TRY(cudaMemcpyAsync(ctx->slot[slot].dg->frames, h, sizeof(void*) * ctx->hg.n_views,
+                           cudaMemcpyHostToDevice, cs));
+  CUDA_TRY(cudaEventRecord(ctx->ring_ev[r], cs));
   return STITCH_B200_OK;
 }
 
@@ -730,18 +813,57 @@ int retire_slot(Ctx* ctx, int slot) {
   return STITCH_B200_OK;
 }
 
-// Compute-stream part of one frame on `slot`: wait until the slot's
-// previous download has drained, point the frame table at `dev_in`, launch
-// the slot's graph, fetch the report, mark completion.
+// Compute part of one frame on `slot`'s stream: wait until the slot's
+// previous download has drained, point the frame table at `dev_in`, then the
+// four segment graphs, with the frame-order points of the temporal state
+// between slots: the colour solves (3D-M windows) wait for the previous
+// frame's, the canvas (threshold history, frame counter) for the previous
+// frame's canvas.  Everything else of consecutive frames overlaps.
 int enqueue_frame(Ctx* ctx, int slot, const std::uint8_t* const* dev_in) {
-  CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->d2h_done[slot], 0));
-  int rc = set_frame_pointers(ctx, dev_in);
+  SlotRes& S = ctx->slot[slot];
+  const int prev = (slot + Ctx::kSlots - 1) % Ctx::kSlots;
+  CUDA_TRY(cudaStreamWaitEvent(S.cs, ctx->d2h_done[slot], 0));
+  int rc = set_frame_pointers(ctx, slot, dev_in);
   if (rc) return rc;
-  CUDA_TRY(cudaGraphLaunch(ctx->exec[slot], ctx->stream));
-  CUDA_TRY(cudaMemcpyAsync(&ctx->h_report[slot], &ctx->dst->report, sizeof(DevReport),
-                           cudaMemcpyDeviceToHost, ctx->stream));
-  CUDA_TRY(cudaEventRecord(ctx->comp_done[slot], ctx->stream));
+  if (S.exec[0]) CUDA_TRY(cudaGraphLaunch(S.exec[0], S.cs));
+  CUDA_TRY(cudaStreamWaitEvent(S.cs, ctx->color_done[prev], 0));
+  if (S.exec[1]) CUDA_TRY(cudaGraphLaunch(S.exec[1], S.cs));
+  CUDA_TRY(cudaEventRecord(ctx->color_done[slot], S.cs));
+  if (S.exec[2]) CUDA_TRY(cudaGraphLaunch(S.exec[2], S.cs));
+  CUDA_TRY(cudaStreamWaitEvent(S.cs, ctx->canvas_done[prev], 0));
+  if (S.exec[3]) CUDA_TRY(cudaGraphLaunch(S.exec[3], S.cs));
+  CUDA_TRY(cudaEventRecord(ctx->canvas_done[slot], S.cs));
+  CUDA_TRY(cudaMemcpyAsync(&ctx->h_report[slot], &S.dst->report, sizeof(DevReport),
+                           cudaMemcpyDeviceToHost, S.cs));
+  CUDA_TRY(cudaEventRecord(ctx->comp_done[slot], S.cs));
   ctx->last_slot = slot;
+  ctx->slot_joined[slot] = false;
+  return STITCH_B200_OK;
+}
+
+// Wait for all work of the context (uploads, frames, downloads, API stream).
+int sync_all(Ctx* ctx) {
+  CUDA_TRY(cudaStreamSynchronize(ctx->h2d));
+  for (auto& S : ctx->slot) CUDA_TRY(cudaStreamSynchronize(S.cs));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->d2h));
+  return STITCH_B200_OK;
+}
+
+// The slot streams wait for the work enqueued so far on the API stream.
+int fork_api_stream(Ctx* ctx) {
+  CUDA_TRY(cudaEventRecord(ctx->fork_ev, ctx->stream));
+  for (auto& S : ctx->slot) CUDA_TRY(cudaStreamWaitEvent(S.cs, ctx->fork_ev, 0));
+  return STITCH_B200_OK;
+}
+
+// The API stream waits for every frame enqueued so far.
+int join_api_stream(Ctx* ctx) {
+  for (int sl = 0; sl < Ctx::kSlots; ++sl)
+    if (!ctx->slot_joined[sl]) {
+      CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->comp_done[sl], 0));
+      ctx->slot_joined[sl] = true;
+    }
   return STITCH_B200_OK;
 }
 
@@ -760,7 +882,7 @@ int submit_host(Ctx* ctx, const std::uint8_t* const* frames, std::uint8_t* pano_
     CUDA_TRY(cudaMemcpyAsync(ctx->d_in[slot][v], frames[v], ctx->frame_bytes[v],
                              cudaMemcpyHostToDevice, ctx->h2d));
   CUDA_TRY(cudaEventRecord(ctx->h2d_done[slot], ctx->h2d));
-  CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->h2d_done[slot], 0));
+  CUDA_TRY(cudaStreamWaitEvent(ctx->slot[slot].cs, ctx->h2d_done[slot], 0));
   const std::uint8_t* in[kMaxViews];
   for (int v = 0; v < ctx->hg.n_views; ++v) in[v] = ctx->d_in[slot][v];
   rc = enqueue_frame(ctx, slot, in);
@@ -1110,17 +1232,11 @@ int stitch_b200_refine_warning(const stitch_b200_ctx* h, int k) {
 // threshold history and frame counter over (pipeline.cpp:399-405).
 static int carry_into(stitch_b200_ctx* h, std::unique_ptr<Ctx>& fresh) {
   Ctx* ctx = h->c.get();
-  CUDA_TRY(cudaStreamSynchronize(ctx->h2d));
-  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-  CUDA_TRY(cudaStreamSynchronize(ctx->d2h));
+  int rc = sync_all(ctx);
+  if (rc) return rc;
   // carry windows, threshold history and the frame counter over
   // (pipeline.cpp:399-405)
-  CUDA_TRY(cudaMemcpy(&fresh->dst->windows, &ctx->dst->windows, sizeof(DevState::windows),
-                      cudaMemcpyDeviceToDevice));
-  CUDA_TRY(cudaMemcpy(&fresh->dst->balance, &ctx->dst->balance, sizeof(BalanceState),
-                      cudaMemcpyDeviceToDevice));
-  CUDA_TRY(cudaMemcpy(&fresh->dst->frame_counter, &ctx->dst->frame_counter, sizeof(long long),
-                      cudaMemcpyDeviceToDevice));
+  CUDA_TRY(cudaMemcpy(fresh->dtemp, ctx->dtemp, sizeof(TemporalState), cudaMemcpyDeviceToDevice));
   h->c = std::move(fresh);  // the old context is released here
   return STITCH_B200_OK;
 }
@@ -1269,7 +1385,13 @@ int stitch_b200_process_device(stitch_b200_ctx* h, const uint8_t* const* dev_fra
   const int slot = static_cast<int>(ctx->seq % Ctx::kSlots);
   int rc = retire_slot(ctx, slot);
   if (rc) return rc;
+  // stream-ordered on the API stream: inputs written there are seen, and
+  // work enqueued there afterwards sees the outputs
+  rc = fork_api_stream(ctx);
+  if (rc) return rc;
   rc = enqueue_frame(ctx, slot, dev_frames);
+  if (rc) return rc;
+  rc = join_api_stream(ctx);
   if (rc) return rc;
   ++ctx->seq;
   if (report) {
@@ -1277,6 +1399,30 @@ int stitch_b200_process_device(stitch_b200_ctx* h, const uint8_t* const* dev_fra
     fill_report(ctx, slot, report);
   }
   return STITCH_B200_OK;
+}
+
+int stitch_b200_process_device_async(stitch_b200_ctx* h, const uint8_t* const* dev_frames) {
+  Ctx* ctx = h->c.get();
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  const int slot = static_cast<int>(ctx->seq % Ctx::kSlots);
+  int rc = retire_slot(ctx, slot);
+  if (rc) return rc;
+  rc = enqueue_frame(ctx, slot, dev_frames);
+  if (rc) return rc;
+  ++ctx->seq;
+  return STITCH_B200_OK;
+}
+
+int stitch_b200_fork(stitch_b200_ctx* h) {
+  Ctx* ctx = h->c.get();
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  return fork_api_stream(ctx);
+}
+
+int stitch_b200_join(stitch_b200_ctx* h) {
+  Ctx* ctx = h->c.get();
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  return join_api_stream(ctx);
 }
 
 int stitch_b200_profile_frame(stitch_b200_ctx* h, const uint8_t* const* dev_frames, int max_ops,
@@ -1288,10 +1434,12 @@ int stitch_b200_profile_frame(stitch_b200_ctx* h, const uint8_t* const* dev_fram
     int rc = retire_slot(ctx, sl);
     if (rc) return -rc;
   }
+  for (auto& S : ctx->slot) CUDA_TRY(cudaStreamSynchronize(S.cs));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->d2h));
-  int rc = set_frame_pointers(ctx, dev_frames);
+  int rc = set_frame_pointers(ctx, 0, dev_frames);
   if (rc) return -rc;
+  CUDA_TRY(cudaStreamSynchronize(ctx->slot[0].cs));
   ctx->last_slot = 0;
   std::vector<cudaEvent_t> evs;
   std::vector<int> ks;
@@ -1338,13 +1486,7 @@ int stitch_b200_device_pano(const stitch_b200_ctx* h, uint8_t** rgb, uint8_t** m
 
 void* stitch_b200_stream(const stitch_b200_ctx* h) { return h->c->stream; }
 
-int stitch_b200_synchronize(stitch_b200_ctx* h) {
-  Ctx* ctx = h->c.get();
-  CUDA_TRY(cudaStreamSynchronize(ctx->h2d));
-  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-  CUDA_TRY(cudaStreamSynchronize(ctx->d2h));
-  return STITCH_B200_OK;
-}
+int stitch_b200_synchronize(stitch_b200_ctx* h) { return sync_all(h->c.get()); }
 
 int stitch_b200_launches_per_frame(const stitch_b200_ctx* h) { return h->c->launches; }
 
@@ -1380,8 +1522,8 @@ int stitch_b200_debug_crop(stitch_b200_ctx* h, int k, int side, int corrected, u
   Ctx* ctx = h->c.get();
   if (k < 0 || k >= ctx->hg.n_pairs || side < 0 || side > 1)
     return fail(STITCH_B200_ConfigurationError, "bad pair/side");
-  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-  const PairDesc& p = ctx->hg.pairs[k];
+  if (int rc_ = sync_all(ctx)) return rc_;
+  const PairDesc& p = ctx->slot[ctx->last_slot].hg.pairs[k];
   std::vector<uchar4> buf(static_cast<size_t>(p.w) * p.h);
   CUDA_TRY(cudaMemcpy(buf.data(), corrected ? p.crop_cor[side] : p.crop_raw[side],
                       buf.size() * sizeof(uchar4), cudaMemcpyDeviceToHost));
@@ -1398,8 +1540,8 @@ int stitch_b200_debug_flow(stitch_b200_ctx* h, int k, int dir, float* u, float* 
   Ctx* ctx = h->c.get();
   if (k < 0 || k >= ctx->hg.n_pairs || dir < 0 || dir > 1)
     return fail(STITCH_B200_ConfigurationError, "bad pair/dir");
-  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-  const PairDesc& p = ctx->hg.pairs[k];
+  if (int rc_ = sync_all(ctx)) return rc_;
+  const PairDesc& p = ctx->slot[ctx->last_slot].hg.pairs[k];
   const size_t n = static_cast<size_t>(p.w) * p.h;
   std::vector<float2> uv(n);
   CUDA_TRY(cudaMemcpy(uv.data(), p.flow_uv[dir], n * sizeof(float2), cudaMemcpyDeviceToHost));
@@ -1420,9 +1562,9 @@ int stitch_b200_debug_flow(stitch_b200_ctx* h, int k, int dir, float* u, float* 
 
 int stitch_b200_debug_prebalance(stitch_b200_ctx* h, uint8_t* rgb, uint8_t* mask) {
   Ctx* ctx = h->c.get();
-  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  if (int rc_ = sync_all(ctx)) return rc_;
   std::vector<uchar4> buf(static_cast<size_t>(ctx->n_px));
-  CUDA_TRY(cudaMemcpy(buf.data(), ctx->d_pano, buf.size() * sizeof(uchar4),
+  CUDA_TRY(cudaMemcpy(buf.data(), ctx->slot[ctx->last_slot].d_pano, buf.size() * sizeof(uchar4),
                       cudaMemcpyDeviceToHost));
   for (size_t i = 0; i < buf.size(); ++i) {
     rgb[3 * i + 0] = buf[i].x;
@@ -1438,7 +1580,7 @@ int stitch_b200_debug_warp_view(stitch_b200_ctx* h, int view, const uint8_t* hos
   Ctx* ctx = h->c.get();
   if (view < 0 || view >= ctx->hg.n_views) return fail(STITCH_B200_ConfigurationError, "bad view");
   CUDA_TRY(cudaSetDevice(ctx->device));
-  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  if (int rc_ = sync_all(ctx)) return rc_;
   std::uint8_t *df = nullptr, *dr = nullptr, *dm = nullptr;
   uchar4* dq = nullptr;
   const size_t n = static_cast<size_t>(ctx->n_px);
@@ -1449,7 +1591,7 @@ int stitch_b200_debug_warp_view(stitch_b200_ctx* h, int view, const uint8_t* hos
   CUDA_TRY(cudaMalloc(&dm, n));
   CUDA_TRY(cudaMemcpy(df, host_frame, ctx->frame_bytes[view], cudaMemcpyHostToDevice));
   launch_expand_one(df, dq, vpx, ctx->stream);
-  launch_warp_view(ctx->dg, view, dq, dr, dm, ctx->stream);
+  launch_warp_view(ctx->slot[0].dg, view, dq, dr, dm, ctx->stream);
   cudaError_t e = cudaStreamSynchronize(ctx->stream);
   if (e == cudaSuccess) e = cudaMemcpy(rgb, dr, n * 3, cudaMemcpyDeviceToHost);
   if (e == cudaSuccess) e = cudaMemcpy(mask, dm, n, cudaMemcpyDeviceToHost);
@@ -1528,8 +1670,8 @@ int stitch_b200_ssim(int width, int height, const uint8_t* a_rgb, const uint8_t*
 int stitch_b200_pair_quality(stitch_b200_ctx* h, int k, double out[3]) {
   Ctx* ctx = h->c.get();
   if (k < 0 || k >= ctx->hg.n_pairs) return fail(STITCH_B200_ConfigurationError, "bad pair index");
-  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-  const PairDesc& p = ctx->hg.pairs[k];
+  if (int rc_ = sync_all(ctx)) return rc_;
+  const PairDesc& p = ctx->slot[ctx->last_slot].hg.pairs[k];
   const int n = p.w * p.h;
   unsigned long long sse = 0, cnt = 0;
   CUDA_TRY(gpu_psnr_parts(p.crop_cor[0], p.crop_raw[0], n, &sse, &cnt, ctx->stream));

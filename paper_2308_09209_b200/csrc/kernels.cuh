@@ -172,15 +172,25 @@ struct PyrTask {
 };
 
 // mutable per-context device state
+// Temporal state of one stream (PipelineState's windows, threshold history
+// and frame counter): shared by the pipeline slots, updated in frame order.
+struct TemporalState {
+  PairWindow windows[kMaxPairs];
+  BalanceState balance;
+  long long frame_counter;
+};
+
+// Per-slot frame state: scratch accumulators, this frame's colour matrices,
+// LUT and report, plus pointers into the shared TemporalState.
 struct DevState {
   PairStats stats[kMaxPairs];
-  PairWindow windows[kMaxPairs];
+  PairWindow* windows;          // -> TemporalState::windows
   double mview[kMaxViews][9];  // colour matrix applied to each view
   unsigned int pano_hist[3][256];
-  BalanceState balance;
+  BalanceState* balance;        // -> TemporalState::balance
   unsigned char lut[3][256];
   DevReport report;
-  long long frame_counter;
+  long long* frame_counter;     // -> TemporalState::frame_counter
   unsigned int pair_done[kMaxPairs];  // CTA completion counters (last-CTA solve)
   unsigned int canvas_done;
 };
