@@ -74,7 +74,7 @@ struct Ctx {
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;  // the API stream (process_device, profile, debug)
-  static constexpr int kSlots = 2;
+  static constexpr int kSlots = 3;
   SlotRes slot[kSlots];
   Geometry hg{};  // metadata (slot 0's mirror; buffers: use slot[s].hg)
   TemporalState* dtemp = nullptr;
@@ -106,9 +106,9 @@ struct Ctx {
   cudaEvent_t color_done[kSlots] = {}, canvas_done[kSlots] = {};
   cudaEvent_t fork_ev = nullptr;
   long long seq = 0;                       // frames submitted (any API)
-  long long slot_ticket[kSlots] = {-1, -1};  // ticket occupying each slot
-  bool slot_pending[kSlots] = {false, false};
-  bool slot_joined[kSlots] = {true, true};  // the API stream waited for the slot's frame
+  long long slot_ticket[kSlots];  // ticket occupying each slot
+  bool slot_pending[kSlots];
+  bool slot_joined[kSlots];  // the API stream waited for the slot's frame
   std::vector<std::pair<long long, stitch_b200_report>> done_reports;
   int last_slot = 0;
   // pinned ring for device-frame pointer tables
@@ -118,6 +118,14 @@ struct Ctx {
   DevReport* h_report = nullptr;  // one per slot (pinned)
   std::vector<int> pair_levels;
   float2* d_zero = nullptr;
+
+  Ctx() {
+    for (int s = 0; s < kSlots; ++s) {
+      slot_ticket[s] = -1;
+      slot_pending[s] = false;
+      slot_joined[s] = true;
+    }
+  }
 
   ~Ctx() {
     if (stream) cudaStreamSynchronize(stream);
