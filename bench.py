@@ -35,7 +35,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-E2E_IN_FLIGHT = 3  # frames in flight on the host path (the context has 3 pipeline slots)
+E2E_IN_FLIGHT = 4  # frames in flight on the host path (the context has 4 pipeline slots)
 METRIC = "stitched panorama frames/s & p50 ms/frame, 4x1080p cams; achieved HBM GB/s"
 UNIT = "frames/s"
 

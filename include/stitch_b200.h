@@ -280,7 +280,7 @@ int stitch_b200_process_device(stitch_b200_ctx* ctx,
                                const uint8_t* const* dev_frames,
                                stitch_b200_report* report);
 
-/* Pipelined device-resident frames.  A context runs two pipeline slots on
+/* Pipelined device-resident frames.  A context runs four pipeline slots on
  * their own streams; consecutive frames overlap except at the points where
  * the reference's temporal state orders them (the 3D-M window update, the
  * threshold history), which the slots chain in frame order.
@@ -288,7 +288,7 @@ int stitch_b200_process_device(stitch_b200_ctx* ctx,
  * stream; stitch_b200_fork makes subsequently enqueued frames wait for the
  * API stream's work so far, stitch_b200_join makes the API stream wait for
  * every frame enqueued so far.  The outputs of frame t stay valid until
- * frame t + 2 is enqueued. */
+ * frame t + 4 is enqueued. */
 int stitch_b200_process_device_async(stitch_b200_ctx* ctx, const uint8_t* const* dev_frames);
 int stitch_b200_fork(stitch_b200_ctx* ctx);
 int stitch_b200_join(stitch_b200_ctx* ctx);

@@ -74,7 +74,7 @@ struct Ctx {
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;  // the API stream (process_device, profile, debug)
-  static constexpr int kSlots = 3;
+  static constexpr int kSlots = 4;
   SlotRes slot[kSlots];
   Geometry hg{};  // metadata (slot 0's mirror; buffers: use slot[s].hg)
   TemporalState* dtemp = nullptr;
