@@ -413,3 +413,34 @@ def test_ring_360_parity():
     assert [(p.view, p.partner) for p in state.pairs] == [(1, 0), (5, 0), (2, 1), (4, 5), (3, 2)]
     for t in range(3):
         check_frame(state, ost, frames_at(sc, t), t)
+
+
+def test_heterogeneous_camera_sizes():
+    """Views of different sizes (the reference's Frame sizes are per view):
+    view 2's frames are a cropped window of the synthetic camera, with the
+    principal point shifted accordingly (a cropped pinhole image)."""
+    sc = scene(views=3, width=240, height=180, frames=3,
+               casts=[(1, 1, 1), (0.9, 1.0, 1.1), (1.1, 0.95, 1.0)])
+    cfg = product_config(sc)
+    x0, y0, cw, ch = 24, 12, 200, 150
+    cfg.views[2].intrinsics.cx -= x0
+    cfg.views[2].intrinsics.cy -= y0
+
+    def frames(t):
+        fs = frames_at(sc, t)
+        fs[2] = pb.Frame(np.ascontiguousarray(fs[2].data[y0:y0 + ch, x0:x0 + cw]))
+        return fs
+
+    state = pb.initialize(cfg, frames(0))
+    cams = []
+    for v in cfg.views:
+        r = np.asarray(v.extrinsics.rotation, np.float64).reshape(9)
+        t = np.asarray(v.extrinsics.translation, np.float64).reshape(3)
+        cams.append((v.intrinsics.fx, v.intrinsics.fy, v.intrinsics.cx, v.intrinsics.cy,
+                     list(r), list(t)))
+    sizes = [(240, 180), (240, 180), (cw, ch)]
+    ost = O.OracleState(O.make_config(3, cfg.reference, sizes, cams, threads=4, keep_debug=1))
+    check_geometry(state, ost, 3)
+    for t in range(3):
+        check_frame(state, ost, frames(t), t)
+    state.close()
