@@ -2,6 +2,7 @@
 // against the CPU oracle, written in the style of the reference's doctest
 // suites (proj/tests/test_imaging.cpp).  Needs a B200; run by
 // tests/test_cpp_api.py (gpu marker).
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -183,10 +184,67 @@ TEST_CASE(run_sequence_reports_every_frame) {
   stitch_b200_synth_destroy(s);
 }
 
+TEST_CASE(quality_metrics_match_oracle) {
+  // metrics.cpp psnr / ssim through the C ABI (device) against the oracle
+  const int w = 96, h = 64;
+  std::vector<std::uint8_t> a(w * h * 3), b(w * h * 3), mb(w * h, 1);
+  unsigned x = 12345;
+  for (size_t i = 0; i < a.size(); ++i) {
+    x = x * 1103515245u + 12345u;
+    a[i] = static_cast<std::uint8_t>(x >> 24);
+    b[i] = static_cast<std::uint8_t>((3 * a[i] + ((x >> 16) & 255)) / 4);
+  }
+  for (int y = 0; y < 20; ++y)
+    for (int xx = 0; xx < 30; ++xx) mb[y * w + xx] = 0;
+  so_frame fa{w, h, a.data(), nullptr}, fb{w, h, b.data(), mb.data()};
+  double gp = 0, op = 0, gs = 0, os = 0;
+  check(stitch_b200_psnr(w, h, a.data(), nullptr, b.data(), mb.data(), &gp));
+  CHECK(so_psnr(&fa, &fb, &op) == SO_OK);
+  CHECK(gp == op);
+  check(stitch_b200_ssim(w, h, a.data(), nullptr, b.data(), mb.data(), &gs));
+  CHECK(so_ssim(&fa, &fb, &os) == SO_OK);
+  CHECK(gs == os);
+  double same = 0;
+  check(stitch_b200_psnr(w, h, a.data(), nullptr, a.data(), nullptr, &same));
+  CHECK(std::isinf(same));
+}
+
+TEST_CASE(update_maps_keeps_geometry_for_unchanged_maps) {
+  // re-refinement with the unrefined maps rebuilds the same device geometry
+  stitch_b200_synth* s = make_scene(3, 160, 120);
+  stitch_b200_config c;
+  StitchConfig cfg = config_of(s, c);
+  std::vector<Frame> first(3, Frame(160, 120));
+  for (int v = 0; v < 3; ++v) check(stitch_b200_synth_render(s, v, 0, first[v].data.data(), 4));
+  PipelineState st = initialize(cfg, first);
+  stitch_b200_pair p0{};
+  std::vector<float> th0(160 * 120 * 2), th1(160 * 120 * 2);
+  check(stitch_b200_get_pair(st.handle(), 0, &p0, th0.data()));
+  std::vector<double> maps(9 * 3);
+  check(stitch_b200_camera_maps(&c, maps.data()));
+  std::vector<std::array<double, 9>> m(3);
+  for (int v = 0; v < 3; ++v)
+    for (int i = 0; i < 9; ++i) m[v][i] = maps[9 * v + i];
+  process_frame(st, first);
+  st.update_maps(m);
+  stitch_b200_pair p1{};
+  check(stitch_b200_get_pair(st.handle(), 0, &p1, th1.data()));
+  CHECK(p0.x0 == p1.x0 && p0.y0 == p1.y0 && p0.x1 == p1.x1 && p0.y1 == p1.y1);
+  const size_t n = static_cast<size_t>(p0.x1 - p0.x0) * (p0.y1 - p0.y0);
+  bool same = true;
+  for (size_t i = 0; i < n; ++i) same = same && th0[i] == th1[i];
+  CHECK(same);
+  ProcessResult r = process_frame(st, first);
+  CHECK(r.report.frame_index == 1);  // the temporal state was carried over
+  stitch_b200_synth_destroy(s);
+}
+
 int main() {
   process_frame_matches_oracle();
   errors_surface_as_stitch_error();
   run_sequence_reports_every_frame();
+  quality_metrics_match_oracle();
+  update_maps_keeps_geometry_for_unchanged_maps();
   std::printf("%d checks, %d failures\n", g_checks, g_failures);
   return g_failures ? 1 : 0;
 }
