@@ -356,6 +356,9 @@ inline RunResult run_sequence(const StitchConfig& config, const std::vector<std:
   result.report.scene_id = config.scene_id;
   result.report.threads = config.threads;
   result.report.frames = static_cast<long>(frames);
+  // pipeline.cpp:390-392: any pair whose refinement fell back
+  for (int k = 0; k < state.n_pairs(); ++k)
+    result.report.refine_warning |= stitch_b200_refine_warning(state.handle(), k) != 0;
   const int every = config.refine.rerefine_every;
   for (std::size_t t = 0; t < frames; ++t) {
     std::vector<Frame> set;

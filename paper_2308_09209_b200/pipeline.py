@@ -505,6 +505,8 @@ def run_sequence(config: StitchConfig, views: Sequence[Sequence[Frame]],
     state = initialize(config, [s[0] for s in views])
     result = RunResult([], RunReport(scene_id=config.scene_id, threads=config.threads,
                                      frames=frames))
+    # pipeline.cpp:390-392: any pair whose refinement fell back
+    result.report.refine_warning = any(p.refine_warning for p in state.pairs)
     try:
         every = config.refine.rerefine_every
         for t in range(frames):
