@@ -150,20 +150,32 @@ __global__ void __launch_bounds__(256) k_ssim_v(const double* __restrict__ tmp,
   }
 }
 
-// the reference's running sum over window positions, in row-major order
+// the reference's running sum over window positions, in row-major order:
+// the warp stages 32 terms at a time (coalesced loads), lane 0 adds them in
+// order
 __global__ void k_ssim_sum(const double* __restrict__ term, const std::uint8_t* __restrict__ valid,
                            long long n, double* __restrict__ out_sum,
                            long long* __restrict__ out_cnt) {
-  if (threadIdx.x != 0) return;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x >= 32) return;
   double sum = 0.0;
   long long cnt = 0;
-  for (long long i = 0; i < n; ++i)
-    if (valid[i]) {
-      sum += term[i];
-      ++cnt;
+  for (long long base = 0; base < n; base += 32) {
+    const long long i = base + lane;
+    const bool ok = i < n && valid[i];
+    const double t = ok ? term[i] : 0.0;
+    const unsigned m = __ballot_sync(0xffffffffu, ok);
+#pragma unroll 8
+    for (int j = 0; j < 32; ++j) {
+      const double x = __shfl_sync(0xffffffffu, t, j);
+      if (lane == 0 && ((m >> j) & 1u)) sum += x;
     }
-  *out_sum = sum;
-  *out_cnt = cnt;
+    cnt += __popc(m);
+  }
+  if (lane == 0) {
+    *out_sum = sum;
+    *out_cnt = cnt;
+  }
 }
 
 namespace {
