@@ -10,12 +10,14 @@ no collective on the frame path; "scaling": "weak").
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
 value  : aggregate panorama frames/s with the input frames resident in HBM
-         (device-to-device path, stitch_b200_process_device), CUDA-event timed
-         on the context stream, max over ranks.
-e2e    : the same metric through the reference-facing C-ABI call
-         (stitch_b200_process) with pinned HOST frames: H2D of every camera
-         frame + D2H of the balanced panorama (RGB + mask) inside the timed
-         region, max over ranks.
+         (stitch_b200_process_device_async, four frames in flight over the
+         context's pipeline slots), CUDA-event timed on the context's API
+         stream around a fork and a join, max over ranks.
+e2e    : the same metric through the reference-facing C-ABI calls with
+         pinned HOST frames (stitch_b200_submit / stitch_b200_wait, four in
+         flight): H2D of every camera frame + D2H of the balanced panorama
+         (RGB + mask) inside the timed region, max over ranks; the
+         synchronous stitch_b200_process is reported as sync_process_value.
 --impl reference : the CPU oracle (the reference's path restated in C; the
          reference itself needs Eigen3 and cannot be built here) on the box's
          host cores, same workload, rank 0 only.
