@@ -323,7 +323,8 @@ def test_create_from_snapshot_matches_initialize():
                                  {"STITCH_B200_HS_SEGS": "3"},
                                  {"STITCH_B200_HS_SEGS": "10", "STITCH_B200_HS_VARIANT": "5"},
                                  {"STITCH_B200_PREP_VARIANT": "0", "STITCH_B200_HS_FUSE": "0"},
-                                 {"STITCH_B200_HS_FUSE": "0"}])
+                                 {"STITCH_B200_HS_FUSE": "0"},
+                                 {"STITCH_B200_HS_XL": "1"}])
 def test_flow_kernel_variants_bit_exact(env):
     """The register-blocked Jacobi kernel's region variants, sweep
     segmentations and its exact IEEE-division fallback path (forced) all
