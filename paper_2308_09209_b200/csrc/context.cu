@@ -43,7 +43,8 @@ struct Op {
   int max_w = 0, max_h = 0, max_px = 0;
   int event = 0;
   int sweeps = 0;  // OP_HS: Jacobi sweeps of this launch (segment length)
-  int fuse = 0;    // OP_HS: the launch also linearises the warp iteration
+  int fuse = 0;    // OP_HS: 1 also linearises this warp iteration (prologue),
+                   // 2 also the next one (epilogue)
 };
 
 }  // namespace
@@ -441,8 +442,9 @@ int build_context(const stitch_b200_init* in, int device,
       int k, dir, L;
       int dims[kMaxLevels][2];
       float2* UV[2];  // (u, v) ping-pong
-      float4* KQ;  // (gx, gy, c, denom) per pixel of the current warp iteration
-      int cur;
+      float4* KQ[2];  // (gx, gy, c, denom) per pixel: current warp iteration /
+                      // the next one's, written by an epilogue linearisation
+      int cur, kc;
     };
     std::vector<TaskState> tasks;
     ctx->pair_levels.assign(in->n_pairs, 0);
@@ -478,8 +480,9 @@ int build_context(const stitch_b200_init* in, int device,
         for (int b = 0; b < 2; ++b) {
           CUDA_TRY(ctx->alloc(&t.UV[b], p.w * p.h));
         }
-        CUDA_TRY(ctx->alloc(&t.KQ, p.w * p.h));
+        for (int b = 0; b < 2; ++b) CUDA_TRY(ctx->alloc(&t.KQ[b], p.w * p.h));
         t.cur = 0;
+        t.kc = 0;
         tasks.push_back(t);
       }
     }
@@ -532,7 +535,9 @@ int build_context(const stitch_b200_init* in, int device,
     // launches (segments), ping-ponging two flow buffers per task.  The
     // linearisation is fused into the first segment on the levels where the
     // sweep launcher says it pays (hs_fuse_wanted), else it is a launch of its
-    // own.
+    // own; from the second warp iteration on, the previous iteration's last
+    // segment linearises it in its epilogue where that is wanted
+    // (hs_elin_wanted; the constants then ping-pong between two planes).
     const int nseg = hs_segments(ctx->sweeps);
     std::vector<int> seg_len(nseg, ctx->sweeps / nseg);
     for (int j = 0; j < ctx->sweeps % nseg; ++j) seg_len[j]++;
@@ -545,13 +550,17 @@ int build_context(const stitch_b200_init* in, int device,
           h_l = std::max(h_l, t.dims[l][1]);
         }
       const bool fuse = n_l > 0 && hs_fuse_wanted(n_l, w_l, h_l, seg_len[0]);
+      // (a single segment cannot carry both a prologue and an epilogue)
+      const bool elin = n_l > 0 && hs_elin_wanted(n_l, w_l, h_l, seg_len[nseg - 1]) &&
+                        (nseg >= 2 || !fuse);
       for (int it = 0; it < 5; ++it) {
+        const bool lin_done = elin && it > 0;  // by the previous iteration's epilogue
         // u0: zero at the coarsest level's first warp, the coarser flow
         // upsampled at a finer level's first warp, else the previous warp's
         auto lin_mode = [&](const TaskState& t) {
           return (l == t.L - 1 && it == 0) ? 0 : (it == 0 ? 2 : 1);
         };
-        if (!fuse) {
+        if (!fuse && !lin_done) {
           Op pop{OP_HSPREP};
           pop.offset = static_cast<int>(hp_table.size());
           for (auto& t : tasks) {
@@ -567,7 +576,7 @@ int build_context(const stitch_b200_init* in, int device,
             q.hc = q.mode == 2 ? t.dims[l + 1][1] : 0;
             q.w = t.dims[l][0];
             q.h = t.dims[l][1];
-            q.kq = t.KQ;
+            q.kq = t.KQ[t.kc];
             if (q.mode != 1) {
               q.uv0_out = t.UV[1 - t.cur];
               t.cur ^= 1;
@@ -582,19 +591,26 @@ int build_context(const stitch_b200_init* in, int device,
         for (int j = 0; j < nseg; ++j) {
           Op op{OP_HS};
           op.sweeps = seg_len[j];
-          op.fuse = (fuse && j == 0) ? 1 : 0;
+          op.fuse = (fuse && j == 0 && !lin_done) ? 1
+                    : (elin && j == nseg - 1 && it < 4) ? 2
+                                                         : 0;
           op.offset = static_cast<int>(hs_table.size());
           for (auto& t : tasks) {
             if (l >= t.L) continue;
             const PairDesc& p = g.pairs[t.k];
             const int sa = t.dir == 0 ? 0 : 1, sb = 1 - sa;
             HsTask h{};
-            h.kq = t.KQ;
+            h.kq = t.KQ[t.kc];
             h.uv_in = t.UV[t.cur];
             h.uv_out = t.UV[1 - t.cur];
             h.w = t.dims[l][0];
             h.h = t.dims[l][1];
-            if (op.fuse) {
+            if (op.fuse == 2) {
+              h.lin_a = p.pyr[sa][l];
+              h.lin_b = p.pyr[sb][l];
+              h.kq_next = t.KQ[1 - t.kc];
+              t.kc ^= 1;
+            } else if (op.fuse == 1) {
               h.lin_a = p.pyr[sa][l];
               h.lin_b = p.pyr[sb][l];
               h.lin_mode = lin_mode(t);

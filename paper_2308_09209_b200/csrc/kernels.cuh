@@ -162,6 +162,9 @@ struct HsTask {
   const float* lin_b;
   int lin_mode;  // 0: u0 = 0, 1: u0 = uv_in, 2: uv_in upsampled from wc x hc
   int wc, hc;
+  // epilogue linearisation (last segment of a warp iteration): the next warp
+  // iteration's constants, from lin_a / lin_b and this segment's result
+  float4* kq_next;
 };
 
 struct PyrTask {
@@ -209,7 +212,9 @@ int hs_segments(int sweeps);
 cudaError_t prepare_hs(int sweeps);
 void launch_hs_prepare(const PrepTask* tasks, int n, int max_w, int max_h, float alpha2,
                        cudaStream_t s);
-// fuse_lin: the segment first linearises the warp (HsTask lin_* fields)
+// fuse_lin: 0 plain segment; 1 the segment first linearises the warp
+// iteration (HsTask lin_* fields); 2 the segment also linearises the next
+// warp iteration on its output tile (HsTask lin_a, lin_b, kq_next)
 void launch_hs_iter(const HsTask* tasks, int n, int max_w, int max_h, int sweeps, int fuse_lin,
                     float alpha2, cudaStream_t s);
 // the fused linearisation serves segments of up to this many sweeps
@@ -217,6 +222,9 @@ int hs_fuse_max_sweeps();
 // whether the first segment of a warp iteration with these dimensions should
 // fuse the linearisation (the launch it would use supports and profits from it)
 int hs_fuse_wanted(int n, int max_w, int max_h, int sweeps);
+// whether a warp iteration's last segment (`sweeps` long) should linearise
+// the next warp iteration in its epilogue
+int hs_elin_wanted(int n, int max_w, int max_h, int sweeps);
 // mode 0: whole canvas; 1: outside every pair's bounds (flow-independent);
 // 2: inside the bounds.  Modes 1 + 2 together cover the canvas once.
 void launch_canvas(const CanvasParams& P, const Geometry* g, DevState* st, uchar4* pano,
