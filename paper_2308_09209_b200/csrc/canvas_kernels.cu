@@ -335,7 +335,19 @@ __global__ void __launch_bounds__(256, kCanvasCtasPerSm) k_canvas(const __grid_c
     const int y = ty * 4 + threadIdx.x / 64;
     if (x >= cw || y >= ch) continue;
     const long long idx = static_cast<long long>(y) * cw + x;
-    const uchar4 pv = canvas_pixel<CYL>(P, mview, x, y);
+    uchar4 pv;
+    const std::uint8_t c = P.cls ? P.cls[idx] : kClassFold;
+    if (c == kClassFold) {
+      pv = canvas_pixel<CYL>(P, mview, x, y);
+    } else if (c == kClassNone) {
+      pv = make_uchar4(0, 0, 0, 0);
+    } else {
+      // a single view provides the pixel: its warp, colour-corrected unless
+      // it is the reference (the fold's result, without evaluating the
+      // views that do not cover the pixel)
+      pv = warp_cv<CYL>(P.views[c], canvas_lift<CYL>(P, x, y));
+      if (c != P.ref) pv = apply_matrix(mview[c], pv);
+    }
     pano[idx] = pv;
     if (pv.w) {
       atomicAdd(&hist[0][pv.x], 1u);
@@ -433,6 +445,24 @@ __global__ void __launch_bounds__(256) k_warp_view(const Geometry* __restrict__ 
 // Geometry-only validity of the warp (the input frames are unmasked, so the
 // mask does not depend on pixel values): sample_bilinear is valid iff a
 // neighbour with positive weight lies inside the frame.
+template <bool CYL>
+__device__ __forceinline__ bool warp_valid(const double* inv, int W, int H, Lift L) {
+  double sx0, sy0, sz0;
+  warp_point<CYL>(inv, L, sx0, sy0, sz0);
+  if (fabs(sz0) < 1e-12 || (CYL && !(sz0 > 0.0))) return false;
+  const double sx = sx0 / sz0, sy = sy0 / sz0;
+  const double fx0 = floor(sx), fy0 = floor(sy);
+  const int x0 = static_cast<int>(fx0), y0 = static_cast<int>(fy0);
+  const double ax = sx - fx0, ay = sy - fy0;
+  for (int j = 0; j < 2; ++j)
+    for (int i = 0; i < 2; ++i) {
+      const double w = (i ? ax : 1.0 - ax) * (j ? ay : 1.0 - ay);
+      const unsigned xx = static_cast<unsigned>(x0) + i, yy = static_cast<unsigned>(y0) + j;
+      if (w > 0.0 && xx < static_cast<unsigned>(W) && yy < static_cast<unsigned>(H)) return true;
+    }
+  return false;
+}
+
 __global__ void __launch_bounds__(256) k_warp_mask(const Geometry* __restrict__ g, int view,
                                                    std::uint8_t* __restrict__ mask) {
   const ViewDesc& v = g->views[view];
@@ -441,26 +471,40 @@ __global__ void __launch_bounds__(256) k_warp_mask(const Geometry* __restrict__ 
        idx += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int y = static_cast<int>(idx / g->canvas_w);
     const int x = static_cast<int>(idx - static_cast<long long>(y) * g->canvas_w);
-    double sx0, sy0, sz0;
-    if (g->projection == 1)
-      warp_point<true>(v.inv, canvas_lift<true>(*g, x, y), sx0, sy0, sz0);
-    else
-      warp_point<false>(v.inv, canvas_lift<false>(*g, x, y), sx0, sy0, sz0);
-    unsigned char ok = 0;
-    if (!(fabs(sz0) < 1e-12) && (g->projection != 1 || sz0 > 0.0)) {
-      const double sx = sx0 / sz0, sy = sy0 / sz0;
-      const double fx0 = floor(sx), fy0 = floor(sy);
-      const int x0 = static_cast<int>(fx0), y0 = static_cast<int>(fy0);
-      const double ax = sx - fx0, ay = sy - fy0;
-      for (int j = 0; j < 2 && !ok; ++j)
-        for (int i = 0; i < 2 && !ok; ++i) {
-          const double w = (i ? ax : 1.0 - ax) * (j ? ay : 1.0 - ay);
-          const unsigned xx = static_cast<unsigned>(x0) + i, yy = static_cast<unsigned>(y0) + j;
-          if (w > 0.0 && xx < static_cast<unsigned>(v.width) && yy < static_cast<unsigned>(v.height))
-            ok = 1;
-        }
+    mask[idx] = g->projection == 1
+                    ? warp_valid<true>(v.inv, v.width, v.height, canvas_lift<true>(*g, x, y))
+                    : warp_valid<false>(v.inv, v.width, v.height, canvas_lift<false>(*g, x, y));
+  }
+}
+
+// Canvas class map (CanvasParams::cls): outside every pair's bounds the
+// compose fold (pipeline.cpp:326-333, flow.cpp:324-357) keeps the warped
+// reference where it is valid, else takes the first valid view of the pairs
+// in order (colour-corrected); validity is geometry-only, so which view that
+// is depends on the maps alone and is fixed per context.
+template <bool CYL>
+__global__ void __launch_bounds__(256) k_canvas_class(const __grid_constant__ CanvasParams P,
+                                                      std::uint8_t* __restrict__ cls) {
+  const long long n = static_cast<long long>(P.cw) * P.ch;
+  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < n;
+       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int y = static_cast<int>(idx / P.cw);
+    const int x = static_cast<int>(idx - static_cast<long long>(y) * P.cw);
+    std::uint8_t c = kClassNone;
+    bool fold = false;
+    for (int k = 0; k < P.np; ++k) fold = fold || in_rect(P.pairs[k], x, y);
+    if (fold) {
+      c = kClassFold;
+    } else {
+      const Lift L = canvas_lift<CYL>(P, x, y);
+      for (int k = -1; k < P.np && c == kClassNone; ++k) {
+        const int v = k < 0 ? P.ref : P.pairs[k].view;
+        const CanvasView& vv = P.views[v];
+        if (may_cover(vv, x, y) && warp_valid<CYL>(vv.inv, vv.w, vv.h, L))
+          c = static_cast<std::uint8_t>(v);
+      }
     }
-    mask[idx] = ok;
+    cls[idx] = c;
   }
 }
 
@@ -512,6 +556,13 @@ void launch_warp_view(const Geometry* g, int view, const uchar4* frame, std::uin
 
 void launch_warp_mask(const Geometry* g, int view, std::uint8_t* mask, cudaStream_t s) {
   k_warp_mask<<<148 * 8, 256, 0, s>>>(g, view, mask);
+}
+
+void launch_canvas_class(const CanvasParams& P, std::uint8_t* cls, cudaStream_t s) {
+  if (P.projection == 1)
+    k_canvas_class<true><<<148 * 8, 256, 0, s>>>(P, cls);
+  else
+    k_canvas_class<false><<<148 * 8, 256, 0, s>>>(P, cls);
 }
 
 }  // namespace stitch_b200_dev

@@ -715,6 +715,18 @@ int build_context(const stitch_b200_init* in, int device,
     }
   }
   ctx->hg = ctx->slot[0].hg;
+  {
+    // canvas class map (geometry only): shared by the slots
+    const char* e = getenv("STITCH_B200_CANVAS_CLASS");
+    if (!e || atoi(e) != 0) {
+      std::uint8_t* cls = nullptr;
+      CUDA_TRY(ctx->alloc(&cls, static_cast<size_t>(ctx->n_px)));
+      launch_canvas_class(ctx->slot[0].cparams, cls, ctx->stream);
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+      for (int sl = 0; sl < Ctx::kSlots; ++sl) ctx->slot[sl].cparams.cls = cls;
+    }
+  }
   CUDA_TRY(prepare_hs(ctx->sweeps));
   for (int j = 1; j <= ctx->sweeps; ++j) CUDA_TRY(prepare_hs(j));
   for (int sl = 0; sl < Ctx::kSlots; ++sl) {

@@ -147,7 +147,13 @@ struct CanvasParams {
   const double* lift_h;
   CanvasView views[kMaxViews];
   CanvasPair pairs[kMaxPairs];
+  // per canvas pixel, from the geometry alone (k_canvas_class): the view the
+  // compose fold takes the pixel from when it lies outside every pair's
+  // bounds, kClassFold inside some pair's bounds, kClassNone if no view
+  // covers it; nullptr = evaluate the fold everywhere
+  const std::uint8_t* cls;
 };
+constexpr std::uint8_t kClassFold = 254, kClassNone = 255;
 
 struct HsTask {
   float4* kq;  // Jacobi constants (gx, gy, c, denom) per pixel: read by plain
@@ -235,6 +241,8 @@ void launch_warp_view(const Geometry* g, int view, const uchar4* frame, std::uin
                       std::uint8_t* mask, cudaStream_t s);
 void launch_expand_one(const std::uint8_t* rgb, uchar4* rgba, long long n_px, cudaStream_t s);
 void launch_warp_mask(const Geometry* g, int view, std::uint8_t* mask, cudaStream_t s);
+// the canvas class map of CanvasParams::cls (init time, geometry only)
+void launch_canvas_class(const CanvasParams& P, std::uint8_t* cls, cudaStream_t s);
 
 // ---- feature refinement image work (features_kernels.cu) ----
 struct FeatPoint {
