@@ -315,6 +315,47 @@ int stitch_b200_profile_frame(stitch_b200_ctx* ctx,
                               const uint8_t* const* dev_frames, int max_ops,
                               int* kinds, float* ms);
 
+/* ---- frame ingress / egress ----
+ * PPM (P6, maxval 255) I/O, replacing read_ppm / write_ppm
+ * (proj/src/image_io.cpp:61-85, header tokens with '#' comments as
+ * read_ppm_token :19-37); failures return IoError like the reference's
+ * StitchError(IoError).  read_ppm writes the raster into rgb (capacity
+ * bytes, e.g. a pinned buffer) and the size into width/height; rgb == NULL
+ * reads the header only.  PNG needs libpng, which this build does not have. */
+int stitch_b200_ppm_info(const char* path, int* width, int* height);
+int stitch_b200_read_ppm(const char* path, uint8_t* rgb, size_t capacity, int* width,
+                         int* height);
+int stitch_b200_write_ppm(const char* path, int width, int height, const uint8_t* rgb);
+/* sequence_name (image_io.cpp:194-199): stem + "_%06d" + ext into out. */
+int stitch_b200_sequence_name(const char* stem, int index, const char* ext, char* out,
+                              size_t capacity);
+
+typedef struct {
+  long long frames;     /* panoramas written */
+  double seconds;       /* wall time of the whole run */
+  double read_seconds;  /* summed per-file read time (reader threads) */
+  double write_seconds; /* summed per-file write time (writer threads) */
+} stitch_b200_files_stats;
+
+/* run_sequence (pipeline.hpp:90-92, pipeline.cpp:364-412) with file sources
+ * and sink: view_dirs[v] holds view v's numbered PPM sequence (list_sequence,
+ * image_io.cpp:181-192: the .ppm files sorted by name); frame t of every view
+ * is stitched in order and the panorama written to
+ * out_dir/<stem>_%06d.ppm (out_dir NULL: not written).  One reader thread per
+ * view reads straight into pinned staging, frames run four in flight through
+ * stitch_b200_submit / stitch_b200_wait, four writer threads encode the
+ * panoramas.  max_frames <= 0: every frame present in all views.  reports
+ * (optional) receives one FrameReport per frame. */
+int stitch_b200_run_files(stitch_b200_ctx* ctx, const char* const* view_dirs,
+                          const char* out_dir, const char* stem, int max_frames,
+                          stitch_b200_report* reports, stitch_b200_files_stats* stats);
+
+/* Number of views / a view's camera size of a context. */
+int stitch_b200_n_views(const stitch_b200_ctx* ctx);
+int stitch_b200_view_size(const stitch_b200_ctx* ctx, int view, int* width, int* height);
+/* Set the calling thread's last error; returns code. */
+int stitch_b200_set_error(int code, const char* what);
+
 /* Pinned host memory helpers (cudaHostAlloc / cudaFreeHost). */
 void* stitch_b200_host_alloc(size_t bytes);
 void stitch_b200_host_free(void* p);

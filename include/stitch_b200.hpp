@@ -384,4 +384,75 @@ inline RunResult run_sequence(const StitchConfig& config, const std::vector<std:
   return result;
 }
 
+// ---- image_io.hpp (image_io.cpp:61-199), PPM only (no libpng here) ----
+inline Frame read_ppm(const std::string& path) {
+  int w = 0, h = 0;
+  check(stitch_b200_read_ppm(path.c_str(), nullptr, 0, &w, &h));
+  Frame f(w, h);
+  check(stitch_b200_read_ppm(path.c_str(), f.data.data(), f.data.size(), nullptr, nullptr));
+  return f;
+}
+
+inline void write_ppm(const std::string& path, const Frame& frame) {
+  if (frame.data.size() != frame.pixel_count() * 3)
+    throw StitchError(ErrorCode::InputMismatch, "frame data must be width*height*3 bytes");
+  check(stitch_b200_write_ppm(path.c_str(), frame.width, frame.height, frame.data.data()));
+}
+
+inline std::string sequence_name(const std::string& stem, int index,
+                                 const std::string& ext = ".png") {
+  std::vector<char> buf(stem.size() + ext.size() + 32);
+  check(stitch_b200_sequence_name(stem.c_str(), index, ext.c_str(), buf.data(), buf.size()));
+  return std::string(buf.data());
+}
+
+struct FilesRunResult {
+  std::vector<FrameReport> per_frame;
+  long frames = 0;
+  double wall_seconds = 0.0, read_seconds = 0.0, write_seconds = 0.0;
+  double fps() const { return wall_seconds > 0 ? frames / wall_seconds : 0.0; }
+};
+
+// run_sequence over numbered PPM sequences (one directory per view) with the
+// panoramas written to out_dir/<stem>_%06d.ppm (empty out_dir: not written);
+// reads, GPU frames and writes overlap inside the library.
+inline FilesRunResult run_files(PipelineState& state, const std::vector<std::string>& view_dirs,
+                                const std::string& out_dir = {}, const std::string& stem = "pano",
+                                int max_frames = 0) {
+  std::vector<const char*> dirs;
+  for (const auto& d : view_dirs) dirs.push_back(d.c_str());
+  if (static_cast<int>(dirs.size()) != stitch_b200_n_views(state.handle()))
+    throw StitchError(ErrorCode::InputMismatch, "one directory per view");
+  std::vector<stitch_b200_report> reps;
+  stitch_b200_files_stats st{};
+  // reports are collected only for a bounded run (max_frames > 0)
+  if (max_frames > 0) reps.resize(static_cast<std::size_t>(max_frames));
+  check(stitch_b200_run_files(state.handle(), dirs.data(), out_dir.empty() ? nullptr : out_dir.c_str(),
+                              stem.c_str(), max_frames, reps.empty() ? nullptr : reps.data(), &st));
+  FilesRunResult res;
+  res.frames = static_cast<long>(st.frames);
+  res.wall_seconds = st.seconds;
+  res.read_seconds = st.read_seconds;
+  res.write_seconds = st.write_seconds;
+  for (long t = 0; t < res.frames && !reps.empty(); ++t) {
+    const stitch_b200_report& r = reps[static_cast<std::size_t>(t)];
+    FrameReport rep;
+    rep.frame_index = static_cast<long>(r.frame_index);
+    for (int i = 0; i < kStageCount; ++i) rep.times.seconds[i] = r.stage_ms[i] * 1e-3;
+    for (int k = 0; k < r.n_pairs; ++k) {
+      Matrix3d m;
+      for (int i = 0; i < 9; ++i) m[i] = r.color_matrices[k][i];
+      rep.color_matrices.push_back(m);
+      rep.rank_deficient.push_back(r.rank_deficient[k] != 0);
+    }
+    for (int c = 0; c < 3; ++c) {
+      rep.threshold_m1[c] = r.threshold_m1[c];
+      rep.threshold_m2[c] = r.threshold_m2[c];
+    }
+    res.per_frame.push_back(rep);
+  }
+  state.frame_counter += res.frames;
+  return res;
+}
+
 }  // namespace stitch_b200

@@ -36,6 +36,12 @@ from .pipeline import (  # noqa: F401
     initialize,
     process_frame,
     run_sequence,
+    read_ppm,
+    write_ppm,
+    sequence_name,
+    list_sequence,
+    run_files,
+    FilesResult,
 )
 
 lib = _abi.load()

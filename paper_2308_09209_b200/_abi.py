@@ -73,6 +73,11 @@ class SynthSpec(C.Structure):
                 ("strip_yaw", C.c_double)]
 
 
+class FilesStats(C.Structure):
+    _fields_ = [("frames", C.c_longlong), ("seconds", C.c_double),
+                ("read_seconds", C.c_double), ("write_seconds", C.c_double)]
+
+
 # exported symbols (name, restype, argtypes) -- every declaration of the header
 SYMBOLS = [
     ("stitch_b200_last_error", C.c_char_p, []),
@@ -120,6 +125,18 @@ SYMBOLS = [
     ("stitch_b200_launches_per_frame", C.c_int, [C.c_void_p]),
     ("stitch_b200_profile_frame", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.c_int,
                                             C.POINTER(C.c_int), C.POINTER(C.c_float)]),
+    ("stitch_b200_ppm_info", C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    ("stitch_b200_read_ppm", C.c_int, [C.c_char_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_int),
+                                       C.POINTER(C.c_int)]),
+    ("stitch_b200_write_ppm", C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_void_p]),
+    ("stitch_b200_sequence_name", C.c_int, [C.c_char_p, C.c_int, C.c_char_p, C.c_char_p,
+                                            C.c_size_t]),
+    ("stitch_b200_run_files", C.c_int, [C.c_void_p, C.POINTER(C.c_char_p), C.c_char_p,
+                                        C.c_char_p, C.c_int, C.c_void_p, C.POINTER(FilesStats)]),
+    ("stitch_b200_n_views", C.c_int, [C.c_void_p]),
+    ("stitch_b200_view_size", C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int),
+                                        C.POINTER(C.c_int)]),
+    ("stitch_b200_set_error", C.c_int, [C.c_int, C.c_char_p]),
     ("stitch_b200_host_alloc", C.c_void_p, [C.c_size_t]),
     ("stitch_b200_host_free", None, [C.c_void_p]),
     ("stitch_b200_device_alloc", C.c_void_p, [C.c_int, C.c_size_t]),

@@ -1365,6 +1365,19 @@ int stitch_b200_canvas(const stitch_b200_ctx* hd, int* w, int* h, double* ox, do
 
 int stitch_b200_n_pairs(const stitch_b200_ctx* h) { return h->c->hg.n_pairs; }
 
+int stitch_b200_n_views(const stitch_b200_ctx* h) { return h->c->hg.n_views; }
+
+int stitch_b200_view_size(const stitch_b200_ctx* h, int view, int* width, int* height) {
+  const Ctx* ctx = h->c.get();
+  if (view < 0 || view >= ctx->hg.n_views)
+    return fail(STITCH_B200_InputMismatch, "view index out of range");
+  if (width) *width = ctx->hg.views[view].width;
+  if (height) *height = ctx->hg.views[view].height;
+  return STITCH_B200_OK;
+}
+
+int stitch_b200_set_error(int code, const char* what) { return fail(code, what ? what : ""); }
+
 int stitch_b200_get_pair(const stitch_b200_ctx* h, int k, stitch_b200_pair* pair,
                          float* theta_out) {
   const Ctx* ctx = h->c.get();

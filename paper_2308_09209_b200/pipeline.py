@@ -527,6 +527,79 @@ def run_sequence(config: StitchConfig, views: Sequence[Sequence[Frame]],
 
 
 # ---------------------------------------------------------------------------
+# Frame ingress / egress (image_io.hpp / image_io.cpp:19-199)
+# ---------------------------------------------------------------------------
+def read_ppm(path) -> Frame:
+    """read_ppm (image_io.cpp:61-76): P6, maxval 255; IoError otherwise."""
+    lib = _lib()
+    p = str(path).encode()
+    w, h = C.c_int(), C.c_int()
+    check(lib.stitch_b200_read_ppm(p, None, 0, C.byref(w), C.byref(h)))
+    data = np.empty((h.value, w.value, 3), np.uint8)
+    check(lib.stitch_b200_read_ppm(p, data.ctypes.data_as(C.c_void_p), data.nbytes, None, None))
+    return Frame(data)
+
+
+def write_ppm(path, frame: Frame) -> None:
+    """write_ppm (image_io.cpp:78-85); the mask is not stored (PPM is RGB)."""
+    data = np.ascontiguousarray(frame.data, dtype=np.uint8)
+    check(_lib().stitch_b200_write_ppm(str(path).encode(), frame.width, frame.height,
+                                       data.ctypes.data_as(C.c_void_p)))
+
+
+def sequence_name(stem: str, index: int, ext: str = ".png") -> str:
+    """sequence_name (image_io.cpp:194-199): stem_000003.png."""
+    buf = C.create_string_buffer(len(stem) + len(ext) + 32)
+    check(_lib().stitch_b200_sequence_name(stem.encode(), index, ext.encode(), buf, len(buf)))
+    return buf.value.decode()
+
+
+def list_sequence(directory) -> List[str]:
+    """list_sequence (image_io.cpp:181-192): the .png / .ppm regular files of
+    a directory, sorted by name; IoError when it is not a directory."""
+    import os
+
+    d = str(directory)
+    if not os.path.isdir(d):
+        raise StitchError(ErrorCode.IoError + 1, f"{d}: not a directory")
+    return sorted(os.path.join(d, f) for f in os.listdir(d)
+                  if os.path.isfile(os.path.join(d, f)) and os.path.splitext(f)[1] in (".png", ".ppm"))
+
+
+@dataclass
+class FilesResult:
+    reports: List[FrameReport]
+    frames: int
+    seconds: float
+    read_seconds: float
+    write_seconds: float
+
+    def fps(self) -> float:
+        return self.frames / self.seconds if self.seconds > 0 else 0.0
+
+
+def run_files(state: PipelineState, view_dirs: Sequence[str], out_dir: Optional[str] = None,
+              stem: str = "pano", max_frames: int = 0) -> FilesResult:
+    """run_sequence (pipeline.cpp:364-412) on numbered PPM sequences, one
+    directory per view, panoramas written as out_dir/stem_%06d.ppm; file
+    reads, the pipelined GPU frames and the writes overlap (C++ threads in
+    libstitch_b200.so)."""
+    lib = _lib()
+    n = lib.stitch_b200_n_views(state.handle)
+    if len(view_dirs) != n:
+        raise StitchError(ErrorCode.InputMismatch + 1, "one directory per view")
+    dirs = (C.c_char_p * n)(*[str(d).encode() for d in view_dirs])
+    cap = max_frames if max_frames > 0 else min(
+        len([f for f in list_sequence(d) if f.endswith(".ppm")]) for d in view_dirs)
+    reps = (_abi.Report * max(1, cap))()
+    st = _abi.FilesStats()
+    check(lib.stitch_b200_run_files(state.handle, dirs, str(out_dir).encode() if out_dir else None,
+                                    stem.encode(), cap, reps, C.byref(st)))
+    return FilesResult([_report_from_c(reps[i]) for i in range(st.frames)], st.frames,
+                       st.seconds, st.read_seconds, st.write_seconds)
+
+
+# ---------------------------------------------------------------------------
 # Synthetic scenes (synth.hpp:17-87)
 # ---------------------------------------------------------------------------
 @dataclass

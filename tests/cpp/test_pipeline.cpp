@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "../../oracle/stitch_oracle.h"
@@ -239,12 +240,57 @@ TEST_CASE(update_maps_keeps_geometry_for_unchanged_maps) {
   stitch_b200_synth_destroy(s);
 }
 
+TEST_CASE(run_files_writes_the_process_frame_panoramas) {
+  // image_io PPM sequences in, PPM panoramas out (run_files) == process_frame
+  stitch_b200_synth* s = make_scene(2, 160, 120);
+  stitch_b200_config c;
+  StitchConfig cfg = config_of(s, c);
+  char tmpl[] = "/tmp/stitch_b200_cpp_XXXXXX";
+  const std::string root = mkdtemp(tmpl);
+  std::vector<std::string> dirs;
+  std::vector<std::vector<Frame>> frames(4);
+  for (int v = 0; v < 2; ++v) {
+    dirs.push_back(root + "/view" + std::to_string(v));
+    CHECK(std::system(("mkdir -p " + dirs.back()).c_str()) == 0);
+    for (int t = 0; t < 4; ++t) {
+      Frame f(160, 120);
+      check(stitch_b200_synth_render(s, v, t, f.data.data(), 4));
+      write_ppm(dirs.back() + "/" + sequence_name("cam", t, ".ppm"), f);
+      Frame back = read_ppm(dirs.back() + "/" + sequence_name("cam", t, ".ppm"));
+      CHECK(back.width == 160 && back.height == 120 && back.data == f.data);
+      frames[t].push_back(f);
+    }
+  }
+  PipelineState a = initialize(cfg, frames[0]);
+  FilesRunResult fr = run_files(a, dirs, root + "/out", "pano", 4);
+  CHECK(fr.frames == 4);
+  CHECK(fr.per_frame.size() == 4);
+  PipelineState b = initialize(cfg, frames[0]);
+  for (int t = 0; t < 4; ++t) {
+    ProcessResult pr = process_frame(b, frames[t]);
+    Frame got = read_ppm(root + "/out/" + sequence_name("pano", t, ".ppm"));
+    CHECK(got.data == pr.panorama.data);
+    CHECK(fr.per_frame[t].frame_index == t);
+    CHECK(fr.per_frame[t].color_matrices == pr.report.color_matrices);
+  }
+  bool threw = false;
+  try {
+    read_ppm(root + "/missing.ppm");
+  } catch (const StitchError& e) {
+    threw = e.code() == ErrorCode::IoError;
+  }
+  CHECK(threw);
+  CHECK(std::system(("rm -rf " + root).c_str()) == 0);
+  stitch_b200_synth_destroy(s);
+}
+
 int main() {
   process_frame_matches_oracle();
   errors_surface_as_stitch_error();
   run_sequence_reports_every_frame();
   quality_metrics_match_oracle();
   update_maps_keeps_geometry_for_unchanged_maps();
+  run_files_writes_the_process_frame_panoramas();
   std::printf("%d checks, %d failures\n", g_checks, g_failures);
   return g_failures ? 1 : 0;
 }
