@@ -177,6 +177,7 @@ def kernel_model(state, wl, sweeps=10, warps=5, lin_levels=None):
     fused_px = flow_px - lin_px
     coarse_px = 2 * sum(a * b for dims in lv for a, b in dims[:-1])  # finer levels (upsampled u0)
     segs = int(os.environ.get("STITCH_B200_HS_SEGS", "2"))
+    elin = os.environ.get("STITCH_B200_HS_ELIN", "1") != "0"
     return {
         # RGB8 read, RGBA8 write
         "expand_rgba": dict(bytes=7 * in_px),
@@ -189,9 +190,14 @@ def kernel_model(state, wl, sweeps=10, warps=5, lin_levels=None):
         # per warp iteration and pixel: u0 (8) + a (4) + b (4) read, 4 constant planes
         # (16) written; + u0 materialised (8) on each level's first warp
         "hs_linearize": dict(bytes=warps * 32 * lin_px + 8 * lin_px),
-        # per segment and pixel: state (8) + constants (16) read, state (8) written; a
-        # fused first segment reads u0 (8) + a, b (8), writes constants (16) + state (8)
-        "hs_sweeps": dict(bytes=warps * segs * 32 * flow_px + warps * 8 * fused_px,
+        # per segment and pixel: state (8) + constants (16) read, state (8) written.
+        # On the fused (coarse) levels the first warp iteration's first segment
+        # linearises in its prologue (+8: a, b read; constants written instead of
+        # read), and the last segment of warp iterations 1-4 linearises the next
+        # one in its epilogue (+24: a, b read, next constants written); with
+        # STITCH_B200_HS_ELIN=0 every warp iteration uses the prologue
+        "hs_sweeps": dict(bytes=warps * segs * 32 * flow_px + (
+            (8 + 24 * (warps - 1)) * fused_px if elin else warps * 8 * fused_px),
                           flops=warps * sweeps * 17 * flow_px),
         # per canvas pixel one RGBA source pixel read + uchar4 write; overlap pixels add
         # raw crops (8) + corrected crop samples (8) + flows (16) + weight (4)
