@@ -538,9 +538,6 @@ int build_context(const stitch_b200_init* in, int device,
     // own; from the second warp iteration on, the previous iteration's last
     // segment linearises it in its epilogue where that is wanted
     // (hs_elin_wanted; the constants then ping-pong between two planes).
-    const int nseg = hs_segments(ctx->sweeps);
-    std::vector<int> seg_len(nseg, ctx->sweeps / nseg);
-    for (int j = 0; j < ctx->sweeps % nseg; ++j) seg_len[j]++;
     for (int l = Lmax - 1; l >= 0; --l) {
       int n_l = 0, w_l = 0, h_l = 0;
       for (const auto& t : tasks)
@@ -549,6 +546,9 @@ int build_context(const stitch_b200_init* in, int device,
           w_l = std::max(w_l, t.dims[l][0]);
           h_l = std::max(h_l, t.dims[l][1]);
         }
+      const std::vector<int> seg_len =
+          n_l > 0 ? hs_split(n_l, w_l, h_l, ctx->sweeps) : std::vector<int>(1, ctx->sweeps);
+      const int nseg = static_cast<int>(seg_len.size());
       const bool fuse = n_l > 0 && hs_fuse_wanted(n_l, w_l, h_l, seg_len[0]);
       // (a single segment cannot carry both a prologue and an epilogue)
       const bool elin = n_l > 0 && hs_elin_wanted(n_l, w_l, h_l, seg_len[nseg - 1]) &&

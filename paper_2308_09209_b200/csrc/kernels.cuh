@@ -215,6 +215,8 @@ void launch_pyr_down(const PyrTask* tasks, int n, int max_px, cudaStream_t s);
 size_t hs_smem_bytes(int sweeps);
 // how many launches (sweep segments) one warp iteration of `sweeps` uses
 int hs_segments(int sweeps);
+// segment lengths of one warp iteration at a level (tasks n, max w x h)
+std::vector<int> hs_split(int n, int max_w, int max_h, int sweeps);
 cudaError_t prepare_hs(int sweeps);
 void launch_hs_prepare(const PrepTask* tasks, int n, int max_w, int max_h, float alpha2,
                        cudaStream_t s);
