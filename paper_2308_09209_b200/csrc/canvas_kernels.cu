@@ -329,10 +329,21 @@ __global__ void __launch_bounds__(256, kCanvasCtasPerSm) k_canvas(const __grid_c
   const int cw = P.cw, ch = P.ch;
   const int tiles_x = (cw + 63) / 64;
   const int ntiles = tiles_x * ((ch + 3) / 4);
+  // tile -> (column, row) kept incrementally: the grid stride advances by
+  // (dq rows, dr columns), one integer division per thread instead of one
+  // per tile
+  const int dq = static_cast<int>(gridDim.x) / tiles_x, dr = static_cast<int>(gridDim.x) - dq * tiles_x;
+  int ty = static_cast<int>(blockIdx.x) / tiles_x;
+  int tcol = static_cast<int>(blockIdx.x) - ty * tiles_x;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int ty = tile / tiles_x;
-    const int x = (tile - ty * tiles_x) * 64 + threadIdx.x % 64;
+    const int x = tcol * 64 + threadIdx.x % 64;
     const int y = ty * 4 + threadIdx.x / 64;
+    tcol += dr;
+    ty += dq;
+    if (tcol >= tiles_x) {
+      tcol -= tiles_x;
+      ++ty;
+    }
     if (x >= cw || y >= ch) continue;
     const long long idx = static_cast<long long>(y) * cw + x;
     uchar4 pv;
