@@ -411,6 +411,18 @@ def test_eight_view_chain_parity():
         check_frame(state, ost, frames_at(sc, t), t)
 
 
+def test_sixteen_view_chain_parity():
+    """The maximum view count (STITCH_B200_MAX_VIEWS = 16, 15 chain pairs,
+    colour-correction depth 8) at small frames, bit-exact vs the oracle."""
+    casts = [(1.0 - 0.02 * v, 1.0, 1.0 + 0.015 * v) for v in range(16)]
+    sc = scene(views=16, width=128, height=96, frames=2, focal_scale=1.02, casts=casts)
+    state, ost = make_pair(sc)
+    check_geometry(state, ost, 16)
+    assert len(state.pairs) == 15
+    for t in range(2):
+        check_frame(state, ost, frames_at(sc, t), t)
+
+
 def test_ring_360_parity():
     """BASELINE config 3 topology: 6-camera 360-degree ring on a cylindrical
     canvas (extension: lift tables, ring-chain pairs, the opposite view
