@@ -326,6 +326,17 @@ int stitch_b200_ppm_info(const char* path, int* width, int* height);
 int stitch_b200_read_ppm(const char* path, uint8_t* rgb, size_t capacity, int* width,
                          int* height);
 int stitch_b200_write_ppm(const char* path, int width, int height, const uint8_t* rgb);
+/* PNG, replacing read_png / write_png (image_io.cpp:87-165), on zlib (libpng
+ * is not in this image).  Read: palette / grey / 16-bit expanded to 8-bit RGB
+ * as libpng's expand + strip_16 + gray_to_rgb; alpha 0 (or tRNS) marks the
+ * pixel invalid.  rgb (capacity bytes) and mask (mask_capacity bytes, 0/1,
+ * all 1 without transparency) may be NULL to query the size; has_mask = 1
+ * when some pixel is transparent.  Interlaced files are an IoError.  Write:
+ * 8-bit RGB, or RGBA with alpha 255 / 0 from mask when mask != NULL. */
+int stitch_b200_read_png(const char* path, uint8_t* rgb, size_t capacity, uint8_t* mask,
+                         size_t mask_capacity, int* width, int* height, int* has_mask);
+int stitch_b200_write_png(const char* path, int width, int height, const uint8_t* rgb,
+                          const uint8_t* mask);
 /* sequence_name (image_io.cpp:194-199): stem + "_%06d" + ext into out. */
 int stitch_b200_sequence_name(const char* stem, int index, const char* ext, char* out,
                               size_t capacity);
@@ -338,16 +349,18 @@ typedef struct {
 } stitch_b200_files_stats;
 
 /* run_sequence (pipeline.hpp:90-92, pipeline.cpp:364-412) with file sources
- * and sink: view_dirs[v] holds view v's numbered PPM sequence (list_sequence,
- * image_io.cpp:181-192: the .ppm files sorted by name); frame t of every view
- * is stitched in order and the panorama written to
- * out_dir/<stem>_%06d.ppm (out_dir NULL: not written).  One reader thread per
+ * and sink: view_dirs[v] holds view v's numbered image sequence
+ * (list_sequence, image_io.cpp:181-192: the .ppm / .png files sorted by name;
+ * inputs must be unmasked, a transparent PNG pixel is an InputMismatch);
+ * frame t of every view is stitched in order and the panorama written to
+ * out_dir/<stem>_%06d<ext> (ext ".ppm" (NULL) or ".png" with the mask as
+ * alpha; out_dir NULL: not written).  One reader thread per
  * view reads straight into pinned staging, frames run four in flight through
  * stitch_b200_submit / stitch_b200_wait, four writer threads encode the
  * panoramas.  max_frames <= 0: every frame present in all views.  reports
  * (optional) receives one FrameReport per frame. */
 int stitch_b200_run_files(stitch_b200_ctx* ctx, const char* const* view_dirs,
-                          const char* out_dir, const char* stem, int max_frames,
+                          const char* out_dir, const char* stem, const char* ext, int max_frames,
                           stitch_b200_report* reports, stitch_b200_files_stats* stats);
 
 /* Number of views / a view's camera size of a context. */

@@ -384,7 +384,7 @@ inline RunResult run_sequence(const StitchConfig& config, const std::vector<std:
   return result;
 }
 
-// ---- image_io.hpp (image_io.cpp:61-199), PPM only (no libpng here) ----
+// ---- image_io.hpp (image_io.cpp:61-199); PNG on zlib (no libpng here) ----
 inline Frame read_ppm(const std::string& path) {
   int w = 0, h = 0;
   check(stitch_b200_read_ppm(path.c_str(), nullptr, 0, &w, &h));
@@ -397,6 +397,24 @@ inline void write_ppm(const std::string& path, const Frame& frame) {
   if (frame.data.size() != frame.pixel_count() * 3)
     throw StitchError(ErrorCode::InputMismatch, "frame data must be width*height*3 bytes");
   check(stitch_b200_write_ppm(path.c_str(), frame.width, frame.height, frame.data.data()));
+}
+
+inline Frame read_png(const std::string& path) {
+  int w = 0, h = 0, hm = 0;
+  check(stitch_b200_read_png(path.c_str(), nullptr, 0, nullptr, 0, &w, &h, &hm));
+  Frame f(w, h);
+  std::vector<std::uint8_t> mask(f.pixel_count());
+  check(stitch_b200_read_png(path.c_str(), f.data.data(), f.data.size(), mask.data(), mask.size(),
+                             nullptr, nullptr, nullptr));
+  if (hm) f.mask = std::move(mask);
+  return f;
+}
+
+inline void write_png(const std::string& path, const Frame& frame) {
+  if (frame.data.size() != frame.pixel_count() * 3)
+    throw StitchError(ErrorCode::InputMismatch, "frame data must be width*height*3 bytes");
+  check(stitch_b200_write_png(path.c_str(), frame.width, frame.height, frame.data.data(),
+                              frame.has_mask() ? frame.mask.data() : nullptr));
 }
 
 inline std::string sequence_name(const std::string& stem, int index,
@@ -418,7 +436,7 @@ struct FilesRunResult {
 // reads, GPU frames and writes overlap inside the library.
 inline FilesRunResult run_files(PipelineState& state, const std::vector<std::string>& view_dirs,
                                 const std::string& out_dir = {}, const std::string& stem = "pano",
-                                int max_frames = 0) {
+                                int max_frames = 0, const std::string& ext = ".ppm") {
   std::vector<const char*> dirs;
   for (const auto& d : view_dirs) dirs.push_back(d.c_str());
   if (static_cast<int>(dirs.size()) != stitch_b200_n_views(state.handle()))
@@ -428,7 +446,8 @@ inline FilesRunResult run_files(PipelineState& state, const std::vector<std::str
   // reports are collected only for a bounded run (max_frames > 0)
   if (max_frames > 0) reps.resize(static_cast<std::size_t>(max_frames));
   check(stitch_b200_run_files(state.handle(), dirs.data(), out_dir.empty() ? nullptr : out_dir.c_str(),
-                              stem.c_str(), max_frames, reps.empty() ? nullptr : reps.data(), &st));
+                              stem.c_str(), ext.c_str(), max_frames,
+                              reps.empty() ? nullptr : reps.data(), &st));
   FilesRunResult res;
   res.frames = static_cast<long>(st.frames);
   res.wall_seconds = st.seconds;

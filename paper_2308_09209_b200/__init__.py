@@ -38,6 +38,10 @@ from .pipeline import (  # noqa: F401
     run_sequence,
     read_ppm,
     write_ppm,
+    read_png,
+    write_png,
+    read_image,
+    write_image,
     sequence_name,
     list_sequence,
     run_files,

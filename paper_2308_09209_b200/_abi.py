@@ -132,7 +132,12 @@ SYMBOLS = [
     ("stitch_b200_sequence_name", C.c_int, [C.c_char_p, C.c_int, C.c_char_p, C.c_char_p,
                                             C.c_size_t]),
     ("stitch_b200_run_files", C.c_int, [C.c_void_p, C.POINTER(C.c_char_p), C.c_char_p,
-                                        C.c_char_p, C.c_int, C.c_void_p, C.POINTER(FilesStats)]),
+                                        C.c_char_p, C.c_char_p, C.c_int, C.c_void_p,
+                                        C.POINTER(FilesStats)]),
+    ("stitch_b200_read_png", C.c_int, [C.c_char_p, C.c_void_p, C.c_size_t, C.c_void_p,
+                                       C.c_size_t, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                       C.POINTER(C.c_int)]),
+    ("stitch_b200_write_png", C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
     ("stitch_b200_n_views", C.c_int, [C.c_void_p]),
     ("stitch_b200_view_size", C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int),
                                         C.POINTER(C.c_int)]),

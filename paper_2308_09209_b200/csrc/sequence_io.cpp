@@ -1,13 +1,13 @@
 // sequence_io.cpp -- frame ingress / egress either side of the per-frame path
-// (SURVEY §8f rank 3): the reference's PPM image I/O and numbered-sequence
-// helpers (image_io.cpp:19-85, 181-199) and a file-to-file sequence runner
-// (run_sequence, pipeline.cpp:364-412, with directory sources and a PPM
-// sink).  B200 side: view files are read straight into pinned staging
-// buffers by one reader thread per view, frames go through the pipelined
-// submit / wait path (four frames in flight: uploads, kernels and downloads
-// overlap), and four writer threads encode the panoramas from an eight-frame
-// pinned ring, so file I/O overlaps the GPU.  PNG needs libpng, which this image does not ship: .png inputs
-// are reported as IoError.
+// (SURVEY §8f rank 3): the reference's image I/O and numbered-sequence helpers
+// (image_io.cpp:19-199; PNG through png_codec.cpp on zlib, libpng is not in
+// this image) and a file-to-file sequence runner (run_sequence,
+// pipeline.cpp:364-412, with directory sources and an image sink).  B200
+// side: view files are read straight into pinned staging buffers by one
+// reader thread per view, frames go through the pipelined submit / wait path
+// (four frames in flight: uploads, kernels and downloads overlap), and four
+// writer threads encode the panoramas from an eight-frame pinned ring, so
+// file I/O overlaps the GPU.
 #include <algorithm>
 #include <atomic>
 #include <cctype>
@@ -21,6 +21,7 @@
 #include <thread>
 #include <vector>
 
+#include "png_codec.hpp"
 #include "stitch_b200.h"
 
 namespace fs = std::filesystem;
@@ -75,7 +76,7 @@ int ppm_header(std::FILE* f, const std::string& path, int* w, int* h) {
   return STITCH_B200_OK;
 }
 
-std::vector<fs::path> list_ppm(const std::string& dir, int* rc) {
+std::vector<fs::path> list_images(const std::string& dir, int* rc) {
   // list_sequence (image_io.cpp:181-192): regular .png / .ppm files, sorted
   std::vector<fs::path> files;
   std::error_code ec;
@@ -86,15 +87,33 @@ std::vector<fs::path> list_ppm(const std::string& dir, int* rc) {
   for (const auto& e : fs::directory_iterator(dir, ec)) {
     if (!e.is_regular_file()) continue;
     const auto ext = e.path().extension().string();
-    if (ext == ".png") {
-      *rc = io_fail(e.path().string(), "PNG input needs libpng, which this build does not have");
-      return {};
-    }
-    if (ext == ".ppm") files.push_back(e.path());
+    if (ext == ".ppm" || ext == ".png") files.push_back(e.path());
   }
   std::sort(files.begin(), files.end());
   *rc = STITCH_B200_OK;
   return files;
+}
+
+// read_image (image_io.cpp:167-172) of one unmasked camera frame straight
+// into rgb (capacity bytes): the PPM raster is read in place, a PNG decoded
+// then copied.  A PNG with transparent pixels is a masked frame, which the
+// device path does not take (its inputs are unmasked).
+int read_frame(const fs::path& path, uint8_t* rgb, size_t capacity, int* w, int* h) {
+  const std::string ext = path.extension().string();
+  if (ext == ".ppm") return stitch_b200_read_ppm(path.string().c_str(), rgb, capacity, w, h);
+  if (ext != ".png") return io_fail(path.string(), "unsupported image extension");
+  stitch_b200_png::Image img;
+  const int rc = stitch_b200_png::read_png(path.string(), img);
+  if (rc) return rc;
+  *w = img.width;
+  *h = img.height;
+  if (!img.mask.empty())
+    return stitch_b200_set_error(STITCH_B200_InputMismatch,
+                                 (path.string() + ": masked (transparent) input frame").c_str());
+  if (img.rgb.size() > capacity)
+    return stitch_b200_set_error(STITCH_B200_InputMismatch, "frame size differs from the view size");
+  std::memcpy(rgb, img.rgb.data(), img.rgb.size());
+  return STITCH_B200_OK;
 }
 
 }  // namespace
@@ -144,6 +163,35 @@ int stitch_b200_write_ppm(const char* path, int width, int height, const uint8_t
   return STITCH_B200_OK;
 }
 
+int stitch_b200_read_png(const char* path, uint8_t* rgb, size_t capacity, uint8_t* mask,
+                         size_t mask_capacity, int* width, int* height, int* has_mask) {
+  stitch_b200_png::Image img;
+  const int rc = stitch_b200_png::read_png(path, img);
+  if (rc) return rc;
+  if (width) *width = img.width;
+  if (height) *height = img.height;
+  if (has_mask) *has_mask = img.mask.empty() ? 0 : 1;
+  if (rgb) {
+    if (img.rgb.size() > capacity)
+      return stitch_b200_set_error(STITCH_B200_InputMismatch, "buffer too small");
+    std::memcpy(rgb, img.rgb.data(), img.rgb.size());
+  }
+  if (mask) {
+    const size_t n = static_cast<size_t>(img.width) * img.height;
+    if (n > mask_capacity) return stitch_b200_set_error(STITCH_B200_InputMismatch, "buffer too small");
+    if (img.mask.empty())
+      std::memset(mask, 1, n);
+    else
+      std::memcpy(mask, img.mask.data(), n);
+  }
+  return STITCH_B200_OK;
+}
+
+int stitch_b200_write_png(const char* path, int width, int height, const uint8_t* rgb,
+                          const uint8_t* mask) {
+  return stitch_b200_png::write_png(path, width, height, rgb, mask);
+}
+
 int stitch_b200_sequence_name(const char* stem, int index, const char* ext, char* out,
                               size_t capacity) {
   // sequence_name (image_io.cpp:194-199): stem + "_%06d" + ext
@@ -154,8 +202,11 @@ int stitch_b200_sequence_name(const char* stem, int index, const char* ext, char
 }
 
 int stitch_b200_run_files(stitch_b200_ctx* ctx, const char* const* view_dirs,
-                          const char* out_dir, const char* stem, int max_frames,
+                          const char* out_dir, const char* stem, const char* ext, int max_frames,
                           stitch_b200_report* reports, stitch_b200_files_stats* stats) {
+  const std::string out_ext = ext ? ext : ".ppm";
+  if (out_ext != ".ppm" && out_ext != ".png")
+    return io_fail(out_ext, "unsupported output image extension");
   const int nv = stitch_b200_n_views(ctx);
   if (nv < 1) return nv < 0 ? nv : stitch_b200_set_error(STITCH_B200_MissingState, "no views");
   int cw = 0, ch = 0;
@@ -165,7 +216,7 @@ int stitch_b200_run_files(stitch_b200_ctx* ctx, const char* const* view_dirs,
   std::vector<std::vector<fs::path>> lists(nv);
   size_t n = 0;
   for (int v = 0; v < nv; ++v) {
-    lists[v] = list_ppm(view_dirs[v], &rc);
+    lists[v] = list_images(view_dirs[v], &rc);
     if (rc) return rc;
     n = v == 0 ? lists[v].size() : std::min(n, lists[v].size());
   }
@@ -245,8 +296,7 @@ int stitch_b200_run_files(stitch_b200_ctx* ctx, const char* const* view_dirs,
         }
         const auto t0 = now();
         int w = 0, h = 0;
-        const int r = stitch_b200_read_ppm(lists[v][t].string().c_str(), ring[t % kRing].in[v],
-                                           vbytes[v], &w, &h);
+        const int r = read_frame(lists[v][t], ring[t % kRing].in[v], vbytes[v], &w, &h);
         if (r == STITCH_B200_OK && static_cast<size_t>(w) * h * 3 != vbytes[v]) {
           stitch_b200_set_error(STITCH_B200_InputMismatch, "frame size differs from the view size");
           set_err(STITCH_B200_InputMismatch);
@@ -280,11 +330,16 @@ int stitch_b200_run_files(stitch_b200_ctx* ctx, const char* const* view_dirs,
         if (out_dir) {
           const auto t0 = now();
           char name[512];
-          int r = stitch_b200_sequence_name(stem ? stem : "pano", static_cast<int>(t), ".ppm",
-                                            name, sizeof(name));
+          int r = stitch_b200_sequence_name(stem ? stem : "pano", static_cast<int>(t),
+                                            out_ext.c_str(), name, sizeof(name));
+          const std::string file = (fs::path(out_dir) / name).string();
+          // write_image (image_io.cpp:174-179): PPM drops the mask, PNG
+          // stores it as alpha (the panorama always carries one)
           if (!r)
-            r = stitch_b200_write_ppm((fs::path(out_dir) / name).string().c_str(), cw, ch,
-                                      ring[t % kRing].rgb);
+            r = out_ext == ".png"
+                    ? stitch_b200_write_png(file.c_str(), cw, ch, ring[t % kRing].rgb,
+                                            ring[t % kRing].mask)
+                    : stitch_b200_write_ppm(file.c_str(), cw, ch, ring[t % kRing].rgb);
           if (r) {
             set_err(r);
             return;

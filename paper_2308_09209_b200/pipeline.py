@@ -547,6 +547,54 @@ def write_ppm(path, frame: Frame) -> None:
                                        data.ctypes.data_as(C.c_void_p)))
 
 
+def read_png(path) -> Frame:
+    """read_png (image_io.cpp:87-129): 8-bit RGB after libpng's expand /
+    strip_16 / gray_to_rgb; transparent pixels become the mask (None when
+    every pixel is opaque)."""
+    lib = _lib()
+    p = str(path).encode()
+    w, h, hm = C.c_int(), C.c_int(), C.c_int()
+    check(lib.stitch_b200_read_png(p, None, 0, None, 0, C.byref(w), C.byref(h), C.byref(hm)))
+    data = np.empty((h.value, w.value, 3), np.uint8)
+    mask = np.empty((h.value, w.value), np.uint8)
+    check(lib.stitch_b200_read_png(p, data.ctypes.data_as(C.c_void_p), data.nbytes,
+                                   mask.ctypes.data_as(C.c_void_p), mask.nbytes, None, None, None))
+    return Frame(data, mask if hm.value else None)
+
+
+def write_png(path, frame: Frame) -> None:
+    """write_png (image_io.cpp:131-165): RGB, or RGBA with the mask as alpha."""
+    data = np.ascontiguousarray(frame.data, dtype=np.uint8)
+    mask = None if frame.mask is None else np.ascontiguousarray(frame.mask, dtype=np.uint8)
+    check(_lib().stitch_b200_write_png(str(path).encode(), frame.width, frame.height,
+                                       data.ctypes.data_as(C.c_void_p),
+                                       None if mask is None else mask.ctypes.data_as(C.c_void_p)))
+
+
+def read_image(path) -> Frame:
+    """read_image (image_io.cpp:167-172): dispatch on .ppm / .png."""
+    import os
+
+    ext = os.path.splitext(str(path))[1]
+    if ext == ".ppm":
+        return read_ppm(path)
+    if ext == ".png":
+        return read_png(path)
+    raise StitchError(ErrorCode.IoError + 1, f"{path}: unsupported image extension")
+
+
+def write_image(path, frame: Frame) -> None:
+    """write_image (image_io.cpp:174-179)."""
+    import os
+
+    ext = os.path.splitext(str(path))[1]
+    if ext == ".ppm":
+        return write_ppm(path, frame)
+    if ext == ".png":
+        return write_png(path, frame)
+    raise StitchError(ErrorCode.IoError + 1, f"{path}: unsupported image extension")
+
+
 def sequence_name(stem: str, index: int, ext: str = ".png") -> str:
     """sequence_name (image_io.cpp:194-199): stem_000003.png."""
     buf = C.create_string_buffer(len(stem) + len(ext) + 32)
@@ -579,22 +627,22 @@ class FilesResult:
 
 
 def run_files(state: PipelineState, view_dirs: Sequence[str], out_dir: Optional[str] = None,
-              stem: str = "pano", max_frames: int = 0) -> FilesResult:
-    """run_sequence (pipeline.cpp:364-412) on numbered PPM sequences, one
-    directory per view, panoramas written as out_dir/stem_%06d.ppm; file
-    reads, the pipelined GPU frames and the writes overlap (C++ threads in
+              stem: str = "pano", max_frames: int = 0, ext: str = ".ppm") -> FilesResult:
+    """run_sequence (pipeline.cpp:364-412) on numbered .ppm / .png
+    sequences, one directory per view, panoramas written as
+    out_dir/stem_%06d<ext> (.ppm, or .png with the mask as alpha); file reads,
+    the pipelined GPU frames and the writes overlap (C++ threads in
     libstitch_b200.so)."""
     lib = _lib()
     n = lib.stitch_b200_n_views(state.handle)
     if len(view_dirs) != n:
         raise StitchError(ErrorCode.InputMismatch + 1, "one directory per view")
     dirs = (C.c_char_p * n)(*[str(d).encode() for d in view_dirs])
-    cap = max_frames if max_frames > 0 else min(
-        len([f for f in list_sequence(d) if f.endswith(".ppm")]) for d in view_dirs)
+    cap = max_frames if max_frames > 0 else min(len(list_sequence(d)) for d in view_dirs)
     reps = (_abi.Report * max(1, cap))()
     st = _abi.FilesStats()
     check(lib.stitch_b200_run_files(state.handle, dirs, str(out_dir).encode() if out_dir else None,
-                                    stem.encode(), cap, reps, C.byref(st)))
+                                    stem.encode(), ext.encode(), cap, reps, C.byref(st)))
     return FilesResult([_report_from_c(reps[i]) for i in range(st.frames)], st.frames,
                        st.seconds, st.read_seconds, st.write_seconds)
 

@@ -15,13 +15,14 @@ from tests.helpers import frames_at, oracle_config, product_config, scene
 pytestmark = pytest.mark.gpu
 
 
-def write_views(sc, root, frames):
+def write_views(sc, root, frames, png_views=()):
     dirs = []
     for v in range(sc.spec.views):
         d = os.path.join(root, f"view{v}")
         os.makedirs(d, exist_ok=True)
+        ext = ".png" if v in png_views else ".ppm"
         for t in range(frames):
-            pb.write_ppm(os.path.join(d, pb.sequence_name("cam", t, ".ppm")), sc.render_view(v, t))
+            pb.write_image(os.path.join(d, pb.sequence_name("cam", t, ext)), sc.render_view(v, t))
         dirs.append(d)
     return dirs
 
@@ -52,6 +53,27 @@ def test_run_files_matches_oracle(tmp_path):
         ost.close()
 
 
+def test_run_files_png_in_and_out(tmp_path):
+    """PNG sources (one view) and PNG panoramas with the mask as alpha."""
+    sc = scene(views=2, width=160, height=120, frames=3, casts=[(1, 1, 1), (0.9, 1, 1.1)])
+    dirs = write_views(sc, str(tmp_path / "in"), 3, png_views=(1,))
+    state = pb.initialize(product_config(sc), frames_at(sc, 0))
+    ost = O.OracleState(oracle_config(sc))
+    try:
+        out = str(tmp_path / "out")
+        res = pb.run_files(state, dirs, out, "pano", ext=".png")
+        assert res.frames == 3
+        for t in range(3):
+            odata, omask, _ = ost.process([f.data for f in frames_at(sc, t)])
+            got = pb.read_png(os.path.join(out, pb.sequence_name("pano", t, ".png")))
+            np.testing.assert_array_equal(got.mask if got.mask is not None else
+                                          np.ones_like(omask), omask)
+            np.testing.assert_array_equal(got.data, odata)
+    finally:
+        state.close()
+        ost.close()
+
+
 def test_run_files_limits_and_errors(tmp_path):
     sc = scene(views=2, width=160, height=120, frames=4)
     dirs = write_views(sc, str(tmp_path / "in"), 4)
@@ -68,8 +90,18 @@ def test_run_files_limits_and_errors(tmp_path):
             pb.run_files(state, dirs, None)
         assert e.value.code == ErrorCode.InputMismatch
         pb.process_frame(state, frames_at(sc, 0))
-        # PNG sources need libpng -> IoError; a missing directory -> IoError
-        open(os.path.join(dirs[0], "x.png"), "wb").close()
+        # a transparent PNG source pixel is a masked frame -> InputMismatch
+        f0 = frames_at(sc, 0)[0]
+        mask = np.ones((120, 160), np.uint8)
+        mask[5, 7] = 0
+        pb.write_png(os.path.join(dirs[0], pb.sequence_name("cam", 1, ".png")),
+                     pb.Frame(f0.data, mask))
+        os.remove(os.path.join(dirs[0], pb.sequence_name("cam", 1, ".ppm")))
+        with pytest.raises(StitchError) as e:
+            pb.run_files(state, dirs, None)
+        assert e.value.code == ErrorCode.InputMismatch
+        # a corrupt file -> IoError; a missing directory -> IoError
+        open(os.path.join(dirs[0], pb.sequence_name("cam", 1, ".png")), "wb").close()
         with pytest.raises(StitchError) as e:
             pb.run_files(state, dirs, None)
         assert e.value.code == ErrorCode.IoError
