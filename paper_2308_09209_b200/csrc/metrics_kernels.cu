@@ -150,29 +150,51 @@ __global__ void __launch_bounds__(256) k_ssim_v(const double* __restrict__ tmp,
   }
 }
 
-// the reference's running sum over window positions, in row-major order:
-// the warp stages 32 terms at a time (coalesced loads), lane 0 adds them in
-// order
-__global__ void k_ssim_sum(const double* __restrict__ term, const std::uint8_t* __restrict__ valid,
-                           long long n, double* __restrict__ out_sum,
-                           long long* __restrict__ out_cnt) {
-  const int lane = threadIdx.x & 31;
-  if (threadIdx.x >= 32) return;
+// The reference's running sum over window positions, in row-major order
+// (metrics.cpp:140-150): one lane adds the terms of the fully valid windows
+// in order (FP64, so the rounding sequence is the reference's).
+// Same running sum, with the loads off the sum's critical path: warps 1..15
+// stage chunk c + 1 of the terms (and their window-validity flags) in shared
+// memory while lane 0 of warp 0 adds chunk c in order, so the sum is bound by
+// the dependent DADD chain instead of one global round trip per 32 terms.
+constexpr int kSumChunk = 2048;
+
+__global__ void __launch_bounds__(512) k_ssim_sum_staged(const double* __restrict__ term,
+                                                         const std::uint8_t* __restrict__ valid,
+                                                         long long n, double* __restrict__ out_sum,
+                                                         long long* __restrict__ out_cnt) {
+  __shared__ double st[2][kSumChunk];
+  __shared__ std::uint8_t sv[2][kSumChunk];
+  const int warp = threadIdx.x >> 5;
+  const long long nchunks = (n + kSumChunk - 1) / kSumChunk;
+  auto stage = [&](long long c, int buf) {
+    const long long base = c * kSumChunk;
+    for (int i = threadIdx.x - 32; i < kSumChunk; i += blockDim.x - 32) {
+      const long long k = base + i;
+      const bool ok = k < n && valid[k];
+      sv[buf][i] = ok ? 1 : 0;
+      st[buf][i] = ok ? term[k] : 0.0;
+    }
+  };
+  if (warp != 0 && nchunks > 0) stage(0, 0);
+  __syncthreads();
   double sum = 0.0;
   long long cnt = 0;
-  for (long long base = 0; base < n; base += 32) {
-    const long long i = base + lane;
-    const bool ok = i < n && valid[i];
-    const double t = ok ? term[i] : 0.0;
-    const unsigned m = __ballot_sync(0xffffffffu, ok);
-#pragma unroll 8
-    for (int j = 0; j < 32; ++j) {
-      const double x = __shfl_sync(0xffffffffu, t, j);
-      if (lane == 0 && ((m >> j) & 1u)) sum += x;
+  for (long long c = 0; c < nchunks; ++c) {
+    const int buf = static_cast<int>(c & 1);
+    if (warp != 0) {
+      if (c + 1 < nchunks) stage(c + 1, buf ^ 1);
+    } else if (threadIdx.x == 0) {
+      const int m = static_cast<int>(n - c * kSumChunk < kSumChunk ? n - c * kSumChunk : kSumChunk);
+      for (int i = 0; i < m; ++i)
+        if (sv[buf][i]) {
+          sum += st[buf][i];
+          ++cnt;
+        }
     }
-    cnt += __popc(m);
+    __syncthreads();
   }
-  if (lane == 0) {
+  if (threadIdx.x == 0) {
     *out_sum = sum;
     *out_cnt = cnt;
   }
@@ -236,7 +258,7 @@ cudaError_t gpu_ssim_parts(const uchar4* a, const uchar4* b, int w, int h, doubl
   const int blocks = static_cast<int>(std::max<long long>(1, std::min<long long>(2368, (n + 255) / 256)));
   k_ssim_h<<<blocks, 256, 0, s>>>(a, b, w, h, g, tmp, hcnt);
   k_ssim_v<<<blocks, 256, 0, s>>>(tmp, hcnt, w, h, g, term, valid);
-  k_ssim_sum<<<1, 32, 0, s>>>(term, valid, n, dsum, dcnt);
+  k_ssim_sum_staged<<<1, 512, 0, s>>>(term, valid, n, dsum, dcnt);
   MET_TRY(cudaGetLastError());
   MET_TRY(cudaMemcpyAsync(sum, dsum, sizeof(double), cudaMemcpyDeviceToHost, s));
   MET_TRY(cudaMemcpyAsync(count, dcnt, sizeof(long long), cudaMemcpyDeviceToHost, s));
