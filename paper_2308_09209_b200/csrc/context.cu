@@ -8,6 +8,7 @@
 #include <limits>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -1675,44 +1676,43 @@ namespace {
 struct PackedPair {
   uchar4* a = nullptr;
   uchar4* b = nullptr;
-  ~PackedPair() {
-    if (a) cudaFree(a);
-    if (b) cudaFree(b);
-  }
 };
 
-int pack_pair(int w, int h, const uint8_t* a_rgb, const uint8_t* a_mask, const uint8_t* b_rgb,
-              const uint8_t* b_mask, PackedPair& pp) {
+// caller holds ws.mu
+int pack_pair(MetricsWorkspace& ws, int w, int h, const uint8_t* a_rgb, const uint8_t* a_mask,
+              const uint8_t* b_rgb, const uint8_t* b_mask, PackedPair& pp) {
   if (w <= 0 || h <= 0 || !a_rgb || !b_rgb)
     return fail(STITCH_B200_ConfigurationError, "bad frame arguments");
   const int n = w * h;
-  CUDA_TRY(cudaMalloc(&pp.a, sizeof(uchar4) * n));
-  CUDA_TRY(cudaMalloc(&pp.b, sizeof(uchar4) * n));
-  CUDA_TRY(gpu_pack_rgba(a_rgb, a_mask, n, pp.a, nullptr));
-  CUDA_TRY(gpu_pack_rgba(b_rgb, b_mask, n, pp.b, nullptr));
+  CUDA_TRY(gpu_pack_rgba(ws, 0, a_rgb, a_mask, n, &pp.a, ws.s));
+  CUDA_TRY(gpu_pack_rgba(ws, 1, b_rgb, b_mask, n, &pp.b, ws.s));
   return STITCH_B200_OK;
 }
 }  // namespace
 
 int stitch_b200_psnr(int width, int height, const uint8_t* a_rgb, const uint8_t* a_mask,
                      const uint8_t* b_rgb, const uint8_t* b_mask, double* out) {
+  MetricsWorkspace& ws = metrics_workspace();
+  std::lock_guard<std::mutex> lk(ws.mu);
   PackedPair pp;
-  int rc = pack_pair(width, height, a_rgb, a_mask, b_rgb, b_mask, pp);
+  int rc = pack_pair(ws, width, height, a_rgb, a_mask, b_rgb, b_mask, pp);
   if (rc) return rc;
   unsigned long long sse = 0, n = 0;
-  CUDA_TRY(gpu_psnr_parts(pp.a, pp.b, width * height, &sse, &n, nullptr));
+  CUDA_TRY(gpu_psnr_parts(ws, pp.a, pp.b, width * height, &sse, &n, ws.s));
   return psnr_from_parts(sse, n, out);
 }
 
 int stitch_b200_ssim(int width, int height, const uint8_t* a_rgb, const uint8_t* a_mask,
                      const uint8_t* b_rgb, const uint8_t* b_mask, double* out) {
   if (width < 11 || height < 11) return fail(STITCH_B200_TooSmall, "ssim needs >= 11x11");
+  MetricsWorkspace& ws = metrics_workspace();
+  std::lock_guard<std::mutex> lk(ws.mu);
   PackedPair pp;
-  int rc = pack_pair(width, height, a_rgb, a_mask, b_rgb, b_mask, pp);
+  int rc = pack_pair(ws, width, height, a_rgb, a_mask, b_rgb, b_mask, pp);
   if (rc) return rc;
   double sum = 0.0;
   long long n = 0;
-  CUDA_TRY(gpu_ssim_parts(pp.a, pp.b, width, height, &sum, &n, nullptr));
+  CUDA_TRY(gpu_ssim_parts(ws, pp.a, pp.b, width, height, &sum, &n, ws.s));
   return ssim_from_parts(sum, n, out);
 }
 
@@ -1722,17 +1722,20 @@ int stitch_b200_pair_quality(stitch_b200_ctx* h, int k, double out[3]) {
   if (int rc_ = sync_all(ctx)) return rc_;
   const PairDesc& p = ctx->slot[ctx->last_slot].hg.pairs[k];
   const int n = p.w * p.h;
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  MetricsWorkspace& ws = metrics_workspace();
+  std::lock_guard<std::mutex> lk(ws.mu);
   unsigned long long sse = 0, cnt = 0;
-  CUDA_TRY(gpu_psnr_parts(p.crop_cor[0], p.crop_raw[0], n, &sse, &cnt, ctx->stream));
+  CUDA_TRY(gpu_psnr_parts(ws, p.crop_cor[0], p.crop_raw[0], n, &sse, &cnt, ctx->stream));
   int rc = psnr_from_parts(sse, cnt, &out[0]);
   if (rc) return rc;
-  CUDA_TRY(gpu_psnr_parts(p.crop_cor[0], p.crop_cor[1], n, &sse, &cnt, ctx->stream));
+  CUDA_TRY(gpu_psnr_parts(ws, p.crop_cor[0], p.crop_cor[1], n, &sse, &cnt, ctx->stream));
   rc = psnr_from_parts(sse, cnt, &out[1]);
   if (rc) return rc;
   if (p.w < 11 || p.h < 11) return fail(STITCH_B200_TooSmall, "ssim needs >= 11x11");
   double sum = 0.0;
   long long wn = 0;
-  CUDA_TRY(gpu_ssim_parts(p.crop_cor[0], p.crop_cor[1], p.w, p.h, &sum, &wn, ctx->stream));
+  CUDA_TRY(gpu_ssim_parts(ws, p.crop_cor[0], p.crop_cor[1], p.w, p.h, &sum, &wn, ctx->stream));
   return ssim_from_parts(sum, wn, &out[2]);
 }
 

@@ -13,6 +13,8 @@
 
 #include <cuda_runtime.h>
 
+#include <mutex>
+
 #include <cstddef>
 #include <cstdint>
 #include <utility>
@@ -275,12 +277,27 @@ cudaError_t feat_match(const std::vector<float>& da, const std::vector<float>& d
                        std::vector<int>& best_a, cudaStream_t s);
 
 // ---- quality metrics (metrics_kernels.cu) ----
-cudaError_t gpu_psnr_parts(const uchar4* a, const uchar4* b, int n, unsigned long long* sse,
-                           unsigned long long* count, cudaStream_t s);
-cudaError_t gpu_ssim_parts(const uchar4* a, const uchar4* b, int w, int h, double* sum,
-                           long long* count, cudaStream_t s);
-cudaError_t gpu_pack_rgba(const std::uint8_t* rgb_host, const std::uint8_t* mask_host, int n,
-                          uchar4* out, cudaStream_t s);
+// Quality-metric scratch: grow-only device buffers and a stream per device,
+// reused across calls (no allocation or free per metric call); callers hold
+// mu for the duration of a metric.
+struct MetricsWorkspace {
+  enum { kPackRgb, kPackMask, kPackA, kPackB, kPsnrAcc, kSsimTmp, kSsimTerm, kSsimCnt, kSsimValid,
+         kSsimSum, kSlots };
+  std::mutex mu;
+  cudaStream_t s = nullptr;
+  void* p[kSlots] = {};
+  size_t cap[kSlots] = {};
+  cudaError_t get(int slot, size_t bytes, void** out);
+};
+MetricsWorkspace& metrics_workspace();  // the current device's
+
+cudaError_t gpu_psnr_parts(MetricsWorkspace& ws, const uchar4* a, const uchar4* b, int n,
+                           unsigned long long* sse, unsigned long long* count, cudaStream_t s);
+cudaError_t gpu_ssim_parts(MetricsWorkspace& ws, const uchar4* a, const uchar4* b, int w, int h,
+                           double* sum, long long* count, cudaStream_t s);
+// which: 0 / 1 = the workspace's first / second packed frame
+cudaError_t gpu_pack_rgba(MetricsWorkspace& ws, int which, const std::uint8_t* rgb_host,
+                          const std::uint8_t* mask_host, int n, uchar4** out, cudaStream_t s);
 
 // ---- init-time geometry on the device (geometry_kernels.cu) ----
 struct ViewFootprint {

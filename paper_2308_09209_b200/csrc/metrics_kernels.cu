@@ -11,6 +11,9 @@
 // equal the reference's values bit for bit.
 #include <cuda_runtime.h>
 
+#include <map>
+#include <mutex>
+
 #include <cmath>
 #include <cstdint>
 #include <vector>
@@ -200,22 +203,33 @@ __global__ void __launch_bounds__(512) k_ssim_sum_staged(const double* __restric
   }
 }
 
-namespace {
-struct Scratch {
-  std::vector<void*> ptrs;
-  ~Scratch() {
-    for (void* p : ptrs) cudaFree(p);
+MetricsWorkspace& metrics_workspace() {
+  static std::mutex map_mu;
+  static std::map<int, MetricsWorkspace*> per_device;  // never freed: process lifetime
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(map_mu);
+  MetricsWorkspace*& w = per_device[dev];
+  if (!w) {
+    w = new MetricsWorkspace();
+    cudaStreamCreateWithFlags(&w->s, cudaStreamNonBlocking);
   }
-  template <typename T>
-  cudaError_t alloc(T** p, size_t count) {
-    void* q = nullptr;
-    cudaError_t e = cudaMalloc(&q, count * sizeof(T) + 16);
-    if (e == cudaSuccess) ptrs.push_back(q);
-    *p = static_cast<T*>(q);
-    return e;
+  return *w;
+}
+
+cudaError_t MetricsWorkspace::get(int slot, size_t bytes, void** out) {
+  if (bytes + 16 > cap[slot]) {
+    if (p[slot]) cudaFree(p[slot]);
+    p[slot] = nullptr;
+    cap[slot] = 0;
+    const size_t want = bytes + bytes / 4 + 16;  // grow with slack
+    cudaError_t e = cudaMalloc(&p[slot], want);
+    if (e != cudaSuccess) return e;
+    cap[slot] = want;
   }
-};
-}  // namespace
+  *out = p[slot];
+  return cudaSuccess;
+}
 
 #define MET_TRY(x)                    \
   do {                                \
@@ -223,11 +237,18 @@ struct Scratch {
     if (e_ != cudaSuccess) return e_; \
   } while (0)
 
-cudaError_t gpu_psnr_parts(const uchar4* a, const uchar4* b, int n, unsigned long long* sse,
-                           unsigned long long* count, cudaStream_t s) {
-  Scratch sc;
+template <typename T>
+static cudaError_t ws_get(MetricsWorkspace& ws, int slot, size_t count, T** out) {
+  void* q = nullptr;
+  cudaError_t e = ws.get(slot, count * sizeof(T), &q);
+  *out = static_cast<T*>(q);
+  return e;
+}
+
+cudaError_t gpu_psnr_parts(MetricsWorkspace& ws, const uchar4* a, const uchar4* b, int n,
+                           unsigned long long* sse, unsigned long long* count, cudaStream_t s) {
   unsigned long long* acc;
-  MET_TRY(sc.alloc(&acc, 2));
+  MET_TRY(ws_get(ws, MetricsWorkspace::kPsnrAcc, 2, &acc));
   MET_TRY(cudaMemsetAsync(acc, 0, 2 * sizeof(unsigned long long), s));
   const int blocks = std::max(1, std::min(1184, (n + 255) / 256));
   k_psnr_sse<<<blocks, 256, 0, s>>>(a, b, n, acc);
@@ -240,20 +261,18 @@ cudaError_t gpu_psnr_parts(const uchar4* a, const uchar4* b, int n, unsigned lon
   return cudaSuccess;
 }
 
-cudaError_t gpu_ssim_parts(const uchar4* a, const uchar4* b, int w, int h, double* sum,
-                           long long* count, cudaStream_t s) {
+cudaError_t gpu_ssim_parts(MetricsWorkspace& ws, const uchar4* a, const uchar4* b, int w, int h,
+                           double* sum, long long* count, cudaStream_t s) {
   const long long n = static_cast<long long>(w) * h;
-  Scratch sc;
   double *tmp, *term, *dsum;
   int* hcnt;
   std::uint8_t* valid;
-  long long* dcnt;
-  MET_TRY(sc.alloc(&tmp, static_cast<size_t>(5 * n)));
-  MET_TRY(sc.alloc(&term, static_cast<size_t>(n)));
-  MET_TRY(sc.alloc(&hcnt, static_cast<size_t>(n)));
-  MET_TRY(sc.alloc(&valid, static_cast<size_t>(n)));
-  MET_TRY(sc.alloc(&dsum, 1));
-  MET_TRY(sc.alloc(&dcnt, 1));
+  MET_TRY(ws_get(ws, MetricsWorkspace::kSsimTmp, static_cast<size_t>(5 * n), &tmp));
+  MET_TRY(ws_get(ws, MetricsWorkspace::kSsimTerm, static_cast<size_t>(n), &term));
+  MET_TRY(ws_get(ws, MetricsWorkspace::kSsimCnt, static_cast<size_t>(n), &hcnt));
+  MET_TRY(ws_get(ws, MetricsWorkspace::kSsimValid, static_cast<size_t>(n), &valid));
+  MET_TRY(ws_get(ws, MetricsWorkspace::kSsimSum, 2, &dsum));
+  long long* dcnt = reinterpret_cast<long long*>(dsum + 1);
   const SsimKernel g = ssim_kernel();
   const int blocks = static_cast<int>(std::max<long long>(1, std::min<long long>(2368, (n + 255) / 256)));
   k_ssim_h<<<blocks, 256, 0, s>>>(a, b, w, h, g, tmp, hcnt);
@@ -266,18 +285,20 @@ cudaError_t gpu_ssim_parts(const uchar4* a, const uchar4* b, int w, int h, doubl
   return cudaSuccess;
 }
 
-cudaError_t gpu_pack_rgba(const std::uint8_t* rgb_host, const std::uint8_t* mask_host, int n,
-                          uchar4* out, cudaStream_t s) {
-  Scratch sc;
+cudaError_t gpu_pack_rgba(MetricsWorkspace& ws, int which, const std::uint8_t* rgb_host,
+                          const std::uint8_t* mask_host, int n, uchar4** out, cudaStream_t s) {
   std::uint8_t *drgb, *dmask = nullptr;
-  MET_TRY(sc.alloc(&drgb, static_cast<size_t>(3) * n));
+  MET_TRY(ws_get(ws, MetricsWorkspace::kPackRgb, static_cast<size_t>(3) * n, &drgb));
+  MET_TRY(ws_get(ws, which ? MetricsWorkspace::kPackB : MetricsWorkspace::kPackA,
+                 static_cast<size_t>(n), out));
   MET_TRY(cudaMemcpyAsync(drgb, rgb_host, static_cast<size_t>(3) * n, cudaMemcpyHostToDevice, s));
   if (mask_host) {
-    MET_TRY(sc.alloc(&dmask, static_cast<size_t>(n)));
+    MET_TRY(ws_get(ws, MetricsWorkspace::kPackMask, static_cast<size_t>(n), &dmask));
     MET_TRY(cudaMemcpyAsync(dmask, mask_host, static_cast<size_t>(n), cudaMemcpyHostToDevice, s));
   }
-  k_pack_rgba<<<std::max(1, std::min(1184, (n + 255) / 256)), 256, 0, s>>>(drgb, dmask, n, out);
+  k_pack_rgba<<<std::max(1, std::min(1184, (n + 255) / 256)), 256, 0, s>>>(drgb, dmask, n, *out);
   MET_TRY(cudaGetLastError());
+  // the staging buffers are reused by the next pack: order it after this one
   MET_TRY(cudaStreamSynchronize(s));
   return cudaSuccess;
 }
