@@ -466,3 +466,42 @@ def test_heterogeneous_camera_sizes():
     for t in range(3):
         check_frame(state, ost, frames(t), t)
     state.close()
+
+
+def test_concurrent_contexts_on_host_threads():
+    """Two panorama streams on their own contexts, driven from two host
+    threads at once (ctypes releases the GIL in the C ABI calls): each
+    stream's panoramas and reports equal its own sequential run."""
+    import threading
+
+    scs = [scene(views=3, width=200, height=150, frames=4, seed=s,
+                 casts=[(0.9, 1, 1), (1, 1, 1), (1, 0.95, 1.1)]) for s in (3, 4)]
+    expect = []
+    for sc in scs:
+        st = pb.initialize(product_config(sc), frames_at(sc, 0))
+        expect.append([pb.process_frame(st, frames_at(sc, t)) for t in range(4)])
+        st.close()
+    got = [None, None]
+    errs = []
+
+    def run(i):
+        try:
+            sc = scs[i]
+            st = pb.initialize(product_config(sc), frames_at(sc, 0))
+            got[i] = [pb.process_frame(st, frames_at(sc, t)) for t in range(4)]
+            st.close()
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for i in range(2):
+        for t in range(4):
+            np.testing.assert_array_equal(got[i][t].panorama.data, expect[i][t].panorama.data)
+            np.testing.assert_array_equal(got[i][t].panorama.mask, expect[i][t].panorama.mask)
+            np.testing.assert_array_equal(np.array(got[i][t].report.color_matrices),
+                                          np.array(expect[i][t].report.color_matrices))
