@@ -275,7 +275,10 @@ int enqueue_op(Ctx* ctx, const Op& op, cudaStream_t s, int slot = 0) {
       return 1;
     case OP_PREP:
       if (!g.n_pairs) return 0;
-      launch_flow_prepare(S.dg, S.dst, g.n_pairs, ctx->max_crop_px, s);
+      if (op.fuse)
+        launch_flow_prepare_pyr(S.dg, S.dst, g.n_pairs, ctx->max_crop_w, ctx->max_crop_h, s);
+      else
+        launch_flow_prepare(S.dg, S.dst, g.n_pairs, ctx->max_crop_px, s);
       return 1;
     case OP_PYR:
       launch_pyr_down(S.d_pyr + op.offset, op.count, op.max_px, s);
@@ -507,10 +510,18 @@ int build_context(const stitch_b200_init* in, int device,
       op.count = static_cast<int>(lists.size()) - op.offset;
       plan.push_back(op);
     }
-    plan.push_back({OP_PREP});
+    // the corrected crops + level-0 luma, and with pyr_fuse the first
+    // kPyrFused pyramid levels in the same launch
+    const int pyr_fused = pyr_fuse_wanted() ? kPyrFused : 1;
+    for (int k = 0; k < in->n_pairs; ++k) g.pairs[k].levels = ctx->pair_levels[k];
+    {
+      Op op{OP_PREP};
+      op.fuse = pyr_fused > 1 ? 1 : 0;
+      plan.push_back(op);
+    }
     plan.push_back({OP_EVENT, 0, 0, 0, 0, 0, 2});
 
-    for (int l = 1; l < Lmax; ++l) {
+    for (int l = pyr_fused; l < Lmax; ++l) {
       Op op{OP_PYR};
       op.offset = static_cast<int>(pyr_table.size());
       for (int k = 0; k < in->n_pairs; ++k) {

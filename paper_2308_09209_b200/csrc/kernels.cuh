@@ -44,6 +44,7 @@ struct PairDesc {
   uchar4* crop_raw[2];
   uchar4* crop_cor[2];
   float* pyr[2][kMaxLevels];
+  int levels;                // pyramid levels of the pair's flow (0: no flow)
   const float2* flow_uv[2];  // final level-0 flow (u, v), dir 0: view->partner
 };
 
@@ -214,6 +215,11 @@ void launch_pair_color(const Geometry* g, DevState* st, const int* pair_list, in
 void launch_flow_prepare(const Geometry* g, DevState* st, int n_pairs, int max_crop_px,
                          cudaStream_t s);
 void launch_pyr_down(const PyrTask* tasks, int n, int max_px, cudaStream_t s);
+// flow_prepare + the first kPyrFused pyramid levels in one launch
+constexpr int kPyrFused = 4;
+void launch_flow_prepare_pyr(const Geometry* g, DevState* st, int n_pairs, int max_w, int max_h,
+                             cudaStream_t s);
+int pyr_fuse_wanted();
 size_t hs_smem_bytes(int sweeps);
 // how many launches (sweep segments) one warp iteration of `sweeps` uses
 int hs_segments(int sweeps);
