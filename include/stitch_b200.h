@@ -233,6 +233,11 @@ int stitch_b200_pair_quality(stitch_b200_ctx* ctx, int k, double out[3]);
  * descriptor sets (best_b[a] = ratio-tested nearest b or -1, best_a[b]). */
 int stitch_b200_debug_detect(int width, int height, const uint8_t* rgb, const int region[4],
                              double threshold, int max_kp, double* kp, float* desc);
+/* Test entry: the device tone curve (build_curve, color_balance.cpp:65-104)
+ * for n threshold pairs (m1[i], m2[i]) -> out[n * 256]. */
+int stitch_b200_debug_tone_curves(int n, const int* m1, const int* m2, double gamma_dark,
+                                  double gamma_bright, int target_black, int target_white,
+                                  uint8_t* out);
 int stitch_b200_debug_match(const float* da, int na, const float* db, int nb, double ratio,
                             int* best_b, double* best_dist, int* best_a);
 

@@ -558,8 +558,14 @@ void so_ldlt_solve3(const double a_in[9], const double b_in[9], double x[9]) {
       else
         d[i] = 0.0;
     }
-    for (int i = n - 2; i >= 0; --i)
-      for (int j = i + 1; j < n; ++j) d[i] -= m[j][i] * d[j];
+    /* L^T x = y: Eigen's triangular_solve_matrix (row-major U = L^T view)
+     * accumulates b = sum_{j>i} U_ij x_j from 0 first, then x_i = (x_i - b)
+     * -- pinned against the compiled reference (tests/test_ref_pin.py). */
+    for (int i = n - 2; i >= 0; --i) {
+      double b = 0.0;
+      for (int j = i + 1; j < n; ++j) b += m[j][i] * d[j];
+      d[i] = d[i] - b;
+    }
     for (int k = n - 1; k >= 0; --k) {
       const double t = d[k];
       d[k] = d[tr[k]];

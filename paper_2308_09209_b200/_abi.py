@@ -98,6 +98,8 @@ SYMBOLS = [
                                            C.c_double, C.c_int, C.c_void_p, C.c_void_p]),
     ("stitch_b200_debug_match", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_double,
                                           C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("stitch_b200_debug_tone_curves", C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_double,
+                                                C.c_double, C.c_int, C.c_int, C.c_void_p]),
     ("stitch_b200_camera_maps", C.c_int, [C.POINTER(Config), C.POINTER(C.c_double)]),
     ("stitch_b200_psnr", C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_void_p, C.POINTER(C.c_double)]),

@@ -129,6 +129,10 @@ __device__ __forceinline__ bool fused_pixel(const CanvasParams& P, const CanvasP
 // Global balancing on the last CTA: find_thresholds (color_balance.cpp:8-38),
 // history push (pipeline.cpp:340-345), smooth_thresholds
 // (color_balance.cpp:40-63), build_curve (color_balance.cpp:65-104).
+__device__ unsigned char curve_entry(int v, int m1, int m2, double gamma_dark,
+                                     double gamma_bright, double target_black,
+                                     double target_white);
+
 __device__ void balance_lut(const Geometry* __restrict__ g, DevState* __restrict__ st) {
   __shared__ int sm1[3], sm2[3], first1[3], first2[3];
   __shared__ unsigned long long wtot[8];
@@ -222,30 +226,46 @@ __device__ void balance_lut(const Geometry* __restrict__ g, DevState* __restrict
     ++*st->frame_counter;
   }
   __syncthreads();
-  for (int c = 0; c < 3; ++c) {
-    unsigned char out = static_cast<unsigned char>(v);
-    if (ok) {
-      const int m1 = sm1[c], m2 = sm2[c];
-      const double tb = g->target_black, tw = g->target_white;
-      const double x = static_cast<double>(v);
-      double val;
-      if (m1 >= m2) {
-        val = tb + (tw - tb) * (x / 255.0);
-      } else {
-        const double lm1 = tb + (tw - tb) * (static_cast<double>(m1) / 255.0);
-        const double lm2 = tb + (tw - tb) * (static_cast<double>(m2) / 255.0);
-        if (x <= m1) {
-          val = (m1 == 0) ? tb : tb + (lm1 - tb) * pow(x / m1, g->gamma_dark);
-        } else if (x >= m2) {
-          val = (m2 == 255) ? tw : lm2 + (tw - lm2) * pow((x - m2) / (255.0 - m2), g->gamma_bright);
-        } else {
-          val = lm1 + (lm2 - lm1) * (x - m1) / (m2 - m1);
-        }
-      }
-      out = quantize_d(val);
+  for (int c = 0; c < 3; ++c)
+    st->lut[c][v] = ok ? curve_entry(v, sm1[c], sm2[c], g->gamma_dark, g->gamma_bright,
+                                     g->target_black, g->target_white)
+                       : static_cast<unsigned char>(v);
+}
+
+// One entry of build_curve (color_balance.cpp:65-104): balance_curve_value in
+// the reference's operation order (FP64, no FMA, CUDA pow), then
+// quantize_channel.  Checked against the compiled reference's curve for every
+// (m1, m2) by tests/test_ref_pin.py through k_debug_tone_curves.
+__device__ unsigned char curve_entry(int v, int m1, int m2, double gamma_dark,
+                                     double gamma_bright, double target_black,
+                                     double target_white) {
+  const double tb = target_black, tw = target_white;
+  const double x = static_cast<double>(v);
+  double val;
+  if (m1 >= m2) {
+    val = tb + (tw - tb) * (x / 255.0);
+  } else {
+    const double lm1 = tb + (tw - tb) * (static_cast<double>(m1) / 255.0);
+    const double lm2 = tb + (tw - tb) * (static_cast<double>(m2) / 255.0);
+    if (x <= m1) {
+      val = (m1 == 0) ? tb : tb + (lm1 - tb) * pow(x / m1, gamma_dark);
+    } else if (x >= m2) {
+      val = (m2 == 255) ? tw : lm2 + (tw - lm2) * pow((x - m2) / (255.0 - m2), gamma_bright);
+    } else {
+      val = lm1 + (lm2 - lm1) * (x - m1) / (m2 - m1);
     }
-    st->lut[c][v] = out;
   }
+  return quantize_d(val);
+}
+
+// Test entry: n curves (one per (m1[i], m2[i])) of 256 entries each.
+__global__ void k_debug_tone_curves(int n, const int* __restrict__ m1, const int* __restrict__ m2,
+                                    double gamma_dark, double gamma_bright, double tb, double tw,
+                                    unsigned char* __restrict__ out) {
+  const int i = blockIdx.x;
+  if (i >= n) return;
+  out[static_cast<size_t>(i) * 256 + threadIdx.x] =
+      curve_entry(threadIdx.x, m1[i], m2[i], gamma_dark, gamma_bright, tb, tw);
 }
 
 // the view's footprint may contain (x, y): inside its bbox and outside the
@@ -574,6 +594,12 @@ void launch_canvas_class(const CanvasParams& P, std::uint8_t* cls, cudaStream_t 
     k_canvas_class<true><<<148 * 8, 256, 0, s>>>(P, cls);
   else
     k_canvas_class<false><<<148 * 8, 256, 0, s>>>(P, cls);
+}
+
+void launch_debug_tone_curves(int n, const int* m1, const int* m2, double gamma_dark,
+                              double gamma_bright, double tb, double tw, std::uint8_t* out,
+                              cudaStream_t s) {
+  if (n > 0) k_debug_tone_curves<<<n, 256, 0, s>>>(n, m1, m2, gamma_dark, gamma_bright, tb, tw, out);
 }
 
 }  // namespace stitch_b200_dev

@@ -1784,6 +1784,32 @@ int stitch_b200_debug_detect(int width, int height, const uint8_t* rgb, const in
   return static_cast<int>(kps.size());
 }
 
+int stitch_b200_debug_tone_curves(int n, const int* m1, const int* m2, double gamma_dark,
+                                  double gamma_bright, int target_black, int target_white,
+                                  uint8_t* out) {
+  if (n < 0) return fail(STITCH_B200_ConfigurationError, "negative curve count");
+  if (n == 0) return STITCH_B200_OK;
+  int *d1 = nullptr, *d2 = nullptr;
+  uint8_t* dout = nullptr;
+  const size_t ib = sizeof(int) * static_cast<size_t>(n), ob = 256 * static_cast<size_t>(n);
+  cudaError_t e = cudaMalloc(&d1, ib);
+  if (e == cudaSuccess) e = cudaMalloc(&d2, ib);
+  if (e == cudaSuccess) e = cudaMalloc(&dout, ob);
+  if (e == cudaSuccess) e = cudaMemcpy(d1, m1, ib, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(d2, m2, ib, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    stitch_b200_dev::launch_debug_tone_curves(n, d1, d2, gamma_dark, gamma_bright, target_black,
+                                              target_white, dout, 0);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(out, dout, ob, cudaMemcpyDeviceToHost);
+  cudaFree(d1);
+  cudaFree(d2);
+  cudaFree(dout);
+  if (e != cudaSuccess) return fail(STITCH_B200_CudaError, cudaGetErrorString(e));
+  return STITCH_B200_OK;
+}
+
 int stitch_b200_debug_match(const float* da, int na, const float* db, int nb, double ratio,
                             int* best_b, double* best_dist, int* best_a) {
   std::vector<float> a(da, da + 64 * static_cast<size_t>(na)), b(db, db + 64 * static_cast<size_t>(nb));

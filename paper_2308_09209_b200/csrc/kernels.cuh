@@ -253,6 +253,10 @@ void launch_expand_one(const std::uint8_t* rgb, uchar4* rgba, long long n_px, cu
 void launch_warp_mask(const Geometry* g, int view, std::uint8_t* mask, cudaStream_t s);
 // the canvas class map of CanvasParams::cls (init time, geometry only)
 void launch_canvas_class(const CanvasParams& P, std::uint8_t* cls, cudaStream_t s);
+// test entry: n tone curves (build_curve) for the given (m1[i], m2[i])
+void launch_debug_tone_curves(int n, const int* m1, const int* m2, double gamma_dark,
+                              double gamma_bright, double tb, double tw, std::uint8_t* out,
+                              cudaStream_t s);
 
 // ---- feature refinement image work (features_kernels.cu) ----
 struct FeatPoint {
