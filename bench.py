@@ -18,9 +18,22 @@ e2e    : the same metric through the reference-facing C-ABI calls with
          flight): H2D of every camera frame + D2H of the balanced panorama
          (RGB + mask) inside the timed region, max over ranks; the
          synchronous stitch_b200_process is reported as sync_process_value.
---impl reference : the CPU oracle (the reference's path restated in C; the
-         reference itself needs Eigen3 and cannot be built here) on the box's
-         host cores, same workload, rank 0 only.
+--impl reference : the reference's CPU path on the box's host cores, rank 0
+         only.  c1 (2 views, the reference's own rig) runs THE REFERENCE
+         ITSELF: the unmodified sources compiled into oracle/_ref (Eigen-subset
+         shim, oracle/ref/Makefile), kind "reference".  c2-c5 need 4-8 views,
+         which the reference rejects ("pipeline supports 2 or 3 views",
+         pipeline.cpp:24-29), so they run the oracle port (oracle/liboracle.so,
+         bit-exact with the reference on <= 3 views, tests/test_ref_pin.py),
+         kind "port", with the reference/port speed ratio measured on c1 in
+         the same run.
+
+--gpus N : N ranks, one per GPU.  Launched by torchrun (WORLD_SIZE set) or,
+         when WORLD_SIZE is unset, bench.py spawns the N ranks itself
+         (RANK / LOCAL_RANK / WORLD_SIZE / MASTER_*); gloo carries the barrier
+         and the timing reductions -- the frame path has no collective.
+--config c5 : BASELINE configs[4], 64 independent 4x1080p streams sharded
+         s mod N over the ranks (strong scaling: the total is fixed).
 """
 from __future__ import annotations
 
@@ -57,20 +70,33 @@ WORKLOADS = {
                desc="8 cameras 3840x2160 RGB single panorama stream"),
 }
 # BASELINE.json configs[4]: 64 independent 4x1080p streams sharded over the
-# GPUs -> `--config c2 --total-streams 64`
+# GPUs (s mod N) -- the c2 workload with a fixed total stream count
+WORKLOADS["c5"] = dict(WORKLOADS["c2"], total_streams=64,
+                       desc="64 independent 4x1080p panorama streams sharded over the GPUs")
+
+
+def scene_params(wl, seed):
+    """The synthetic scene of a workload (SynthSpec terms, synth.hpp:31-44)."""
+    nv = wl["views"]
+    return dict(seed=seed, views=nv, width=wl["width"], height=wl["height"],
+                focal_scale=wl["focal_scale"],
+                casts=[(1.0, 1.0, 1.0) if v % 2 == 0 else (0.88, 1.0, 1.08) for v in range(nv)],
+                flicker=[dict(frame=5, view=nv - 1, gains=(1.15, 1.1, 0.95))],
+                obj=dict(enabled=True, half_size=0.08 * wl["width"] * 500 / (0.9 * wl["width"]),
+                         velocity=(4.0, 1.0)))
 
 
 def build_scene(wl, seed):
     import paper_2308_09209_b200 as pb
 
-    spec = pb.SynthSpec(seed=seed, views=wl["views"], frames=300, width=wl["width"],
-                        height=wl["height"], overlap_fraction=0.3,
-                        perturb_focal_scale=wl["focal_scale"], rig=wl.get("rig", "auto"))
-    spec.color_casts = [(1.0, 1.0, 1.0) if v % 2 == 0 else (0.88, 1.0, 1.08)
-                        for v in range(wl["views"])]
-    spec.flicker = [pb.FlickerEvent(frame=5, view=wl["views"] - 1, gains=(1.15, 1.1, 0.95))]
-    spec.object = pb.ParallaxObject(enabled=True, half_size=0.08 * wl["width"] * 500 / (
-        0.9 * wl["width"]), velocity=(4.0, 1.0))
+    p = scene_params(wl, seed)
+    spec = pb.SynthSpec(seed=seed, views=p["views"], frames=300, width=p["width"],
+                        height=p["height"], overlap_fraction=0.3,
+                        perturb_focal_scale=p["focal_scale"], rig=wl.get("rig", "auto"))
+    spec.color_casts = p["casts"]
+    spec.flicker = [pb.FlickerEvent(**f) for f in p["flicker"]]
+    spec.object = pb.ParallaxObject(enabled=True, half_size=p["obj"]["half_size"],
+                                    velocity=p["obj"]["velocity"])
     return pb.SynthScene(spec)
 
 
@@ -228,16 +254,20 @@ def run_b200(args, rank, world, local_rank):
     from paper_2308_09209_b200 import _abi, sharding
 
     lib = _abi.load()
-    torch.cuda.set_device(local_rank)
-    dev = f"cuda:{local_rank}"
+    # one rank per GPU; more ranks than visible GPUs (a functional run of the
+    # multi-rank path on one box) share devices round-robin and say so
+    n_dev = max(1, torch.cuda.device_count())
+    device = local_rank % n_dev
+    torch.cuda.set_device(device)
     wl = WORKLOADS[args.config]
-    # streams: one per GPU (weak scaling) unless a fixed stream count is set
-    total_streams = args.total_streams if args.total_streams else world * args.streams_per_gpu
+    # streams: one per GPU (weak scaling) unless a fixed total is set (c5)
+    fixed_total = args.total_streams or wl.get("total_streams", 0)
+    total_streams = fixed_total if fixed_total else world * args.streams_per_gpu
     my_streams = sharding.stream_assignment(total_streams, world, rank)
     ns = len(my_streams)
     sc = build_scene(wl, seed=1 + rank)
-    cfg = sc.config()
-    cfg.device = local_rank
+    cfg = sc.config()  # refinement on, like the reference's default (pipeline.hpp:24)
+    cfg.device = device
     nv = wl["views"]
     F = args.frame_sets
     threads = max(1, cpu_cores() // max(1, world))
@@ -251,20 +281,22 @@ def run_b200(args, rank, world, local_rank):
             img = sc.render_view(v, t, threads).data
             hp = lib.stitch_b200_host_alloc(frame_bytes)
             C.memmove(hp, img.ctypes.data, frame_bytes)
-            dp = lib.stitch_b200_device_alloc(local_rank, frame_bytes)
+            dp = lib.stitch_b200_device_alloc(device, frame_bytes)
             pb.pipeline.check(lib.stitch_b200_memcpy_h2d(dp, hp, frame_bytes))
             hs.append(hp)
             ds.append(dp)
         host_sets.append((C.c_void_p * nv)(*hs))
         dev_sets.append((C.c_void_p * nv)(*ds))
-    first = [pb.Frame(np.zeros((wl["height"], wl["width"], 3), np.uint8)) for _ in range(nv)]
+    # initialize() on the first frames (feature refinement of the coarse
+    # homographies, pipeline.cpp:241-255) -- init time, outside every timing
+    first = [sc.render_view(v, 0, threads) for v in range(nv)]
     states = [pb.initialize(cfg, first) for _ in range(ns)]
     state = states[0]
     hs_ = [st.handle for st in states]
     P = state.canvas_width * state.canvas_height
     out_rgb = lib.stitch_b200_host_alloc(P * 3)
     out_mask = lib.stitch_b200_host_alloc(P)
-    cstreams = [torch.cuda.ExternalStream(lib.stitch_b200_stream(h), device=local_rank)
+    cstreams = [torch.cuda.ExternalStream(lib.stitch_b200_stream(h), device=device)
                 for h in hs_]
     main = torch.cuda.current_stream()
     launches = state.launches_per_frame()
@@ -279,7 +311,7 @@ def run_b200(args, rank, world, local_rank):
         for j, h in enumerate(hs_):
             pb.pipeline.check(lib.stitch_b200_process_device_async(h, dev_sets[(i + j) % F]))
 
-    clocks = ClockSampler(local_rank)
+    clocks = ClockSampler(device)
     clocks.start()
     # ---- warm-up ----
     for i in range(args.warmup):
@@ -311,8 +343,8 @@ def run_b200(args, rank, world, local_rank):
     clocks.active = False
     barrier()
     elapsed_s = e0.elapsed_time(e1) / 1e3
-    max_s = sharding.max_over_ranks(elapsed_s, dev)
-    frames_total = sharding.sum_over_ranks(ns * args.steps, dev)
+    max_s = sharding.max_over_ranks(elapsed_s)
+    frames_total = sharding.sum_over_ranks(ns * args.steps)
     value = frames_total / max_s
     ms_per_step = max_s * 1e3 / args.steps
 
@@ -352,14 +384,14 @@ def run_b200(args, rank, world, local_rank):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     e2e_run(e2e_steps)
-    e2e_s = sharding.max_over_ranks(time.perf_counter() - t0, dev)
+    e2e_s = sharding.max_over_ranks(time.perf_counter() - t0)
     e2e_value = world * e2e_steps / e2e_s
     # the same through the synchronous call (reference semantics, no overlap)
     t0 = time.perf_counter()
     for i in range(min(e2e_steps, 50)):
         pb.pipeline.check(lib.stitch_b200_process(hs_[0], host_sets[i % F], out_rgb, out_mask,
                                                   None))
-    e2e_sync_s = sharding.max_over_ranks(time.perf_counter() - t0, dev)
+    e2e_sync_s = sharding.max_over_ranks(time.perf_counter() - t0)
     e2e_sync = world * min(e2e_steps, 50) / e2e_sync_s
 
     # ---- per-kernel profile (eager plan, CUDA events around each launch) ----
@@ -427,7 +459,7 @@ def run_b200(args, rank, world, local_rank):
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
         "p50_ms_per_frame": round(p50, 4), "higher_is_better": True,
-        "scaling": "strong" if args.total_streams else "weak",
+        "scaling": "strong" if fixed_total else "weak",
         "vs_baseline": None, "dtype": "u8 (fp64 warp, fp32 flow)",
         "data": "synthetic (procedural plane scene, SynthScene restatement; seed 1+rank)",
         "config": {"workload": wl["desc"], "config_key": args.config, "cameras": nv,
@@ -436,6 +468,9 @@ def run_b200(args, rank, world, local_rank):
                    "pairs": [list(p.bounds) for p in state.pairs],
                    "streams_total": int(total_streams), "streams_this_rank": ns,
                    "parallelism": f"independent streams sharded over {world} GPU(s), no collective",
+                   "refined_pairs": sum(1 for p in state.pairs if not p.refine_warning),
+                   "gpus_visible": n_dev,
+                   "oversubscribed": world > n_dev,
                    "l2": (f"inputs cycle over {F} pre-rendered frame sets "
                           f"({F * nv * frame_bytes / 1e6:.0f} MB > 126 MB L2)")},
         "e2e": {"value": round(e2e_value, 2), "unit": UNIT,
@@ -458,88 +493,169 @@ def run_b200(args, rank, world, local_rank):
 
 
 # ---------------------------------------------------------------------------
-# CPU oracle (reference path restated in C) -- baseline only
+# CPU arms: the reference itself (oracle/_ref) or the oracle port -- baseline
+# and reference arm only, never the measured product
 # ---------------------------------------------------------------------------
-def oracle_state_for(sc, threads):
-    import oracle as O
+class CpuRunner:
+    """One stream of the workload on the host: `kind` "reference" runs the
+    compiled reference sources (stitch::initialize / process_frame through
+    oracle/reference.py), "port" the oracle restatement (oracle/liboracle.so).
+    Both initialize on the first frames with the reference's default feature
+    refinement, like the B200 arm."""
 
-    c = sc.config_c()
-    cams = [(c.cams[v].fx, c.cams[v].fy, c.cams[v].cx, c.cams[v].cy, list(c.cams[v].rotation),
-             list(c.cams[v].translation)) for v in range(c.n_views)]
-    sizes = [(c.width[v], c.height[v]) for v in range(c.n_views)]
-    return O.OracleState(O.make_config(c.n_views, c.reference, sizes, cams, threads=threads,
-                                       topology=c.topology, projection=c.projection,
-                                       cyl_focal=c.cyl_focal))
+    def __init__(self, wl, kind, threads, n_sets=2):
+        self.kind = kind
+        p = scene_params(wl, seed=1)
+        if kind == "reference":
+            import oracle.reference as R
+
+            sc = R.Scene(seed=1, views=p["views"], frames=300, width=p["width"],
+                         height=p["height"], casts=p["casts"], flicker=p["flicker"],
+                         obj=p["obj"], focal_scale=p["focal_scale"])
+            self.frames = [[sc.render(v, t) for v in range(p["views"])] for t in range(n_sets)]
+            self.st = R.State(sc, R.default_opts(threads=threads), self.frames[0])
+            sc.close()
+        else:
+            import oracle as O
+
+            sc = build_scene(wl, seed=1)
+            c = sc.config_c()
+            cams = [(c.cams[v].fx, c.cams[v].fy, c.cams[v].cx, c.cams[v].cy,
+                     list(c.cams[v].rotation), list(c.cams[v].translation))
+                    for v in range(c.n_views)]
+            sizes = [(c.width[v], c.height[v]) for v in range(c.n_views)]
+            self.frames = [[sc.render_view(v, t, threads).data for v in range(p["views"])]
+                           for t in range(n_sets)]
+            cfg = O.make_config(c.n_views, c.reference, sizes, cams, threads=threads,
+                                topology=c.topology, projection=c.projection,
+                                cyl_focal=c.cyl_focal, refine=c.projection == 0,
+                                seed=sc.spec.seed)
+            self.st = O.OracleState(cfg, first_frames=self.frames[0])
+            sc.close()
+
+    def rate(self, seconds, max_frames=None, warmup=1):
+        for i in range(warmup):
+            self.st.process(self.frames[i % len(self.frames)])
+        n, t0 = 0, time.perf_counter()
+        while True:
+            self.st.process(self.frames[n % len(self.frames)])
+            n += 1
+            el = time.perf_counter() - t0
+            if el >= seconds or (max_frames and n >= max_frames):
+                return n, el
+
+    def close(self):
+        self.st.close()
 
 
-def cpu_baseline(args, wl, sample_seconds=15.0, max_frames=None):
-    sc = build_scene(wl, seed=1)
+def reference_kind(wl):
+    """The reference itself where it runs the workload (2-3 views, planar),
+    else the port."""
+    import oracle.reference as R
+
+    if wl["views"] <= 3 and wl.get("rig", "auto") != "ring" and R.available():
+        return "reference"
+    return "port"
+
+
+def cpu_baseline(args, wl, sample_seconds=15.0):
     threads = cpu_cores()
-    st = oracle_state_for(sc, threads)
-    frames = [[sc.render_view(v, t, threads).data for v in range(wl["views"])]
-              for t in range(2)]
-    st.process(frames[0])  # warm-up (allocator, page faults)
-    n, t0 = 0, time.perf_counter()
-    while True:
-        st.process(frames[n % 2])
-        n += 1
-        el = time.perf_counter() - t0
-        if el >= sample_seconds or (max_frames and n >= max_frames):
-            break
-    st.close()
-    out = {"value": round(n / el, 4), "unit": UNIT, "cores": threads, "kind": "port",
+    kind = reference_kind(wl)
+    r = CpuRunner(wl, kind, threads)
+    n, el = r.rate(sample_seconds)
+    r.close()
+    src = ("oracle/_ref/libstitch_ref.so: the unmodified reference sources"
+           if kind == "reference" else "oracle/liboracle.so: the reference path restated in C")
+    out = {"value": round(n / el, 4), "unit": UNIT, "cores": threads, "kind": kind,
            "sample": f"{n} frames of the same workload after 1 warm-up frame "
-                     f"({el:.1f} s, oracle/liboracle.so, {threads} OpenMP threads)"}
+                     f"({el:.1f} s, {src}, {threads} threads)"}
     # single-thread rate (the paper's Table-4 shaped CPU ratio), a shorter sample
-    st1 = oracle_state_for(sc, 1)
-    n1, t1 = 0, time.perf_counter()
-    while True:
-        st1.process(frames[n1 % 2])
-        n1 += 1
-        el1 = time.perf_counter() - t1
-        if el1 >= sample_seconds / 3 or (max_frames and n1 >= max_frames):
-            break
-    st1.close()
+    r1 = CpuRunner(wl, kind, 1)
+    n1, el1 = r1.rate(sample_seconds / 3)
+    r1.close()
     out["value_1_thread"] = round(n1 / el1, 4)
     out["sample_1_thread"] = f"{n1} frames, {el1:.1f} s, 1 thread"
     return out
 
 
+def reference_vs_port(seconds=6.0):
+    """Speed of the reference itself vs the port on c1 (both run it), so a
+    port-timed reference arm can be read against the real reference."""
+    import oracle.reference as R
+
+    if not R.available():
+        return None
+    threads = cpu_cores()
+    out = {}
+    for kind in ("reference", "port"):
+        r = CpuRunner(WORKLOADS["c1"], kind, threads)
+        n, el = r.rate(seconds)
+        r.close()
+        out[kind] = round(n / el, 4)
+    out["reference_over_port"] = round(out["reference"] / out["port"], 4)
+    out["note"] = f"c1 frames/s on {threads} host threads, same run"
+    return out
+
+
 def run_reference(args):
     wl = WORKLOADS[args.config]
-    sc = build_scene(wl, seed=1)
     threads = cpu_cores()
-    st = oracle_state_for(sc, threads)
-    frames = [[sc.render_view(v, t, threads).data for v in range(wl["views"])]
-              for t in range(args.frame_sets if args.frame_sets < 4 else 4)]
+    kind = reference_kind(wl)
+    r = CpuRunner(wl, kind, threads, n_sets=min(4, max(1, args.frame_sets)))
     budget = args.ref_budget_s
     t_w = time.perf_counter()
     for i in range(args.warmup):
-        st.process(frames[i % len(frames)])
+        r.st.process(r.frames[i % len(r.frames)])
         if time.perf_counter() - t_w > budget / 4:
             break
     n, t0 = 0, time.perf_counter()
     for i in range(args.steps):
-        st.process(frames[i % len(frames)])
+        r.st.process(r.frames[i % len(r.frames)])
         n += 1
         if time.perf_counter() - t0 > budget:
             break
     el = time.perf_counter() - t0
-    st.close()
+    r.close()
     v = n / el
-    return {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": UNIT,
-            "n_gpus": 0, "steps": n, "warmup": args.warmup, "ms_per_step": round(1e3 * el / n, 2),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "u8 (fp64 warp, fp32 flow)", "data": "synthetic",
-            "config": {"workload": wl["desc"], "config_key": args.config},
-            "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": threads,
-                             "kind": "port",
-                             "sample": f"{n} of {args.steps} requested frames within a "
-                                       f"{budget:.0f} s budget (oracle/liboracle.so: the "
-                                       "reference path restated in C; the reference needs "
-                                       "Eigen3 and cannot be built here)"},
-            "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+    if kind == "reference":
+        what = ("oracle/_ref/libstitch_ref.so: the unmodified reference sources "
+                "(stitch::initialize + process_frame), Eigen-subset shim")
+    else:
+        what = ("oracle/liboracle.so: the reference path restated in C, bit-exact with the "
+                "reference on <= 3 views; the reference itself rejects "
+                f"{wl['views']} views (pipeline.cpp:24-29)")
+    res = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": UNIT,
+           "n_gpus": 0, "steps": n, "warmup": args.warmup, "ms_per_step": round(1e3 * el / n, 2),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "u8 (fp64 warp, fp32 flow)", "data": "synthetic",
+           "config": {"workload": wl["desc"], "config_key": args.config},
+           "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": threads, "kind": kind,
+                            "sample": f"{n} of {args.steps} requested frames within a "
+                                      f"{budget:.0f} s budget ({what})"},
+           "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    if kind == "port" and not args.no_calibration:
+        res["reference_vs_port_c1"] = reference_vs_port()
+    return res
+
+
+def spawn_ranks(n):
+    """bench.py --gpus N without torchrun: run N copies of this script as
+    ranks 0..N-1 (one per GPU) and relay rank 0's output."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                   LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:],
+                                      env=env, stdout=None if r == 0 else subprocess.DEVNULL))
+    rcs = [p.wait() for p in procs]
+    return max(rcs, key=abs)
 
 
 def main():
@@ -552,28 +668,34 @@ def main():
     ap.add_argument("--frame-sets", type=int, default=16)
     ap.add_argument("--streams-per-gpu", type=int, default=1)
     ap.add_argument("--total-streams", type=int, default=0,
-                    help="fixed stream count sharded over the ranks (config c5: 64)")
+                    help="fixed stream count sharded over the ranks (c5 sets 64)")
     ap.add_argument("--e2e-steps", type=int, default=200)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-budget-s", type=float, default=120.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-calibration", action="store_true",
+                    help="reference arm: skip the c1 reference-vs-port speed ratio")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         if rank != 0:
             return
-        print(json.dumps(run_reference(args)))
+        print(json.dumps(run_reference(args)), flush=True)
         return
     if world > 1:
         import torch
 
-        torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl")
+        # gloo: only the barrier and the timing reductions cross ranks
+        torch.distributed.init_process_group("gloo", rank=rank, world_size=world)
     res = run_b200(args, rank, world, local_rank)
     if rank == 0:
-        print(json.dumps(res))
+        print(json.dumps(res), flush=True)
     if world > 1:
         import torch
 

@@ -371,6 +371,15 @@ int stitch_b200_run_files(stitch_b200_ctx* ctx, const char* const* view_dirs,
 /* Number of views / a view's camera size of a context. */
 int stitch_b200_n_views(const stitch_b200_ctx* ctx);
 int stitch_b200_view_size(const stitch_b200_ctx* ctx, int view, int* width, int* height);
+/* Validates one frame set before process/submit: n must equal the configured
+ * views, every frame must have the size its view was initialized with
+ * (InputMismatch otherwise), and masks (may be NULL, or hold NULL entries for
+ * unmasked frames) must be all-nonzero: the reference's masked sampler
+ * (frame.cpp:95-104) is not part of the B200 path, so a frame with any
+ * masked pixel is rejected with InputMismatch instead of being treated as
+ * unmasked.  The C++ and Python mirrors call it on every frame set. */
+int stitch_b200_check_frames(const stitch_b200_ctx* ctx, int n, const int* widths,
+                             const int* heights, const uint8_t* const* masks);
 /* Set the calling thread's last error; returns code. */
 int stitch_b200_set_error(int code, const char* what);
 

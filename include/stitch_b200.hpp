@@ -131,9 +131,9 @@ struct ViewSetup {
 
 struct RefineOptions {
   // Feature refinement at initialize(): detection / description / matching on
-  // the device, RANSAC on the host (stitch_b200_initialize_frames).  The
-  // mirror defaults it off (the reference defaults it on).
-  bool enabled = false;
+  // the device, RANSAC on the host (stitch_b200_initialize_frames).  On by
+  // default, like the reference (pipeline.hpp:24).
+  bool enabled = true;
   double margin = 0.15;
   int ransac_iters = 500;
   double inlier_px = 2.0;
@@ -284,6 +284,15 @@ inline PipelineState initialize(const StitchConfig& config, const std::vector<Fr
     throw StitchError(ErrorCode::ConfigurationError, "pipeline supports 2 to 16 views");
   if (first_frames.size() != config.views.size())
     throw StitchError(ErrorCode::ConfigurationError, "frame count does not match configured views");
+  for (const Frame& f : first_frames) {
+    if (f.data.size() != f.pixel_count() * 3)
+      throw StitchError(ErrorCode::InputMismatch, "frame data must be width*height*3 bytes");
+    for (std::uint8_t m : f.mask)
+      if (m == 0)
+        throw StitchError(ErrorCode::InputMismatch,
+                          "masked input frames (frame.cpp:95-104) are not supported by the "
+                          "B200 path");
+  }
   stitch_b200_config c = to_c(config, first_frames);
   stitch_b200_ctx* ctx = nullptr;
   if (config.refine.enabled) {
@@ -301,12 +310,21 @@ inline PipelineState initialize(const StitchConfig& config, const std::vector<Fr
 inline ProcessResult process_frame(PipelineState& state, const std::vector<Frame>& frames) {
   if (frames.size() != state.config.views.size())
     throw StitchError(ErrorCode::ConfigurationError, "frame count does not match configured views");
-  std::vector<const std::uint8_t*> ptrs;
+  std::vector<const std::uint8_t*> ptrs, masks;
+  std::vector<int> ws, hs;
   for (const Frame& f : frames) {
     if (f.data.size() != f.pixel_count() * 3)
       throw StitchError(ErrorCode::InputMismatch, "frame data must be width*height*3 bytes");
+    if (f.has_mask() && f.mask.size() != f.pixel_count())
+      throw StitchError(ErrorCode::InputMismatch, "frame mask must be width*height bytes");
     ptrs.push_back(f.data.data());
+    masks.push_back(f.has_mask() ? f.mask.data() : nullptr);
+    ws.push_back(f.width);
+    hs.push_back(f.height);
   }
+  // sizes as initialized, no masked pixel (stitch_b200_check_frames)
+  check(stitch_b200_check_frames(state.handle(), static_cast<int>(frames.size()), ws.data(),
+                                 hs.data(), masks.data()));
   ProcessResult result;
   Frame& pano = result.panorama;
   pano.width = state.canvas_width();

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <limits>
 #include <cstring>
 #include <memory>
@@ -988,7 +989,7 @@ void stitch_b200_config_defaults(stitch_b200_config* c) {
   c->window_capacity = 3;
   c->fuse_weighting = 0;
   c->topology = 0;
-  c->refine_enabled = 0;
+  c->refine_enabled = 1;  // RefineOptions::enabled (pipeline.hpp:24)
   c->projection = 0;
   c->cyl_focal = 0.0;
   c->refine_margin = 0.15;  // RefineOptions defaults (pipeline.hpp:23-31)
@@ -1385,6 +1386,30 @@ int stitch_b200_view_size(const stitch_b200_ctx* h, int view, int* width, int* h
     return fail(STITCH_B200_InputMismatch, "view index out of range");
   if (width) *width = ctx->hg.views[view].width;
   if (height) *height = ctx->hg.views[view].height;
+  return STITCH_B200_OK;
+}
+
+int stitch_b200_check_frames(const stitch_b200_ctx* h, int n, const int* widths,
+                             const int* heights, const uint8_t* const* masks) {
+  const Ctx* ctx = h->c.get();
+  if (n != ctx->hg.n_views)
+    return fail(STITCH_B200_ConfigurationError, "frame count does not match configured views");
+  for (int v = 0; v < n; ++v) {
+    const int w = ctx->hg.views[v].width, ht = ctx->hg.views[v].height;
+    if (widths[v] != w || heights[v] != ht) {
+      char msg[160];
+      std::snprintf(msg, sizeof(msg), "frame %d is %dx%d, the context was initialized for %dx%d",
+                    v, widths[v], heights[v], w, ht);
+      return fail(STITCH_B200_InputMismatch, msg);
+    }
+    if (masks && masks[v]) {
+      const size_t px = static_cast<size_t>(w) * static_cast<size_t>(ht);
+      if (std::memchr(masks[v], 0, px) != nullptr)
+        return fail(STITCH_B200_InputMismatch,
+                    "masked input frames (a 0 in Frame::mask, frame.cpp:95-104) are not "
+                    "supported by the B200 path");
+    }
+  }
   return STITCH_B200_OK;
 }
 

@@ -124,10 +124,8 @@ class FlowOptions:  # flow.hpp:29-34
 @dataclass
 class RefineOptions:  # pipeline.hpp:23-31
     # Feature refinement runs at initialize() (detect / describe / match on
-    # the device, RANSAC on the host); the mirror defaults it off (the
-    # reference defaults it on) so that contexts built from a config alone
-    # need no first frames.
-    enabled: bool = False
+    # the device, RANSAC on the host), on by default like the reference.
+    enabled: bool = True
     margin: float = 0.15
     ransac_iters: int = 500
     inlier_px: float = 2.0
@@ -359,10 +357,16 @@ class ProcessResult:  # pipeline.hpp:65-68
 
 
 def initialize(config: StitchConfig, first_frames: Sequence[Frame]) -> PipelineState:
-    """pipeline.hpp:73-74 (refinement must be off; see RefineOptions)."""
+    """pipeline.hpp:73-74; with refine.enabled (the default, as in the
+    reference) the first frames feed the feature refinement."""
     if len(first_frames) != len(config.views):
         raise StitchError(ErrorCode.ConfigurationError + 1,
                           "frame count does not match configured views")
+    for f in first_frames:
+        if f.mask is not None and not np.asarray(f.mask).all():
+            raise StitchError(ErrorCode.InputMismatch + 1,
+                              "masked input frames (frame.cpp:95-104) are not supported by "
+                              "the B200 path")
     sizes = [(f.width, f.height) for f in first_frames]
     c = _config_to_c(config, sizes)
     h = C.c_void_p()
@@ -460,9 +464,34 @@ def _frame_ptrs(frames: Sequence[Frame], n: int):
     if len(frames) != n:
         raise StitchError(ErrorCode.ConfigurationError + 1,
                           "frame count does not match configured views")
-    arrs = [np.ascontiguousarray(f.data, dtype=np.uint8) for f in frames]
+    arrs = []
+    for f in frames:
+        a = np.ascontiguousarray(f.data, dtype=np.uint8)
+        if a.ndim != 3 or a.shape[2] != 3:
+            raise StitchError(ErrorCode.InputMismatch + 1, "frames must be (H, W, 3) uint8")
+        if f.mask is not None and np.asarray(f.mask).shape != a.shape[:2]:
+            raise StitchError(ErrorCode.InputMismatch + 1, "frame mask must be (H, W)")
+        arrs.append(a)
     ptrs = (C.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
     return arrs, ptrs
+
+
+def _mask_ptrs(frames: Sequence[Frame]):
+    masks = [None if f.mask is None else np.ascontiguousarray(f.mask, dtype=np.uint8)
+             for f in frames]
+    ptrs = (C.c_void_p * len(masks))(*[None if m is None else m.ctypes.data for m in masks])
+    return masks, ptrs
+
+
+def check_frames(state: PipelineState, frames: Sequence[Frame]) -> None:
+    """stitch_b200_check_frames: frame count, per-view size as initialized, and
+    no masked pixel (the reference's masked sampler, frame.cpp:95-104, is not
+    on the B200 path) -- InputMismatch instead of a silent misread."""
+    n = len(frames)
+    ws = (C.c_int * max(1, n))(*[f.width for f in frames])
+    hs = (C.c_int * max(1, n))(*[f.height for f in frames])
+    keep, mptrs = _mask_ptrs(frames)
+    check(_lib().stitch_b200_check_frames(state.handle, n, ws, hs, mptrs))
 
 
 def process_frame(state: PipelineState, frames: Sequence[Frame]) -> ProcessResult:
@@ -470,9 +499,7 @@ def process_frame(state: PipelineState, frames: Sequence[Frame]) -> ProcessResul
     blend -> balance, on the GPU."""
     n = len(state.config.views) if state.config else len(frames)
     arrs, ptrs = _frame_ptrs(frames, n)
-    for f, a in zip(frames, arrs):
-        if a.ndim != 3 or a.shape[2] != 3:
-            raise StitchError(ErrorCode.InputMismatch + 1, "frames must be (H, W, 3) uint8")
+    check_frames(state, frames)
     w, h = state.canvas_width, state.canvas_height
     rgb = np.empty((h, w, 3), dtype=np.uint8)
     mask = np.empty((h, w), dtype=np.uint8)

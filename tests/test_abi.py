@@ -8,6 +8,7 @@ import subprocess
 
 import pytest
 
+import paper_2308_09209_b200 as pb
 from paper_2308_09209_b200 import _abi
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -71,7 +72,32 @@ def test_config_defaults_match_reference():
     assert (c.lambda_, c.gamma_dark, c.gamma_bright) == (0.05, 1.5, 1.5)
     assert (c.target_black, c.target_white) == (0, 255)
     assert (c.flow_levels, c.flow_iterations, c.smoothness) == (4, 50, 15.0)
-    assert (c.window_capacity, c.fuse_weighting, c.refine_enabled) == (3, 0, 0)
+    # refinement on (pipeline.hpp:24)
+    assert (c.window_capacity, c.fuse_weighting, c.refine_enabled) == (3, 0, 1)
+    assert pb.RefineOptions().enabled is True
+
+
+def test_mirror_defaults_match_reference():
+    """the Python mirror's StitchConfig equals the compiled reference's
+    StitchConfig defaults (pipeline.hpp:17-45) field by field."""
+    import oracle.reference as R
+
+    if not R.available():
+        pytest.skip("reference neither present nor prebuilt")
+    o = R.default_opts()
+    cfg = pb.StitchConfig()
+    assert (cfg.balance.lambda_, cfg.balance.gamma_dark, cfg.balance.gamma_bright,
+            cfg.balance.target_black, cfg.balance.target_white) == (
+        o.lambda_, o.gamma_dark, o.gamma_bright, o.target_black, o.target_white)
+    assert (cfg.flow.levels, cfg.flow.iterations, cfg.flow.smoothness) == (
+        o.levels, o.iterations, o.smoothness)
+    assert (cfg.window_capacity, cfg.fuse_weighting == "cross", cfg.threads) == (
+        o.window_capacity, bool(o.fuse_weighting), o.threads)
+    r = cfg.refine
+    assert (r.enabled, r.margin, r.ransac_iters, r.inlier_px, r.detect_threshold, r.match_ratio,
+            r.rerefine_every) == (bool(o.refine_enabled), o.refine_margin, o.ransac_iters,
+                                  o.inlier_px, o.detect_threshold, o.match_ratio,
+                                  o.rerefine_every)
 
 
 def test_last_error_is_a_string():
