@@ -48,6 +48,8 @@ static stitch_b200_synth* make_scene(int views, int w, int h) {
 static StitchConfig config_of(stitch_b200_synth* s, stitch_b200_config& c) {
   check(stitch_b200_synth_config(s, &c));
   StitchConfig cfg;
+  CHECK(cfg.refine.enabled);  // the reference's default (pipeline.hpp:24)
+  cfg.refine.enabled = false;  // these cases compare with the unrefined oracle
   cfg.reference = c.reference;
   for (int v = 0; v < c.n_views; ++v) {
     ViewSetup vs;
