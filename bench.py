@@ -386,6 +386,33 @@ def run_b200(args, rank, world, local_rank):
     e2e_run(e2e_steps)
     e2e_s = sharding.max_over_ranks(time.perf_counter() - t0)
     e2e_value = world * e2e_steps / e2e_s
+    # the same with PAGEABLE host buffers (the reference's std::vector frames,
+    # frame.hpp:17-57): the context stages them through its pinned ring
+    pg_in = [[np.empty(frame_bytes, np.uint8) for _ in range(nv)] for _ in range(F)]
+    for t in range(F):
+        for v in range(nv):
+            C.memmove(pg_in[t][v].ctypes.data, host_sets[t][v], frame_bytes)
+    pg_in_ptrs = [(C.c_void_p * nv)(*[a.ctypes.data for a in pg_in[t]]) for t in range(F)]
+    pg_out = [(np.empty(P * 3, np.uint8), np.empty(P, np.uint8)) for _ in range(depth)]
+
+    def e2e_run_pageable(n):
+        tickets = []
+        for i in range(n):
+            o = pg_out[i % depth]
+            pb.pipeline.check(lib.stitch_b200_submit(hs_[0], pg_in_ptrs[i % F], o[0].ctypes.data,
+                                                     o[1].ctypes.data, C.byref(tk)))
+            tickets.append(tk.value)
+            if i >= depth - 1:
+                pb.pipeline.check(lib.stitch_b200_wait(hs_[0], tickets[i - depth + 1], None))
+        for t in tickets[max(0, n - depth + 1):]:
+            pb.pipeline.check(lib.stitch_b200_wait(hs_[0], t, None))
+
+    e2e_run_pageable(min(args.warmup, 3) + 1)
+    barrier()
+    t0 = time.perf_counter()
+    e2e_run_pageable(e2e_steps)
+    e2e_pg_s = sharding.max_over_ranks(time.perf_counter() - t0)
+    e2e_pageable = world * e2e_steps / e2e_pg_s
     # the same through the synchronous call (reference semantics, no overlap)
     t0 = time.perf_counter()
     for i in range(min(e2e_steps, 50)):
@@ -477,7 +504,10 @@ def run_b200(args, rank, world, local_rank):
                 "h2d_bytes_per_step": nv * frame_bytes, "d2h_bytes_per_step": P * 4,
                 "steps": e2e_steps, "streams": 1,
                 "api": f"stitch_b200_submit/stitch_b200_wait ({E2E_IN_FLIGHT} frames in flight, pinned host)",
-                "sync_process_value": round(e2e_sync, 2)},
+                "sync_process_value": round(e2e_sync, 2),
+                "pageable_value": round(e2e_pageable, 2),
+                "pageable_api": "same calls with pageable (numpy) frames and outputs, staged "
+                                "through the context's pinned ring"},
         "realtime_streams": round(value / 30.0, 1),  # sustained 30 fps streams
         "gpu_launches": launches * args.steps * ns,
         "kernels_per_frame": launches,

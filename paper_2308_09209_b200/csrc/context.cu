@@ -9,7 +9,10 @@
 #include <limits>
 #include <cstring>
 #include <memory>
+#include <atomic>
+#include <condition_variable>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -73,6 +76,110 @@ struct SlotRes {
   cudaGraphExec_t exec[kSegs] = {};
 };
 
+// Host copy pool for the pageable-buffer path.  The reference hands frames
+// over as pageable std::vector buffers (frame.hpp:17-57, pipeline.hpp:65-80);
+// an async copy from pageable memory would serialise the pipeline (the
+// driver stages it synchronously, and a D2H to pageable memory returns only
+// after the copy), so such buffers go through a pinned per-slot ring and
+// these workers move the bytes between the caller's buffers and the ring in
+// parallel chunks while the GPU works on the other frames in flight.
+class CopyPool {
+ public:
+  struct Job {
+    void* dst;
+    const void* src;
+    size_t n;
+  };
+
+  explicit CopyPool(int workers) {
+    for (int i = 0; i < workers; ++i) th_.emplace_back([this] { loop(); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+
+  // Copies every (dst, src, n), split into ~1 MiB chunks; the calling thread
+  // works too.  Returns when all bytes have landed.
+  void run(const std::vector<Job>& jobs) {
+    constexpr size_t kChunk = size_t(1) << 20;
+    std::vector<Job> chunks;
+    for (const Job& j : jobs)
+      for (size_t o = 0; o < j.n; o += kChunk)
+        chunks.push_back({static_cast<char*>(j.dst) + o, static_cast<const char*>(j.src) + o,
+                          std::min(kChunk, j.n - o)});
+    if (chunks.empty()) return;
+    std::unique_lock<std::mutex> lk(mu_);
+    work_ = &chunks;
+    next_.store(0);
+    left_ = chunks.size();
+    ++gen_;
+    lk.unlock();
+    cv_.notify_all();
+    drain();
+    lk.lock();
+    done_cv_.wait(lk, [&] { return left_ == 0; });
+    work_ = nullptr;
+  }
+
+ private:
+  void drain() {
+    const std::vector<Job>* w;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      w = work_;
+    }
+    if (!w) return;
+    size_t did = 0;
+    for (size_t i = next_.fetch_add(1); i < w->size(); i = next_.fetch_add(1)) {
+      std::memcpy((*w)[i].dst, (*w)[i].src, (*w)[i].n);
+      ++did;
+    }
+    if (did) {
+      std::lock_guard<std::mutex> lk(mu_);
+      left_ -= did;
+      if (left_ == 0) done_cv_.notify_all();
+    }
+  }
+
+  void loop() {
+    unsigned long long seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+      }
+      drain();
+    }
+  }
+
+  std::vector<std::thread> th_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::vector<Job>* work_ = nullptr;
+  std::atomic<size_t> next_{0};
+  size_t left_ = 0;
+  unsigned long long gen_ = 0;
+  bool stop_ = false;
+};
+
+// Page-locked (cudaHostAlloc'ed or cudaHostRegister'ed) host memory can be the
+// direct source / target of an async copy; anything else is staged.
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 struct Ctx {
   int device = 0;
   int num_sms = 148;
@@ -119,6 +226,15 @@ struct Ctx {
   cudaEvent_t ring_ev[16] = {};
   int ring_pos = 0;
   DevReport* h_report = nullptr;  // one per slot (pinned)
+  // pageable caller buffers: pinned staging per slot (allocated on first
+  // use), the caller's output pointers to fill when the slot retires, and
+  // the copy workers
+  std::uint8_t* h_stage_in[kSlots][kMaxViews] = {};
+  std::uint8_t* h_stage_rgb[kSlots] = {};
+  std::uint8_t* h_stage_mask[kSlots] = {};
+  std::uint8_t* user_rgb[kSlots] = {};
+  std::uint8_t* user_mask[kSlots] = {};
+  std::unique_ptr<CopyPool> copier;
   std::vector<int> pair_levels;
   float2* d_zero = nullptr;
 
@@ -155,6 +271,12 @@ struct Ctx {
     for (void* p : allocs) cudaFree(p);
     if (h_ptr_ring) cudaFreeHost(h_ptr_ring);
     if (h_report) cudaFreeHost(h_report);
+    for (int s = 0; s < kSlots; ++s) {
+      for (auto* q : h_stage_in[s])
+        if (q) cudaFreeHost(q);
+      if (h_stage_rgb[s]) cudaFreeHost(h_stage_rgb[s]);
+      if (h_stage_mask[s]) cudaFreeHost(h_stage_mask[s]);
+    }
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -854,6 +976,15 @@ void fill_report(Ctx* ctx, int slot, stitch_b200_report* r) {
 int retire_slot(Ctx* ctx, int slot) {
   if (!ctx->slot_pending[slot]) return STITCH_B200_OK;
   CUDA_TRY(cudaEventSynchronize(ctx->d2h_done[slot]));
+  if (ctx->user_rgb[slot] || ctx->user_mask[slot]) {  // pageable outputs: ring -> caller
+    std::vector<CopyPool::Job> jobs;
+    if (ctx->user_rgb[slot])
+      jobs.push_back({ctx->user_rgb[slot], ctx->h_stage_rgb[slot], static_cast<size_t>(ctx->n_px) * 3});
+    if (ctx->user_mask[slot])
+      jobs.push_back({ctx->user_mask[slot], ctx->h_stage_mask[slot], static_cast<size_t>(ctx->n_px)});
+    ctx->copier->run(jobs);
+    ctx->user_rgb[slot] = ctx->user_mask[slot] = nullptr;
+  }
   stitch_b200_report r;
   fill_report(ctx, slot, &r);
   ctx->done_reports.emplace_back(ctx->slot_ticket[slot], r);
@@ -916,8 +1047,28 @@ int join_api_stream(Ctx* ctx) {
   return STITCH_B200_OK;
 }
 
+// Pinned staging of one slot for pageable caller buffers (first use only).
+int ensure_staging(Ctx* ctx, int slot) {
+  if (!ctx->copier) {
+    const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+    ctx->copier.reset(new CopyPool(static_cast<int>(std::min(8u, hw / 2))));
+  }
+  for (int v = 0; v < ctx->hg.n_views; ++v)
+    if (!ctx->h_stage_in[slot][v])
+      CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_stage_in[slot][v]),
+                             ctx->frame_bytes[v], cudaHostAllocDefault));
+  if (!ctx->h_stage_rgb[slot])
+    CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_stage_rgb[slot]),
+                           static_cast<size_t>(ctx->n_px) * 3, cudaHostAllocDefault));
+  if (!ctx->h_stage_mask[slot])
+    CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_stage_mask[slot]),
+                           static_cast<size_t>(ctx->n_px), cudaHostAllocDefault));
+  return STITCH_B200_OK;
+}
+
 // Host-buffer frame: H2D on the upload stream, compute, D2H on the download
-// stream; returns the frame's ticket.
+// stream; returns the frame's ticket.  Pinned caller buffers are copied
+// directly; pageable ones through the slot's pinned staging ring.
 int submit_host(Ctx* ctx, const std::uint8_t* const* frames, std::uint8_t* pano_rgb,
                 std::uint8_t* pano_mask, long long* ticket) {
   const int slot = static_cast<int>(ctx->seq % Ctx::kSlots);
@@ -925,11 +1076,28 @@ int submit_host(Ctx* ctx, const std::uint8_t* const* frames, std::uint8_t* pano_
   if (rc) return rc;
   for (int v = 0; v < ctx->hg.n_views; ++v)
     if (!frames[v]) return fail(STITCH_B200_InputMismatch, "null frame");
-  // the slot's inputs were last read by the frame two submissions ago
+  // pageable inputs / outputs go through the slot's pinned staging ring
+  bool stage_in[kMaxViews];
+  bool any_stage = false;
+  for (int v = 0; v < ctx->hg.n_views; ++v) any_stage |= (stage_in[v] = !is_pinned(frames[v]));
+  const bool stage_rgb = pano_rgb && !is_pinned(pano_rgb);
+  const bool stage_mask = pano_mask && !is_pinned(pano_mask);
+  if (any_stage || stage_rgb || stage_mask) {
+    rc = ensure_staging(ctx, slot);
+    if (rc) return rc;
+  }
+  // the slot's inputs were last read by its previous frame (retired above,
+  // so its staging buffers are free as well)
   CUDA_TRY(cudaStreamWaitEvent(ctx->h2d, ctx->comp_done[slot], 0));
+  if (any_stage) {
+    std::vector<CopyPool::Job> jobs;
+    for (int v = 0; v < ctx->hg.n_views; ++v)
+      if (stage_in[v]) jobs.push_back({ctx->h_stage_in[slot][v], frames[v], ctx->frame_bytes[v]});
+    ctx->copier->run(jobs);
+  }
   for (int v = 0; v < ctx->hg.n_views; ++v)
-    CUDA_TRY(cudaMemcpyAsync(ctx->d_in[slot][v], frames[v], ctx->frame_bytes[v],
-                             cudaMemcpyHostToDevice, ctx->h2d));
+    CUDA_TRY(cudaMemcpyAsync(ctx->d_in[slot][v], stage_in[v] ? ctx->h_stage_in[slot][v] : frames[v],
+                             ctx->frame_bytes[v], cudaMemcpyHostToDevice, ctx->h2d));
   CUDA_TRY(cudaEventRecord(ctx->h2d_done[slot], ctx->h2d));
   CUDA_TRY(cudaStreamWaitEvent(ctx->slot[slot].cs, ctx->h2d_done[slot], 0));
   const std::uint8_t* in[kMaxViews];
@@ -938,12 +1106,14 @@ int submit_host(Ctx* ctx, const std::uint8_t* const* frames, std::uint8_t* pano_
   if (rc) return rc;
   CUDA_TRY(cudaStreamWaitEvent(ctx->d2h, ctx->comp_done[slot], 0));
   if (pano_rgb)
-    CUDA_TRY(cudaMemcpyAsync(pano_rgb, ctx->d_out_rgb[slot], static_cast<size_t>(ctx->n_px) * 3,
-                             cudaMemcpyDeviceToHost, ctx->d2h));
+    CUDA_TRY(cudaMemcpyAsync(stage_rgb ? ctx->h_stage_rgb[slot] : pano_rgb, ctx->d_out_rgb[slot],
+                             static_cast<size_t>(ctx->n_px) * 3, cudaMemcpyDeviceToHost, ctx->d2h));
   if (pano_mask)
-    CUDA_TRY(cudaMemcpyAsync(pano_mask, ctx->d_out_mask[slot], static_cast<size_t>(ctx->n_px),
-                             cudaMemcpyDeviceToHost, ctx->d2h));
+    CUDA_TRY(cudaMemcpyAsync(stage_mask ? ctx->h_stage_mask[slot] : pano_mask, ctx->d_out_mask[slot],
+                             static_cast<size_t>(ctx->n_px), cudaMemcpyDeviceToHost, ctx->d2h));
   CUDA_TRY(cudaEventRecord(ctx->d2h_done[slot], ctx->d2h));
+  ctx->user_rgb[slot] = stage_rgb ? pano_rgb : nullptr;
+  ctx->user_mask[slot] = stage_mask ? pano_mask : nullptr;
   ctx->slot_ticket[slot] = ctx->seq;
   ctx->slot_pending[slot] = true;
   if (ticket) *ticket = ctx->seq;
@@ -1283,6 +1453,15 @@ static int carry_into(stitch_b200_ctx* h, std::unique_ptr<Ctx>& fresh) {
   Ctx* ctx = h->c.get();
   int rc = sync_all(ctx);
   if (rc) return rc;
+  // retire every pending host-path frame so its report survives the swap,
+  // and keep ticket numbers monotonic: tickets issued before the swap stay
+  // waitable and can never alias a later frame
+  for (int sl = 0; sl < Ctx::kSlots; ++sl) {
+    rc = retire_slot(ctx, sl);
+    if (rc) return rc;
+  }
+  fresh->done_reports = std::move(ctx->done_reports);
+  fresh->seq = ctx->seq;
   // carry windows, threshold history and the frame counter over
   // (pipeline.cpp:399-405)
   CUDA_TRY(cudaMemcpy(fresh->dtemp, ctx->dtemp, sizeof(TemporalState), cudaMemcpyDeviceToDevice));

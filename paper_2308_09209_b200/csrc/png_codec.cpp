@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <new>
 #include <vector>
 
 #include "png_codec.hpp"
@@ -61,7 +62,7 @@ bool read_file(const std::string& path, std::vector<unsigned char>& out) {
 
 }  // namespace
 
-int read_png(const std::string& path, Image& img) {
+static int read_png_impl(const std::string& path, Image& img) {
   std::vector<unsigned char> file;
   if (!read_file(path, file)) return fail(path, "cannot open");
   if (file.size() < 8 || std::memcmp(file.data(), kSig, 8) != 0) return fail(path, "not a PNG");
@@ -101,6 +102,10 @@ int read_png(const std::string& path, Image& img) {
   }
   if (!seen_ihdr || w == 0 || h == 0 || w > (1u << 24) || h > (1u << 24))
     return fail(path, "bad IHDR");
+  // a crafted or corrupt header must not drive the allocation below: cap the
+  // raster like the canvas (2^31 pixels) before sizing any buffer
+  if (static_cast<unsigned long long>(w) * h > (1ull << 31))
+    return fail(path, "image larger than 2^31 pixels");
   if (interlace != 0) return fail(path, "interlaced PNG is not supported");
   int samples;  // samples per pixel in the file
   switch (ctype) {
@@ -215,6 +220,15 @@ int read_png(const std::string& path, Image& img) {
   }
   if (any_invalid) img.mask = std::move(mask);
   return STITCH_B200_OK;
+}
+
+int read_png(const std::string& path, Image& img) {
+  // no exception crosses the C ABI (ctypes callers, run_files reader threads)
+  try {
+    return read_png_impl(path, img);
+  } catch (const std::bad_alloc&) {
+    return fail(path, "out of memory decoding the image");
+  }
 }
 
 int write_png(const std::string& path, int width, int height, const unsigned char* rgb,

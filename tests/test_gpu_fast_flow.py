@@ -1,0 +1,48 @@
+"""The contract-tolerant Jacobi sweep (STITCH_B200_HS_FAST=1: FMA contraction
+and the approximate reciprocal instead of the reference's unfused arithmetic
+and IEEE division) against the oracle at BASELINE.json's full sizes, C1-C4:
+every frame must stay within north_star's contract -- flows within 1e-3 px,
+colour matrices within 1e-4 relative, panoramas within +-1 LSB, masks,
+thresholds and rank flags identical.  Runs in a subprocess because the switch
+is read once per process; prints the max diffs as one JSON line (the
+numbers DESIGN.md quotes)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CODE = r"""
+import json, sys
+from tests.fullsize import run_config
+key = sys.argv[1]
+geom, frames, info = run_config(key)
+worst = {"config": key, "geometry_equal": geom, "frames": len(frames),
+         "flow_max_abs_px": max(d["flow_max_abs_px"] for d in frames),
+         "color_matrix_max_rel": max(d["color_matrix_max_rel"] for d in frames),
+         "panorama_max_abs_lsb": max(d["panorama_max_abs_lsb"] for d in frames),
+         "mask_equal": all(d["mask_equal"] for d in frames),
+         "thresholds_equal": all(d["thresholds_equal"] for d in frames),
+         "rank_flags_equal": all(d["rank_flags_equal"] for d in frames)}
+print("RESULT " + json.dumps(worst))
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("key", ["c1", "c2", "c3", "c4"])
+def test_fast_sweep_within_contract(key):
+    env = dict(os.environ, STITCH_B200_HS_FAST="1")
+    r = subprocess.run([sys.executable, "-c", CODE, key], cwd=ROOT, env=env, capture_output=True,
+                       text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    line = [ln for ln in r.stdout.splitlines() if ln.startswith("RESULT ")][-1]
+    d = json.loads(line[len("RESULT "):])
+    print(line)
+    assert d["geometry_equal"]
+    assert d["flow_max_abs_px"] <= 1e-3, d
+    assert d["color_matrix_max_rel"] <= 1e-4, d
+    assert d["panorama_max_abs_lsb"] <= 1, d
+    assert d["mask_equal"] and d["thresholds_equal"] and d["rank_flags_equal"], d

@@ -506,3 +506,89 @@ def test_concurrent_contexts_on_host_threads():
             np.testing.assert_array_equal(got[i][t].panorama.mask, expect[i][t].panorama.mask)
             np.testing.assert_array_equal(np.array(got[i][t].report.color_matrices),
                                           np.array(expect[i][t].report.color_matrices))
+
+
+def test_tickets_survive_geometry_update():
+    """Host-path frames still in flight when the geometry is replaced
+    (stitch_b200_update_maps -> a fresh context) keep their reports, and ticket
+    numbers stay monotonic across the swap, so an old ticket never aliases a
+    new frame."""
+    sc = scene(views=2, width=160, height=120, frames=4)
+    cfg = product_config(sc)
+    state = pb.initialize(cfg, frames_at(sc, 0))
+    lib = _lib()
+    w, h = state.canvas_width, state.canvas_height
+    fb = 160 * 120 * 3
+    hin = [[lib.stitch_b200_host_alloc(fb) for _ in range(2)] for _ in range(3)]
+    hout = [(lib.stitch_b200_host_alloc(w * h * 3), lib.stitch_b200_host_alloc(w * h))
+            for _ in range(3)]
+    try:
+        tickets = []
+        for t in range(3):
+            for v, f in enumerate(frames_at(sc, t)):
+                C.memmove(hin[t][v], np.ascontiguousarray(f.data).ctypes.data, fb)
+        for t in range(2):
+            tk = C.c_longlong()
+            pb.pipeline.check(lib.stitch_b200_submit(state.handle, (C.c_void_p * 2)(*hin[t]),
+                                                     hout[t][0], hout[t][1], C.byref(tk)))
+            tickets.append(tk.value)
+        state.update_maps(pb.camera_maps(cfg, [(160, 120)] * 2))
+        tk = C.c_longlong()
+        pb.pipeline.check(lib.stitch_b200_submit(state.handle, (C.c_void_p * 2)(*hin[2]),
+                                                 hout[2][0], hout[2][1], C.byref(tk)))
+        tickets.append(tk.value)
+        assert tickets == sorted(set(tickets))
+        for t, tk in enumerate(tickets):
+            r = _abi.Report()
+            pb.pipeline.check(lib.stitch_b200_wait(state.handle, tk, C.byref(r)))
+            assert r.frame_index == t
+    finally:
+        state.close()
+        for t in range(3):
+            for p in hin[t]:
+                lib.stitch_b200_host_free(p)
+            lib.stitch_b200_host_free(hout[t][0])
+            lib.stitch_b200_host_free(hout[t][1])
+
+
+def test_pageable_submit_matches_pinned():
+    """The reference's caller passes pageable std::vector buffers: submit/wait
+    with pageable (numpy) frames and outputs, four frames in flight, goes
+    through the context's pinned staging ring and yields exactly the pinned
+    path's panoramas and reports."""
+    sc = scene(views=3, width=200, height=150, frames=7,
+               casts=[(0.9, 1, 1), (1, 1, 1), (1, 0.95, 1.1)])
+    lib = _lib()
+    cfg = product_config(sc)
+    a = pb.initialize(cfg, frames_at(sc, 0))
+    w, h = a.canvas_width, a.canvas_height
+    try:
+        want = [pb.process_frame(a, frames_at(sc, t)) for t in range(7)]  # sync path
+    finally:
+        a.close()
+    b = pb.initialize(cfg, frames_at(sc, 0))
+    ins = [[np.ascontiguousarray(f.data) for f in frames_at(sc, t)] for t in range(7)]
+    outs = [(np.zeros((h, w, 3), np.uint8), np.zeros((h, w), np.uint8)) for _ in range(7)]
+    try:
+        tickets, reps = [], {}
+        for t in range(7):
+            tk = C.c_longlong()
+            pb.pipeline.check(lib.stitch_b200_submit(
+                b.handle, (C.c_void_p * 3)(*[x.ctypes.data for x in ins[t]]),
+                outs[t][0].ctypes.data, outs[t][1].ctypes.data, C.byref(tk)))
+            tickets.append(tk.value)
+            if t >= 3:
+                r = _abi.Report()
+                pb.pipeline.check(lib.stitch_b200_wait(b.handle, tickets[t - 3], C.byref(r)))
+                reps[t - 3] = r
+        for t in range(4, 7):
+            r = _abi.Report()
+            pb.pipeline.check(lib.stitch_b200_wait(b.handle, tickets[t], C.byref(r)))
+            reps[t] = r
+        for t in range(7):
+            np.testing.assert_array_equal(outs[t][0], want[t].panorama.data)
+            np.testing.assert_array_equal(outs[t][1], want[t].panorama.mask)
+            assert reps[t].frame_index == t
+            assert list(reps[t].threshold_m1) == list(want[t].report.threshold_m1)
+    finally:
+        b.close()

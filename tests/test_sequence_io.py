@@ -185,6 +185,16 @@ def test_png_interlaced_is_rejected(tmp_path):
     assert e.value.code == ErrorCode.IoError and "interlaced" in str(e.value)
 
 
+def test_png_huge_header_is_rejected_before_allocating(tmp_path):
+    """a crafted IHDR (2^20 x 2^20 pixels) fails with IoError instead of a
+    multi-terabyte allocation that would throw through the C ABI"""
+    p = tmp_path / "huge.png"
+    p.write_bytes(_png_bytes(1 << 20, 1 << 20, 2, 8, [b"\x00" + bytes(6)]))
+    with pytest.raises(StitchError) as e:
+        pb.read_png(p)
+    assert e.value.code == ErrorCode.IoError and "2^31" in str(e.value)
+
+
 def test_sequence_listing_mixes_png_and_ppm(tmp_path):
     # test_imaging.cpp:257-269 with PNG files
     for i in [2, 0, 1]:
