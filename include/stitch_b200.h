@@ -263,14 +263,19 @@ int stitch_b200_process(stitch_b200_ctx* ctx, const uint8_t* const* frames,
 /* Pipelined variant of stitch_b200_process: enqueue one frame (upload of the
  * host frames on the context's copy stream, the frame on the compute stream,
  * download of the panorama into pano_rgb / pano_mask on a second copy
- * stream) and return a ticket without waiting.  Two frames can be in flight:
- * frame t+1's upload and frame t-1's download overlap frame t's kernels.
- * Frames are processed in submission order (the temporal state is
- * sequential).  Host buffers must stay valid until the ticket is waited and
- * should be pinned (stitch_b200_host_alloc) for the copies to be
- * asynchronous.  stitch_b200_wait blocks until the ticket's panorama is in
- * host memory and fills its report; a ticket older than the last 8 frames
- * is reported as MissingState. */
+ * stream) and return a ticket without waiting.  Four frames can be in
+ * flight (the context's pipeline slots): uploads and downloads of some
+ * frames overlap the kernels of others.  Frames are processed in submission
+ * order (the temporal state is sequential).  Host buffers must stay valid
+ * until the ticket is waited.  Pinned buffers (stitch_b200_host_alloc or
+ * stitch_b200_host_register) are copied by DMA directly; pageable ones (the
+ * reference's std::vector frames) go through the slot's pinned staging ring,
+ * filled and drained by the context's host copy workers, so the pipeline
+ * keeps its frames in flight either way.  stitch_b200_wait blocks until the
+ * ticket's panorama is in the caller's buffers and fills its report; a
+ * ticket older than the last 8 retired frames is reported as MissingState.
+ * Ticket numbers increase monotonically for the context's lifetime, across
+ * update_geometry / update_maps / rerefine. */
 int stitch_b200_submit(stitch_b200_ctx* ctx, const uint8_t* const* frames,
                        uint8_t* pano_rgb, uint8_t* pano_mask, long long* ticket);
 int stitch_b200_wait(stitch_b200_ctx* ctx, long long ticket,
@@ -386,6 +391,12 @@ int stitch_b200_set_error(int code, const char* what);
 /* Pinned host memory helpers (cudaHostAlloc / cudaFreeHost). */
 void* stitch_b200_host_alloc(size_t bytes);
 void stitch_b200_host_free(void* p);
+/* Page-lock a caller-owned buffer the caller keeps for the context's
+ * lifetime (its frame / output buffers), so submit/process copy it by DMA
+ * instead of through the context's pinned staging ring; unregister before
+ * freeing it. */
+int stitch_b200_host_register(void* p, size_t bytes);
+int stitch_b200_host_unregister(void* p);
 /* Device memory helpers for callers without another allocator. */
 void* stitch_b200_device_alloc(int device, size_t bytes);
 void stitch_b200_device_free(void* p);

@@ -148,6 +148,8 @@ SYMBOLS = [
     ("stitch_b200_set_error", C.c_int, [C.c_int, C.c_char_p]),
     ("stitch_b200_host_alloc", C.c_void_p, [C.c_size_t]),
     ("stitch_b200_host_free", None, [C.c_void_p]),
+    ("stitch_b200_host_register", C.c_int, [C.c_void_p, C.c_size_t]),
+    ("stitch_b200_host_unregister", C.c_int, [C.c_void_p]),
     ("stitch_b200_device_alloc", C.c_void_p, [C.c_int, C.c_size_t]),
     ("stitch_b200_device_free", None, [C.c_void_p]),
     ("stitch_b200_memcpy_h2d", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t]),

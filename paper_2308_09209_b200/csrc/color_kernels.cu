@@ -13,42 +13,14 @@
 // last CTA of each pair (grid-wide counter) performs the solve.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "device_math.cuh"
 #include "kernels.cuh"
 
 namespace stitch_b200_dev {
 
 __device__ __forceinline__ int sidx(int a, int b) { return a * 2 + (b > a ? b - 1 : b); }
-
-// Block-wide inclusive scan of 256 values (one per thread), u64.
-__device__ __forceinline__ unsigned long long block_scan256(unsigned long long x,
-                                                            unsigned long long* warp_tot) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) warp_tot[wid] = x;
-  __syncthreads();
-  unsigned long long add = 0;
-  for (int i = 0; i < wid; ++i) add += warp_tot[i];
-  __syncthreads();
-  return x + add;
-}
-
-__device__ __forceinline__ unsigned long long block_sum256(unsigned long long x,
-                                                           unsigned long long* warp_tot) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
-  if (lane == 0) warp_tot[wid] = x;
-  __syncthreads();
-  unsigned long long t = 0;
-  for (int i = 0; i < 8; ++i) t += warp_tot[i];
-  __syncthreads();
-  return t;
-}
 
 // The per-pair solve, executed by the pair's last CTA (256 threads):
 // histogram_specification (color_transfer.cpp:28-55), revised-row moments,
@@ -58,7 +30,6 @@ __device__ __forceinline__ unsigned long long block_sum256(unsigned long long x,
 __device__ void pair_solve(const PairDesc& p, int k, DevState* __restrict__ st) {
   __shared__ unsigned char lut[3][256];
   __shared__ unsigned long long cref[3][256];
-  __shared__ unsigned long long wtot[8];
   __shared__ unsigned long long mom[18];
   PairStats& in = st->stats[k];
   const int v = threadIdx.x;  // level owned by this thread
@@ -92,10 +63,31 @@ __device__ void pair_solve(const PairDesc& p, int k, DevState* __restrict__ st) 
   // LUT[c][v] = smallest u in [0, 255) with cum_ref[u] >= cum_src[v], else
   // 255 -- the reference's monotone scan (both histograms count the same n
   // jointly valid pixels, so its cross-multiplied compare reduces to this).
+  // The six inclusive prefix sums (3 reference, 3 source) are scanned
+  // together: warp shuffles, one exchange of the warp totals.
+  __shared__ unsigned long long wsum6[8][6];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned long long sc[6];
+  for (int c = 0; c < 3; ++c) {
+    sc[c] = hr[c];
+    sc[3 + c] = hs[c];
+  }
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1)
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, sc[j], o);
+      if (lane >= o) sc[j] += y;
+    }
+  if (lane == 31)
+    for (int j = 0; j < 6; ++j) wsum6[wid][j] = sc[j];
+  __syncthreads();
+  for (int i = 0; i < wid; ++i)
+    for (int j = 0; j < 6; ++j) sc[j] += wsum6[i][j];
   unsigned long long csrc[3];
   for (int c = 0; c < 3; ++c) {
-    cref[c][v] = block_scan256(hr[c], wtot);
-    csrc[c] = block_scan256(hs[c], wtot);
+    cref[c][v] = sc[c];
+    csrc[c] = sc[3 + c];
   }
   __syncthreads();
   for (int c = 0; c < 3; ++c) {
@@ -110,8 +102,11 @@ __device__ void pair_solve(const PairDesc& p, int k, DevState* __restrict__ st) 
     lut[c][v] = static_cast<unsigned char>(lo);
   }
   __syncthreads();
-  // exact integer moments
+  // exact integer moments: every thread's 18 terms, reduced per warp by
+  // shuffles, the 8 warp partials summed by thread 0 (integer: any order)
+  __shared__ unsigned long long wmom[8][18];
   const unsigned long long vv = static_cast<unsigned long long>(v);
+#pragma unroll
   for (int q = 0; q < 18; ++q) {
     const int which = q / 9, a = (q % 9) / 3, b = q % 3;
     unsigned long long x;
@@ -119,8 +114,15 @@ __device__ void pair_solve(const PairDesc& p, int k, DevState* __restrict__ st) 
       x = (a == b) ? vv * vv * hs[a] : vv * ss[sidx(a, b)];
     else
       x = (a == b) ? vv * lut[a][v] * hs[a] : static_cast<unsigned long long>(lut[b][v]) * ss[sidx(a, b)];
-    const unsigned long long tot = block_sum256(x, wtot);
-    if (threadIdx.x == 0) mom[q] = tot;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if (lane == 0) wmom[wid][q] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < 18) {
+    unsigned long long t = 0;
+    for (int i = 0; i < 8; ++i) t += wmom[i][threadIdx.x];
+    mom[threadIdx.x] = t;
   }
   __syncthreads();
   if (threadIdx.x != 0) return;
@@ -281,7 +283,10 @@ static inline int blocks_for(long long n, int per, int cap) {
 
 void launch_pair_color(const Geometry* g, DevState* st, const int* list, int n, int max_crop_px,
                        cudaStream_t s) {
-  dim3 grid(blocks_for(max_crop_px, 256 * 8, 1024), n);
+  // pixels per thread: fewer, fuller CTAs flush fewer partial tables into the
+  // pair's global accumulators (STITCH_B200_COLOR_PPT)
+  static const int ppt = std::max(1, env_int("STITCH_B200_COLOR_PPT", 8));
+  dim3 grid(blocks_for(max_crop_px, 256 * ppt, 1024), n);
   k_pair_color<<<grid, 256, 0, s>>>(g, st, list);
 }
 

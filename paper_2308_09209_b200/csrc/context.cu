@@ -1051,7 +1051,8 @@ int join_api_stream(Ctx* ctx) {
 int ensure_staging(Ctx* ctx, int slot) {
   if (!ctx->copier) {
     const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
-    ctx->copier.reset(new CopyPool(static_cast<int>(std::min(8u, hw / 2))));
+    const int n = env_int("STITCH_B200_COPY_THREADS", static_cast<int>(std::min(8u, hw / 2)));
+    ctx->copier.reset(new CopyPool(std::max(0, n)));
   }
   for (int v = 0; v < ctx->hg.n_views; ++v)
     if (!ctx->h_stage_in[slot][v])
@@ -1762,6 +1763,16 @@ void* stitch_b200_host_alloc(size_t bytes) {
 }
 
 void stitch_b200_host_free(void* p) { cudaFreeHost(p); }
+
+int stitch_b200_host_register(void* p, size_t bytes) {
+  CUDA_TRY(cudaHostRegister(p, bytes, cudaHostRegisterDefault));
+  return STITCH_B200_OK;
+}
+
+int stitch_b200_host_unregister(void* p) {
+  CUDA_TRY(cudaHostUnregister(p));
+  return STITCH_B200_OK;
+}
 
 void* stitch_b200_device_alloc(int device, size_t bytes) {
   void* p = nullptr;

@@ -17,6 +17,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <cstdlib>
 #include <utility>
 #include <vector>
 
@@ -206,6 +207,13 @@ struct DevState {
   unsigned int pair_done[kMaxPairs];  // CTA completion counters (last-CTA solve)
   unsigned int canvas_done;
 };
+
+// integer experiment / tuning switch from the environment (read once by the
+// callers, which keep it in a static)
+inline int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
 
 // ---- launchers (kernels.cu) ----
 void launch_expand(const Geometry* g, int n_views, long long max_px, cudaStream_t s);

@@ -1,11 +1,15 @@
-"""The contract-tolerant Jacobi sweep (STITCH_B200_HS_FAST=1: FMA contraction
-and the approximate reciprocal instead of the reference's unfused arithmetic
-and IEEE division) against the oracle at BASELINE.json's full sizes, C1-C4:
-every frame must stay within north_star's contract -- flows within 1e-3 px,
-colour matrices within 1e-4 relative, panoramas within +-1 LSB, masks,
-thresholds and rank flags identical.  Runs in a subprocess because the switch
-is read once per process; prints the max diffs as one JSON line (the
-numbers DESIGN.md quotes)."""
+"""Measurement (GPU box): the contract-tolerant Jacobi sweep
+(STITCH_B200_HS_FAST=1: FMA contraction and the approximate reciprocal instead
+of the reference's unfused arithmetic and IEEE division) against the oracle at
+BASELINE.json's full sizes, C1-C4, checked against north_star's contract --
+flows within 1e-3 px, colour matrices within 1e-4 relative, panoramas within
++-1 LSB, masks, thresholds and rank flags identical.  Each config runs in a
+subprocess (the switch is read once per process) and prints its max diffs
+as one RESULT JSON line; profiles/r02_fast_sweep_contract.json records the
+outcome (the variant breaks the contract, so the bit-exact sweep stays).
+
+    python -m pytest scripts/fast_sweep_contract.py -q -s
+"""
 import json
 import os
 import subprocess
