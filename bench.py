@@ -10,7 +10,7 @@ no collective on the frame path; "scaling": "weak").
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
 value  : aggregate panorama frames/s with the input frames resident in HBM
-         (stitch_b200_process_device_async, four frames in flight over the
+         (stitch_b200_process_device_async, one frame per pipeline slot in flight over the
          context's pipeline slots), CUDA-event timed on the context's API
          stream around a fork and a join, max over ranks.
 e2e    : the same metric through the reference-facing C-ABI calls with
@@ -50,7 +50,6 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-E2E_IN_FLIGHT = 4  # frames in flight on the host path (the context has 4 pipeline slots)
 METRIC = "stitched panorama frames/s & p50 ms/frame, 4x1080p cams; achieved HBM GB/s"
 UNIT = "frames/s"
 
@@ -364,7 +363,7 @@ def run_b200(args, rank, world, local_rank):
     # a fixed e2e sample (not --steps): long enough that the 4-deep pipeline
     # fill is negligible
     e2e_steps = max(1, args.e2e_steps)
-    depth = E2E_IN_FLIGHT
+    depth = lib.stitch_b200_slots(hs_[0])  # frames in flight = the context's slots
     outs = [(lib.stitch_b200_host_alloc(P * 3), lib.stitch_b200_host_alloc(P))
             for _ in range(depth)]
     tk = C.c_longlong()
@@ -505,7 +504,7 @@ def run_b200(args, rank, world, local_rank):
         "e2e": {"value": round(e2e_value, 2), "unit": UNIT,
                 "h2d_bytes_per_step": nv * frame_bytes, "d2h_bytes_per_step": P * 4,
                 "steps": e2e_steps, "streams": 1,
-                "api": f"stitch_b200_submit/stitch_b200_wait ({E2E_IN_FLIGHT} frames in flight, pinned host)",
+                "api": f"stitch_b200_submit/stitch_b200_wait ({depth} frames in flight, pinned host)",
                 "sync_process_value": round(e2e_sync, 2),
                 "pageable_value": round(e2e_pageable, 2),
                 "pageable_api": "same calls with pageable (numpy) frames and outputs, staged "

@@ -290,7 +290,8 @@ int stitch_b200_process_device(stitch_b200_ctx* ctx,
                                const uint8_t* const* dev_frames,
                                stitch_b200_report* report);
 
-/* Pipelined device-resident frames.  A context runs four pipeline slots on
+/* Pipelined device-resident frames.  A context runs its pipeline slots
+ * (stitch_b200_slots, 4 by default) on
  * their own streams; consecutive frames overlap except at the points where
  * the reference's temporal state orders them (the 3D-M window update, the
  * threshold history), which the slots chain in frame order.
@@ -298,7 +299,7 @@ int stitch_b200_process_device(stitch_b200_ctx* ctx,
  * stream; stitch_b200_fork makes subsequently enqueued frames wait for the
  * API stream's work so far, stitch_b200_join makes the API stream wait for
  * every frame enqueued so far.  The outputs of frame t stay valid until
- * frame t + 4 is enqueued. */
+ * frame t + slots is enqueued. */
 int stitch_b200_process_device_async(stitch_b200_ctx* ctx, const uint8_t* const* dev_frames);
 int stitch_b200_fork(stitch_b200_ctx* ctx);
 int stitch_b200_join(stitch_b200_ctx* ctx);
@@ -375,6 +376,9 @@ int stitch_b200_run_files(stitch_b200_ctx* ctx, const char* const* view_dirs,
 
 /* Number of views / a view's camera size of a context. */
 int stitch_b200_n_views(const stitch_b200_ctx* ctx);
+/* Pipeline slots (frames that can be in flight) of the context: 4 unless
+ * STITCH_B200_SLOTS (2..8) was set when it was built. */
+int stitch_b200_slots(const stitch_b200_ctx* ctx);
 int stitch_b200_view_size(const stitch_b200_ctx* ctx, int view, int* width, int* height);
 /* Validates one frame set before process/submit: n must equal the configured
  * views, every frame must have the size its view was initialized with

@@ -141,6 +141,7 @@ SYMBOLS = [
                                        C.POINTER(C.c_int)]),
     ("stitch_b200_write_png", C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
     ("stitch_b200_n_views", C.c_int, [C.c_void_p]),
+    ("stitch_b200_slots", C.c_int, [C.c_void_p]),
     ("stitch_b200_check_frames", C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int),
                                            C.POINTER(C.c_int), C.c_void_p]),
     ("stitch_b200_view_size", C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int),

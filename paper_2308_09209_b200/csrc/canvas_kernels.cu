@@ -338,7 +338,6 @@ __global__ void __launch_bounds__(256, kCanvasCtasPerSm) k_canvas(const __grid_c
                                                    uchar4* __restrict__ pano) {
   __shared__ unsigned int hist[3][256];
   __shared__ double mview[kMaxViews][9];
-  __shared__ bool last;
   for (int i = threadIdx.x; i < 256; i += blockDim.x) {
     hist[0][i] = 0;
     hist[1][i] = 0;
@@ -390,12 +389,7 @@ __global__ void __launch_bounds__(256, kCanvasCtasPerSm) k_canvas(const __grid_c
   for (int i = threadIdx.x; i < 256; i += blockDim.x)
     for (int c = 0; c < 3; ++c)
       if (hist[c][i]) atomicAdd(&st->pano_hist[c][i], hist[c][i]);
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(&st->canvas_done, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
+  if (!elect_last_cta(&st->canvas_done, gridDim.x)) return;
   if (threadIdx.x == 0) st->canvas_done = 0;
   balance_lut(g, st);
 }

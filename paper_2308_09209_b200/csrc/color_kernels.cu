@@ -190,23 +190,35 @@ __device__ void pair_solve(const PairDesc& p, int k, DevState* __restrict__ st) 
   st->report.rank_deficient[k] = degraded;
 }
 
+// Pixels per thread (grid = ceil(n / (256 * kColorPpt)) CTAs per pair): each
+// CTA then sees at most 256 * kColorPpt = 2048 pixels, which bounds its
+// per-level partial sums (<= 2048 * 255 < 2^19) and counts (<= 2048 < 2^12)
+// so a count and a conditional sum share one 32-bit shared counter.
+constexpr int kColorPpt = 8;
+constexpr int kSumBits = 19;
+constexpr unsigned kSumMask = (1u << kSumBits) - 1u;
+
 // grid: (blocks per pair, pairs of this depth); 256 threads.
+// Per jointly valid pixel and channel b (bin v = x_b): the count, the sum
+// of the lower other channel x_a1 and of the higher one x_a2 land in the
+// same bin, so the count and x_a1 share one packed counter
+// (count << 19 | sum) and x_a2 gets its own: 6 shared atomics for the
+// source side instead of 9, plus 3 for the reference histogram.
 __global__ void __launch_bounds__(256) k_pair_color(const Geometry* __restrict__ g,
                                                     DevState* __restrict__ st,
                                                     const int* __restrict__ list) {
-  __shared__ unsigned int hs[3][256];
+  __shared__ unsigned int pk[3][256];  // count << 19 | sum of x_a1, bin x_b
+  __shared__ unsigned int s2[3][256];  // sum of x_a2, bin x_b
   __shared__ unsigned int hr[3][256];
-  __shared__ unsigned int ss[6][256];
   __shared__ unsigned int cnt;
-  __shared__ bool last;
   const int k = list[blockIdx.y];
   const PairDesc& p = g->pairs[k];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) {
     for (int c = 0; c < 3; ++c) {
-      hs[c][i] = 0;
+      pk[c][i] = 0;
+      s2[c][i] = 0;
       hr[c][i] = 0;
     }
-    for (int c = 0; c < 6; ++c) ss[c][i] = 0;
   }
   if (threadIdx.x == 0) cnt = 0;
   __syncthreads();
@@ -236,18 +248,16 @@ __global__ void __launch_bounds__(256) k_pair_color(const Geometry* __restrict__
       uchar4 b = pb[j];
       if (!a.w || !b.w) continue;
       if (correct_partner) b = apply_matrix(mp, b);
-      const unsigned int xa[3] = {a.x, a.y, a.z};
-      atomicAdd(&hs[0][a.x], 1u);
-      atomicAdd(&hs[1][a.y], 1u);
-      atomicAdd(&hs[2][a.z], 1u);
+      // bin channel 0: a1 = 1, a2 = 2; channel 1: a1 = 0, a2 = 2; channel 2: a1 = 0, a2 = 1
+      atomicAdd(&pk[0][a.x], (1u << kSumBits) + a.y);
+      atomicAdd(&s2[0][a.x], static_cast<unsigned>(a.z));
+      atomicAdd(&pk[1][a.y], (1u << kSumBits) + a.x);
+      atomicAdd(&s2[1][a.y], static_cast<unsigned>(a.z));
+      atomicAdd(&pk[2][a.z], (1u << kSumBits) + a.x);
+      atomicAdd(&s2[2][a.z], static_cast<unsigned>(a.y));
       atomicAdd(&hr[0][b.x], 1u);
       atomicAdd(&hr[1][b.y], 1u);
       atomicAdd(&hr[2][b.z], 1u);
-#pragma unroll
-      for (int ca = 0; ca < 3; ++ca)
-#pragma unroll
-        for (int cb = 0; cb < 3; ++cb)
-          if (ca != cb) atomicAdd(&ss[sidx(ca, cb)][xa[cb]], xa[ca]);
       ++local;
     }
   }
@@ -256,20 +266,18 @@ __global__ void __launch_bounds__(256) k_pair_color(const Geometry* __restrict__
   PairStats& out = st->stats[k];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) {
     for (int c = 0; c < 3; ++c) {
-      if (hs[c][i]) atomicAdd(&out.hs[c][i], hs[c][i]);
+      const unsigned w = pk[c][i];
+      const unsigned count = w >> kSumBits, sum1 = w & kSumMask, sum2 = s2[c][i];
+      const int a1 = c == 0 ? 1 : 0, a2 = c == 2 ? 1 : 2;
+      if (count) atomicAdd(&out.hs[c][i], count);
       if (hr[c][i]) atomicAdd(&out.hr[c][i], hr[c][i]);
+      if (sum1) atomicAdd(&out.s[sidx(a1, c)][i], static_cast<unsigned long long>(sum1));
+      if (sum2) atomicAdd(&out.s[sidx(a2, c)][i], static_cast<unsigned long long>(sum2));
     }
-    for (int c = 0; c < 6; ++c)
-      if (ss[c][i]) atomicAdd(&out.s[c][i], static_cast<unsigned long long>(ss[c][i]));
   }
   if (threadIdx.x == 0 && cnt) atomicAdd(&out.n, static_cast<unsigned long long>(cnt));
   // last CTA of this pair performs the solve
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(&st->pair_done[k], 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
+  if (!elect_last_cta(&st->pair_done[k], gridDim.x)) return;
   if (threadIdx.x == 0) st->pair_done[k] = 0;
   pair_solve(p, k, st);
 }
@@ -283,10 +291,9 @@ static inline int blocks_for(long long n, int per, int cap) {
 
 void launch_pair_color(const Geometry* g, DevState* st, const int* list, int n, int max_crop_px,
                        cudaStream_t s) {
-  // pixels per thread: fewer, fuller CTAs flush fewer partial tables into the
-  // pair's global accumulators (STITCH_B200_COLOR_PPT)
-  static const int ppt = std::max(1, env_int("STITCH_B200_COLOR_PPT", 8));
-  dim3 grid(blocks_for(max_crop_px, 256 * ppt, 1024), n);
+  // no cap on the CTA count: the packed counters need <= 256 * kColorPpt
+  // pixels per CTA (measured: 16 or 32 pixels per thread are not faster)
+  dim3 grid(blocks_for(max_crop_px, 256 * kColorPpt, 1 << 30), n);
   k_pair_color<<<grid, 256, 0, s>>>(g, st, list);
 }
 

@@ -184,8 +184,11 @@ struct Ctx {
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;  // the API stream (process_device, profile, debug)
-  static constexpr int kSlots = 4;
-  SlotRes slot[kSlots];
+  // pipeline slots: frames in flight (STITCH_B200_SLOTS, 2..kMaxSlots;
+  // default 4), fixed when the context is built
+  static constexpr int kMaxSlots = 8;
+  int n_slots = 4;
+  SlotRes slot[kMaxSlots];
   Geometry hg{};  // metadata (slot 0's mirror; buffers: use slot[s].hg)
   TemporalState* dtemp = nullptr;
   stitch_b200_init init{};  // copy (theta pointers re-pointed at host copies)
@@ -195,9 +198,9 @@ struct Ctx {
   std::uint8_t* d_frames[kMaxViews] = {};
   size_t frame_bytes[kMaxViews] = {};
   // per slot: inputs, outputs, stage events, report
-  std::uint8_t* d_in[kSlots][kMaxViews] = {};
-  std::uint8_t* d_out_rgb[kSlots] = {};
-  std::uint8_t* d_out_mask[kSlots] = {};
+  std::uint8_t* d_in[kMaxSlots][kMaxViews] = {};
+  std::uint8_t* d_out_rgb[kMaxSlots] = {};
+  std::uint8_t* d_out_mask[kMaxSlots] = {};
   long long n_px = 0;
   int max_crop_px = 0;
   int max_crop_w = 0, max_crop_h = 0;
@@ -209,16 +212,16 @@ struct Ctx {
   int seg_begin[SlotRes::kSegs + 1] = {};  // plan index ranges of the segments
   int* d_lists = nullptr;
   int launches = 0;
-  cudaEvent_t ev[kSlots][6] = {};
+  cudaEvent_t ev[kMaxSlots][6] = {};
   cudaStream_t h2d = nullptr, d2h = nullptr;
-  cudaEvent_t h2d_done[kSlots] = {}, comp_done[kSlots] = {}, d2h_done[kSlots] = {};
+  cudaEvent_t h2d_done[kMaxSlots] = {}, comp_done[kMaxSlots] = {}, d2h_done[kMaxSlots] = {};
   // frame-order points between slots: colour solves done, canvas done
-  cudaEvent_t color_done[kSlots] = {}, canvas_done[kSlots] = {};
+  cudaEvent_t color_done[kMaxSlots] = {}, canvas_done[kMaxSlots] = {};
   cudaEvent_t fork_ev = nullptr;
   long long seq = 0;                       // frames submitted (any API)
-  long long slot_ticket[kSlots];  // ticket occupying each slot
-  bool slot_pending[kSlots];
-  bool slot_joined[kSlots];  // the API stream waited for the slot's frame
+  long long slot_ticket[kMaxSlots];  // ticket occupying each slot
+  bool slot_pending[kMaxSlots];
+  bool slot_joined[kMaxSlots];  // the API stream waited for the slot's frame
   std::vector<std::pair<long long, stitch_b200_report>> done_reports;
   int last_slot = 0;
   // pinned ring for device-frame pointer tables
@@ -229,17 +232,17 @@ struct Ctx {
   // pageable caller buffers: pinned staging per slot (allocated on first
   // use), the caller's output pointers to fill when the slot retires, and
   // the copy workers
-  std::uint8_t* h_stage_in[kSlots][kMaxViews] = {};
-  std::uint8_t* h_stage_rgb[kSlots] = {};
-  std::uint8_t* h_stage_mask[kSlots] = {};
-  std::uint8_t* user_rgb[kSlots] = {};
-  std::uint8_t* user_mask[kSlots] = {};
+  std::uint8_t* h_stage_in[kMaxSlots][kMaxViews] = {};
+  std::uint8_t* h_stage_rgb[kMaxSlots] = {};
+  std::uint8_t* h_stage_mask[kMaxSlots] = {};
+  std::uint8_t* user_rgb[kMaxSlots] = {};
+  std::uint8_t* user_mask[kMaxSlots] = {};
   std::unique_ptr<CopyPool> copier;
   std::vector<int> pair_levels;
   float2* d_zero = nullptr;
 
   Ctx() {
-    for (int s = 0; s < kSlots; ++s) {
+    for (int s = 0; s < kMaxSlots; ++s) {
       slot_ticket[s] = -1;
       slot_pending[s] = false;
       slot_joined[s] = true;
@@ -252,7 +255,7 @@ struct Ctx {
       if (S.cs) cudaStreamSynchronize(S.cs);
     if (h2d) cudaStreamSynchronize(h2d);
     if (d2h) cudaStreamSynchronize(d2h);
-    for (int s = 0; s < kSlots; ++s) {
+    for (int s = 0; s < kMaxSlots; ++s) {
       for (int g = 0; g < SlotRes::kSegs; ++g) {
         if (slot[s].exec[g]) cudaGraphExecDestroy(slot[s].exec[g]);
         if (slot[s].graph[g]) cudaGraphDestroy(slot[s].graph[g]);
@@ -271,7 +274,7 @@ struct Ctx {
     for (void* p : allocs) cudaFree(p);
     if (h_ptr_ring) cudaFreeHost(h_ptr_ring);
     if (h_report) cudaFreeHost(h_report);
-    for (int s = 0; s < kSlots; ++s) {
+    for (int s = 0; s < kMaxSlots; ++s) {
       for (auto* q : h_stage_in[s])
         if (q) cudaFreeHost(q);
       if (h_stage_rgb[s]) cudaFreeHost(h_stage_rgb[s]);
@@ -430,6 +433,10 @@ int build_context(const stitch_b200_init* in, int device,
   if (rc) return rc;
   auto ctx = std::make_unique<Ctx>();
   ctx->device = device;
+  {
+    static const int slots = env_int("STITCH_B200_SLOTS", 4);
+    ctx->n_slots = std::min(Ctx::kMaxSlots, std::max(2, slots));
+  }
   CUDA_TRY(cudaSetDevice(device));
   CUDA_TRY(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
   CUDA_TRY(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
@@ -495,7 +502,7 @@ int build_context(const stitch_b200_init* in, int device,
   }
   const Geometry base = g;
   std::vector<float*> theta_dev(in->n_pairs, nullptr);
-  for (int sl = 0; sl < Ctx::kSlots; ++sl) {
+  for (int sl = 0; sl < ctx->n_slots; ++sl) {
     SlotRes& S = ctx->slot[sl];
     Geometry& g = S.hg;
     g = base;
@@ -505,7 +512,7 @@ int build_context(const stitch_b200_init* in, int device,
       if (sl == 0) {
         CUDA_TRY(ctx->alloc(&ctx->d_frames[v], ctx->frame_bytes[v]));
         ctx->d_in[0][v] = ctx->d_frames[v];
-        for (int s2 = 1; s2 < Ctx::kSlots; ++s2)
+        for (int s2 = 1; s2 < ctx->n_slots; ++s2)
           CUDA_TRY(ctx->alloc(&ctx->d_in[s2][v], ctx->frame_bytes[v]));
       }
       g.frames[v] = ctx->d_in[sl][v];
@@ -859,12 +866,12 @@ int build_context(const stitch_b200_init* in, int device,
       launch_canvas_class(ctx->slot[0].cparams, cls, ctx->stream);
       CUDA_TRY(cudaGetLastError());
       CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-      for (int sl = 0; sl < Ctx::kSlots; ++sl) ctx->slot[sl].cparams.cls = cls;
+      for (int sl = 0; sl < ctx->n_slots; ++sl) ctx->slot[sl].cparams.cls = cls;
     }
   }
   CUDA_TRY(prepare_hs(ctx->sweeps));
   for (int j = 1; j <= ctx->sweeps; ++j) CUDA_TRY(prepare_hs(j));
-  for (int sl = 0; sl < Ctx::kSlots; ++sl) {
+  for (int sl = 0; sl < ctx->n_slots; ++sl) {
     for (auto& e : ctx->ev[sl]) CUDA_TRY(cudaEventCreate(&e));
     CUDA_TRY(cudaEventCreateWithFlags(&ctx->h2d_done[sl], cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&ctx->comp_done[sl], cudaEventDisableTiming));
@@ -880,7 +887,7 @@ int build_context(const stitch_b200_init* in, int device,
   CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_ptr_ring),
                          sizeof(void*) * kMaxViews * 16, cudaHostAllocDefault));
   CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_report),
-                         sizeof(DevReport) * Ctx::kSlots, cudaHostAllocDefault));
+                         sizeof(DevReport) * ctx->n_slots, cudaHostAllocDefault));
 
   // ---- the plan's four segments: front | colour | mid (flow) | back ----
   {
@@ -902,7 +909,7 @@ int build_context(const stitch_b200_init* in, int device,
   }
   // ---- capture each slot's segments once ----
   int launches = 0;
-  for (int sl = 0; sl < Ctx::kSlots; ++sl) {
+  for (int sl = 0; sl < ctx->n_slots; ++sl) {
     SlotRes& S = ctx->slot[sl];
     cudaStream_t s = S.cs;
     launches = 0;
@@ -1001,7 +1008,7 @@ int retire_slot(Ctx* ctx, int slot) {
 // frame's canvas.  Everything else of consecutive frames overlaps.
 int enqueue_frame(Ctx* ctx, int slot, const std::uint8_t* const* dev_in) {
   SlotRes& S = ctx->slot[slot];
-  const int prev = (slot + Ctx::kSlots - 1) % Ctx::kSlots;
+  const int prev = (slot + ctx->n_slots - 1) % ctx->n_slots;
   CUDA_TRY(cudaStreamWaitEvent(S.cs, ctx->d2h_done[slot], 0));
   int rc = set_frame_pointers(ctx, slot, dev_in);
   if (rc) return rc;
@@ -1039,7 +1046,7 @@ int fork_api_stream(Ctx* ctx) {
 
 // The API stream waits for every frame enqueued so far.
 int join_api_stream(Ctx* ctx) {
-  for (int sl = 0; sl < Ctx::kSlots; ++sl)
+  for (int sl = 0; sl < ctx->n_slots; ++sl)
     if (!ctx->slot_joined[sl]) {
       CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->comp_done[sl], 0));
       ctx->slot_joined[sl] = true;
@@ -1051,7 +1058,9 @@ int join_api_stream(Ctx* ctx) {
 int ensure_staging(Ctx* ctx, int slot) {
   if (!ctx->copier) {
     const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
-    const int n = env_int("STITCH_B200_COPY_THREADS", static_cast<int>(std::min(8u, hw / 2)));
+    // measured at C2 on a 16-core host: 8 workers 786 fps, 14 workers 826 fps
+    // (pinned 895); the copies are bound by host memory bandwidth
+    const int n = env_int("STITCH_B200_COPY_THREADS", static_cast<int>(std::min(14u, hw > 4 ? hw - 2 : 2u)));
     ctx->copier.reset(new CopyPool(std::max(0, n)));
   }
   for (int v = 0; v < ctx->hg.n_views; ++v)
@@ -1072,7 +1081,7 @@ int ensure_staging(Ctx* ctx, int slot) {
 // directly; pageable ones through the slot's pinned staging ring.
 int submit_host(Ctx* ctx, const std::uint8_t* const* frames, std::uint8_t* pano_rgb,
                 std::uint8_t* pano_mask, long long* ticket) {
-  const int slot = static_cast<int>(ctx->seq % Ctx::kSlots);
+  const int slot = static_cast<int>(ctx->seq % ctx->n_slots);
   int rc = retire_slot(ctx, slot);
   if (rc) return rc;
   for (int v = 0; v < ctx->hg.n_views; ++v)
@@ -1128,7 +1137,7 @@ int wait_ticket(Ctx* ctx, long long ticket, stitch_b200_report* report) {
       if (report) *report = d.second;
       return STITCH_B200_OK;
     }
-  for (int sl = 0; sl < Ctx::kSlots; ++sl)
+  for (int sl = 0; sl < ctx->n_slots; ++sl)
     if (ctx->slot_pending[sl] && ctx->slot_ticket[sl] == ticket) {
       int rc = retire_slot(ctx, sl);
       if (rc) return rc;
@@ -1457,7 +1466,7 @@ static int carry_into(stitch_b200_ctx* h, std::unique_ptr<Ctx>& fresh) {
   // retire every pending host-path frame so its report survives the swap,
   // and keep ticket numbers monotonic: tickets issued before the swap stay
   // waitable and can never alias a later frame
-  for (int sl = 0; sl < Ctx::kSlots; ++sl) {
+  for (int sl = 0; sl < ctx->n_slots; ++sl) {
     rc = retire_slot(ctx, sl);
     if (rc) return rc;
   }
@@ -1560,6 +1569,8 @@ int stitch_b200_n_pairs(const stitch_b200_ctx* h) { return h->c->hg.n_pairs; }
 
 int stitch_b200_n_views(const stitch_b200_ctx* h) { return h->c->hg.n_views; }
 
+int stitch_b200_slots(const stitch_b200_ctx* h) { return h->c->n_slots; }
+
 int stitch_b200_view_size(const stitch_b200_ctx* h, int view, int* width, int* height) {
   const Ctx* ctx = h->c.get();
   if (view < 0 || view >= ctx->hg.n_views)
@@ -1648,7 +1659,7 @@ int stitch_b200_process_device(stitch_b200_ctx* h, const uint8_t* const* dev_fra
                                stitch_b200_report* report) {
   Ctx* ctx = h->c.get();
   CUDA_TRY(cudaSetDevice(ctx->device));
-  const int slot = static_cast<int>(ctx->seq % Ctx::kSlots);
+  const int slot = static_cast<int>(ctx->seq % ctx->n_slots);
   int rc = retire_slot(ctx, slot);
   if (rc) return rc;
   // stream-ordered on the API stream: inputs written there are seen, and
@@ -1670,7 +1681,7 @@ int stitch_b200_process_device(stitch_b200_ctx* h, const uint8_t* const* dev_fra
 int stitch_b200_process_device_async(stitch_b200_ctx* h, const uint8_t* const* dev_frames) {
   Ctx* ctx = h->c.get();
   CUDA_TRY(cudaSetDevice(ctx->device));
-  const int slot = static_cast<int>(ctx->seq % Ctx::kSlots);
+  const int slot = static_cast<int>(ctx->seq % ctx->n_slots);
   int rc = retire_slot(ctx, slot);
   if (rc) return rc;
   rc = enqueue_frame(ctx, slot, dev_frames);
@@ -1696,7 +1707,7 @@ int stitch_b200_profile_frame(stitch_b200_ctx* h, const uint8_t* const* dev_fram
   Ctx* ctx = h->c.get();
   CUDA_TRY(cudaSetDevice(ctx->device));
   // eager run on slot 0 after draining the pipeline
-  for (int sl = 0; sl < Ctx::kSlots; ++sl) {
+  for (int sl = 0; sl < ctx->n_slots; ++sl) {
     int rc = retire_slot(ctx, sl);
     if (rc) return -rc;
   }
