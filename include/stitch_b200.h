@@ -97,7 +97,9 @@ typedef struct {
 } stitch_b200_config;
 
 /* Fill a config with the reference defaults (pipeline.hpp:23-44,
- * color_balance.hpp:19-25, flow.hpp:29-34) and refine disabled. */
+ * color_balance.hpp:19-25, flow.hpp:29-34), feature refinement included
+ * (refine_enabled = 1, pipeline.hpp:24: initialize with the first frames,
+ * stitch_b200_initialize_frames). */
 void stitch_b200_config_defaults(stitch_b200_config* cfg);
 
 /* POD snapshot of an initialised PipelineState: the exact values the

@@ -44,18 +44,6 @@ struct State {
 
 }  // namespace
 
-// image_io.cpp needs libpng (absent) and is left out of the build; only
-// SynthScene::write_scene (synth.cpp) references these two, and the harness
-// never calls it.  They throw instead of writing anything.
-namespace stitch {
-std::string sequence_name(const std::string&, int, const std::string&) {
-  throw StitchError(ErrorCode::IoError, "image_io.cpp is not part of the oracle/_ref build");
-}
-void write_png(const std::filesystem::path&, const Frame&) {
-  throw StitchError(ErrorCode::IoError, "image_io.cpp is not part of the oracle/_ref build");
-}
-}  // namespace stitch
-
 extern "C" {
 
 // Mirrors stitch::SynthSpec (synth.hpp:31-44) as a POD.
