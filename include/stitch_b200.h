@@ -402,6 +402,9 @@ void stitch_b200_host_free(void* p);
  * instead of through the context's pinned staging ring; unregister before
  * freeing it. */
 int stitch_b200_host_register(void* p, size_t bytes);
+/* Test entry (host only): `rounds` back-to-back batches through the host
+ * copy pool that stages pageable buffers, every byte verified. */
+int stitch_b200_debug_copy_pool(int workers, int rounds, size_t bytes);
 int stitch_b200_host_unregister(void* p);
 /* Device memory helpers for callers without another allocator. */
 void* stitch_b200_device_alloc(int device, size_t bytes);

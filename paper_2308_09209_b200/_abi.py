@@ -150,6 +150,7 @@ SYMBOLS = [
     ("stitch_b200_host_alloc", C.c_void_p, [C.c_size_t]),
     ("stitch_b200_host_free", None, [C.c_void_p]),
     ("stitch_b200_host_register", C.c_int, [C.c_void_p, C.c_size_t]),
+    ("stitch_b200_debug_copy_pool", C.c_int, [C.c_int, C.c_int, C.c_size_t]),
     ("stitch_b200_host_unregister", C.c_int, [C.c_void_p]),
     ("stitch_b200_device_alloc", C.c_void_p, [C.c_int, C.c_size_t]),
     ("stitch_b200_device_free", None, [C.c_void_p]),

@@ -104,67 +104,73 @@ class CopyPool {
   }
 
   // Copies every (dst, src, n), split into ~1 MiB chunks; the calling thread
-  // works too.  Returns when all bytes have landed.
+  // works too.  Returns when all bytes have landed.  Each call is its own
+  // batch, shared with the workers that join it, so a worker that wakes late
+  // can only ever claim chunks of a batch it holds alive.
   void run(const std::vector<Job>& jobs) {
     constexpr size_t kChunk = size_t(1) << 20;
-    std::vector<Job> chunks;
+    auto b = std::make_shared<Batch>();
     for (const Job& j : jobs)
       for (size_t o = 0; o < j.n; o += kChunk)
-        chunks.push_back({static_cast<char*>(j.dst) + o, static_cast<const char*>(j.src) + o,
-                          std::min(kChunk, j.n - o)});
-    if (chunks.empty()) return;
-    std::unique_lock<std::mutex> lk(mu_);
-    work_ = &chunks;
-    next_.store(0);
-    left_ = chunks.size();
-    ++gen_;
-    lk.unlock();
+        b->chunks.push_back({static_cast<char*>(j.dst) + o, static_cast<const char*>(j.src) + o,
+                             std::min(kChunk, j.n - o)});
+    if (b->chunks.empty()) return;
+    if (b->chunks.size() == 1 || th_.empty()) {  // small: no hand-off
+      for (const Job& c : b->chunks) std::memcpy(c.dst, c.src, c.n);
+      return;
+    }
+    b->left = b->chunks.size();
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      batch_ = b;
+      ++gen_;
+    }
     cv_.notify_all();
-    drain();
-    lk.lock();
-    done_cv_.wait(lk, [&] { return left_ == 0; });
-    work_ = nullptr;
+    drain(*b);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return b->left == 0; });
+    if (batch_ == b) batch_.reset();
   }
 
  private:
-  void drain() {
-    const std::vector<Job>* w;
-    {
-      std::lock_guard<std::mutex> lk(mu_);
-      w = work_;
-    }
-    if (!w) return;
+  struct Batch {
+    std::vector<Job> chunks;
+    std::atomic<size_t> next{0};
+    size_t left = 0;  // guarded by mu_
+  };
+
+  void drain(Batch& b) {
     size_t did = 0;
-    for (size_t i = next_.fetch_add(1); i < w->size(); i = next_.fetch_add(1)) {
-      std::memcpy((*w)[i].dst, (*w)[i].src, (*w)[i].n);
+    for (size_t i = b.next.fetch_add(1); i < b.chunks.size(); i = b.next.fetch_add(1)) {
+      std::memcpy(b.chunks[i].dst, b.chunks[i].src, b.chunks[i].n);
       ++did;
     }
     if (did) {
       std::lock_guard<std::mutex> lk(mu_);
-      left_ -= did;
-      if (left_ == 0) done_cv_.notify_all();
+      b.left -= did;
+      if (b.left == 0) done_cv_.notify_all();
     }
   }
 
   void loop() {
     unsigned long long seen = 0;
     for (;;) {
+      std::shared_ptr<Batch> b;
       {
         std::unique_lock<std::mutex> lk(mu_);
         cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
         if (stop_) return;
         seen = gen_;
+        b = batch_;
       }
-      drain();
+      if (b) drain(*b);
     }
   }
 
   std::vector<std::thread> th_;
   std::mutex mu_;
   std::condition_variable cv_, done_cv_;
-  const std::vector<Job>* work_ = nullptr;
-  std::atomic<size_t> next_{0};
-  size_t left_ = 0;
+  std::shared_ptr<Batch> batch_;
   unsigned long long gen_ = 0;
   bool stop_ = false;
 };
@@ -1031,7 +1037,7 @@ int enqueue_frame(Ctx* ctx, int slot, const std::uint8_t* const* dev_in) {
 // Wait for all work of the context (uploads, frames, downloads, API stream).
 int sync_all(Ctx* ctx) {
   CUDA_TRY(cudaStreamSynchronize(ctx->h2d));
-  for (auto& S : ctx->slot) CUDA_TRY(cudaStreamSynchronize(S.cs));
+  for (int sl = 0; sl < ctx->n_slots; ++sl) CUDA_TRY(cudaStreamSynchronize(ctx->slot[sl].cs));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->d2h));
   return STITCH_B200_OK;
@@ -1040,7 +1046,8 @@ int sync_all(Ctx* ctx) {
 // The slot streams wait for the work enqueued so far on the API stream.
 int fork_api_stream(Ctx* ctx) {
   CUDA_TRY(cudaEventRecord(ctx->fork_ev, ctx->stream));
-  for (auto& S : ctx->slot) CUDA_TRY(cudaStreamWaitEvent(S.cs, ctx->fork_ev, 0));
+  for (int sl = 0; sl < ctx->n_slots; ++sl)
+    CUDA_TRY(cudaStreamWaitEvent(ctx->slot[sl].cs, ctx->fork_ev, 0));
   return STITCH_B200_OK;
 }
 
@@ -1711,7 +1718,7 @@ int stitch_b200_profile_frame(stitch_b200_ctx* h, const uint8_t* const* dev_fram
     int rc = retire_slot(ctx, sl);
     if (rc) return -rc;
   }
-  for (auto& S : ctx->slot) CUDA_TRY(cudaStreamSynchronize(S.cs));
+  for (int sl = 0; sl < ctx->n_slots; ++sl) CUDA_TRY(cudaStreamSynchronize(ctx->slot[sl].cs));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->d2h));
   int rc = set_frame_pointers(ctx, 0, dev_frames);
@@ -1774,6 +1781,22 @@ void* stitch_b200_host_alloc(size_t bytes) {
 }
 
 void stitch_b200_host_free(void* p) { cudaFreeHost(p); }
+
+int stitch_b200_debug_copy_pool(int workers, int rounds, size_t bytes) {
+  // host only (no device): back-to-back batches of varying sizes through one
+  // pool, every destination byte checked after each batch
+  CopyPool pool(workers);
+  std::vector<unsigned char> src(bytes), dst(bytes);
+  for (int r = 0; r < rounds; ++r) {
+    const size_t n = bytes - (static_cast<size_t>(r) * 7919u) % (bytes / 2 + 1);
+    for (size_t i = 0; i < n; i += 4096) src[i] = static_cast<unsigned char>(r + i / 4096);
+    const size_t half = n / 2;
+    pool.run({{dst.data(), src.data(), half}, {dst.data() + half, src.data() + half, n - half}});
+    if (std::memcmp(dst.data(), src.data(), n) != 0)
+      return fail(STITCH_B200_InputMismatch, "copy pool produced wrong bytes");
+  }
+  return STITCH_B200_OK;
+}
 
 int stitch_b200_host_register(void* p, size_t bytes) {
   CUDA_TRY(cudaHostRegister(p, bytes, cudaHostRegisterDefault));

@@ -114,3 +114,12 @@ def test_missing_library_fails_loudly(tmp_path):
             _abi.load(str(tmp_path / "nope.so"))
     finally:
         _abi._lib = _abi._lib_saved
+
+
+@pytest.mark.parametrize("workers", [0, 1, 3, 14])
+def test_host_copy_pool_back_to_back_batches(workers):
+    """The pool that stages pageable frames: thousands of back-to-back
+    batches (the submit / wait pattern), every byte checked -- a late worker
+    must never touch a finished batch (host only, no GPU needed)."""
+    lib = _abi.load()
+    assert lib.stitch_b200_debug_copy_pool(workers, 3000, 3 << 20) == 0, lib.stitch_b200_last_error()
