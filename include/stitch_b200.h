@@ -147,7 +147,13 @@ typedef struct {
   int threshold_m1[3], threshold_m2[3];
   int balanced; /* 0 when the panorama histogram was empty */
   /* Stage::{GeometricWarping, ColorCorrection, LocalWarping, ImageBlending}
-   * (report.hpp:11-17), device milliseconds from CUDA events. */
+   * (report.hpp:11-17): device milliseconds between CUDA events recorded at
+   * the stage boundaries of this frame's slot.  With several frames in
+   * flight these are wall intervals on a GPU shared with the other frames'
+   * kernels (and include waits on the previous frame's colour solve /
+   * canvas), not the stage's exclusive cost the reference's
+   * FrameReport.times measures on one thread; the per-kernel cost of a frame
+   * run alone is what stitch_b200_profile_frame reports. */
   double stage_ms[4];
 } stitch_b200_report;
 

@@ -15,14 +15,10 @@
 
 #include <algorithm>
 
-#include <cooperative_groups.h>
-
 #include "device_math.cuh"
 #include "kernels.cuh"
 
 namespace stitch_b200_dev {
-
-namespace cg = cooperative_groups;
 
 __device__ __forceinline__ int sidx(int a, int b) { return a * 2 + (b > a ? b - 1 : b); }
 
@@ -202,30 +198,19 @@ constexpr int kColorPpt = 8;
 constexpr int kSumBits = 19;
 constexpr unsigned kSumMask = (1u << kSumBits) - 1u;
 
-// CTAs of a pair reduce their tables in clusters of kColorCluster over
-// distributed shared memory before one CTA per cluster flushes to the pair's
-// global accumulators: 8x fewer same-address global atomics, whose drain the
-// last-CTA election's fence used to wait on (ncu, r02).
-constexpr int kColorCluster = 8;
-
-// grid: (blocks per pair, pairs of this depth), clusters of kColorCluster
-// CTAs along x; 256 threads.
+// grid: (blocks per pair, pairs of this depth); 256 threads.
 // Per jointly valid pixel and channel b (bin v = x_b): the count, the sum
 // of the lower other channel x_a1 and of the higher one x_a2 land in the
 // same bin, so the count and x_a1 share one packed counter
 // (count << 19 | sum) and x_a2 gets its own: 6 shared atomics for the
 // source side instead of 9, plus 3 for the reference histogram.
-__global__ void __cluster_dims__(kColorCluster, 1, 1) __launch_bounds__(256)
-    k_pair_color(const Geometry* __restrict__ g, DevState* __restrict__ st,
-                 const int* __restrict__ list) {
+__global__ void __launch_bounds__(256) k_pair_color(const Geometry* __restrict__ g,
+                                                    DevState* __restrict__ st,
+                                                    const int* __restrict__ list) {
   __shared__ unsigned int pk[3][256];  // count << 19 | sum of x_a1, bin x_b
   __shared__ unsigned int s2[3][256];  // sum of x_a2, bin x_b
   __shared__ unsigned int hr[3][256];
-  // the cluster's merged tables (used in rank 0): hs, hr, 6 conditional sums
-  __shared__ unsigned int mg[12][256];
-  __shared__ unsigned int cnt, ccnt;  // this CTA's / the cluster's (rank 0) pixel count
-  cg::cluster_group cluster = cg::this_cluster();
-  const unsigned rank = cluster.block_rank();
+  __shared__ unsigned int cnt;
   const int k = list[blockIdx.y];
   const PairDesc& p = g->pairs[k];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) {
@@ -234,11 +219,9 @@ __global__ void __cluster_dims__(kColorCluster, 1, 1) __launch_bounds__(256)
       s2[c][i] = 0;
       hr[c][i] = 0;
     }
-    for (int c = 0; c < 12; ++c) mg[c][i] = 0;
   }
-  if (threadIdx.x == 0) cnt = ccnt = 0;
-  // rank 0's merged tables are zero before any CTA of the cluster adds to them
-  cluster.sync();
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
   // the partner is already corrected when it is not the reference (chain)
   const bool correct_partner = p.partner != g->reference;
   const double* mp = st->mview[p.partner];
@@ -280,34 +263,21 @@ __global__ void __cluster_dims__(kColorCluster, 1, 1) __launch_bounds__(256)
   }
   atomicAdd(&cnt, local);
   __syncthreads();
-  // unpack and merge into rank 0 (DSMEM atomics; <= 8 * 2048 * 255 < 2^32)
-  unsigned int* mg0 = cluster.map_shared_rank(&mg[0][0], 0);
+  PairStats& out = st->stats[k];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) {
     for (int c = 0; c < 3; ++c) {
       const unsigned w = pk[c][i];
       const unsigned count = w >> kSumBits, sum1 = w & kSumMask, sum2 = s2[c][i];
       const int a1 = c == 0 ? 1 : 0, a2 = c == 2 ? 1 : 2;
-      if (count) atomicAdd(mg0 + c * 256 + i, count);
-      if (hr[c][i]) atomicAdd(mg0 + (3 + c) * 256 + i, hr[c][i]);
-      if (sum1) atomicAdd(mg0 + (6 + sidx(a1, c)) * 256 + i, sum1);
-      if (sum2) atomicAdd(mg0 + (6 + sidx(a2, c)) * 256 + i, sum2);
+      if (count) atomicAdd(&out.hs[c][i], count);
+      if (hr[c][i]) atomicAdd(&out.hr[c][i], hr[c][i]);
+      if (sum1) atomicAdd(&out.s[sidx(a1, c)][i], static_cast<unsigned long long>(sum1));
+      if (sum2) atomicAdd(&out.s[sidx(a2, c)][i], static_cast<unsigned long long>(sum2));
     }
   }
-  if (threadIdx.x == 0 && cnt) atomicAdd(cluster.map_shared_rank(&ccnt, 0), cnt);
-  cluster.sync();  // every CTA's contribution is in rank 0
-  if (rank != 0) return;
-  PairStats& out = st->stats[k];
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-    for (int c = 0; c < 3; ++c) {
-      if (mg[c][i]) atomicAdd(&out.hs[c][i], mg[c][i]);
-      if (mg[3 + c][i]) atomicAdd(&out.hr[c][i], mg[3 + c][i]);
-    }
-    for (int c = 0; c < 6; ++c)
-      if (mg[6 + c][i]) atomicAdd(&out.s[c][i], static_cast<unsigned long long>(mg[6 + c][i]));
-  }
-  if (threadIdx.x == 0 && ccnt) atomicAdd(&out.n, static_cast<unsigned long long>(ccnt));
-  // the last cluster of this pair performs the solve
-  if (!elect_last_cta(&st->pair_done[k], gridDim.x / kColorCluster)) return;
+  if (threadIdx.x == 0 && cnt) atomicAdd(&out.n, static_cast<unsigned long long>(cnt));
+  // last CTA of this pair performs the solve
+  if (!elect_last_cta(&st->pair_done[k], gridDim.x)) return;
   if (threadIdx.x == 0) st->pair_done[k] = 0;
   pair_solve(p, k, st);
 }
@@ -323,9 +293,7 @@ void launch_pair_color(const Geometry* g, DevState* st, const int* list, int n, 
                        cudaStream_t s) {
   // no cap on the CTA count: the packed counters need <= 256 * kColorPpt
   // pixels per CTA (measured: 16 or 32 pixels per thread are not faster)
-  int bx = blocks_for(max_crop_px, 256 * kColorPpt, 1 << 30);
-  bx = (bx + kColorCluster - 1) / kColorCluster * kColorCluster;  // whole clusters
-  dim3 grid(bx, n);
+  dim3 grid(blocks_for(max_crop_px, 256 * kColorPpt, 1 << 30), n);
   k_pair_color<<<grid, 256, 0, s>>>(g, st, list);
 }
 
