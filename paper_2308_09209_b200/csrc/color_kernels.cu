@@ -31,26 +31,23 @@ __device__ void pair_solve(const PairDesc& p, int k, DevState* __restrict__ st) 
   __shared__ unsigned char lut[3][256];
   __shared__ unsigned long long cref[3][256];
   __shared__ unsigned long long mom[18];
-  PairStats* in = st->stats[k];
+  PairStats& in = st->stats[k];
   const int v = threadIdx.x;  // level owned by this thread
-  unsigned long long n = 0;
-  unsigned int hs[3] = {0, 0, 0}, hr[3] = {0, 0, 0};
-  unsigned long long ss[6] = {0, 0, 0, 0, 0, 0};
-  for (int cp = 0; cp < kStatCopies; ++cp) {
-    n += in[cp].n;
-    for (int c = 0; c < 3; ++c) {
-      hs[c] += in[cp].hs[c][v];
-      hr[c] += in[cp].hr[c][v];
-      in[cp].hs[c][v] = 0;  // reset the accumulators for the next frame
-      in[cp].hr[c][v] = 0;
-    }
-    for (int c = 0; c < 6; ++c) {
-      ss[c] += in[cp].s[c][v];
-      in[cp].s[c][v] = 0;
-    }
+  const unsigned long long n = in.n;
+  unsigned int hs[3], hr[3];
+  unsigned long long ss[6];
+  for (int c = 0; c < 3; ++c) {
+    hs[c] = in.hs[c][v];
+    hr[c] = in.hr[c][v];
+    in.hs[c][v] = 0;  // reset the accumulators for the next frame
+    in.hr[c][v] = 0;
+  }
+  for (int c = 0; c < 6; ++c) {
+    ss[c] = in.s[c][v];
+    in.s[c][v] = 0;
   }
   __syncthreads();
-  if (threadIdx.x < kStatCopies) in[threadIdx.x].n = 0;
+  if (threadIdx.x == 0) in.n = 0;
   if (n == 0) {
     // EmptyRegion from transfer_step: identity M, window untouched
     if (threadIdx.x == 0) {
@@ -266,7 +263,7 @@ __global__ void __launch_bounds__(256) k_pair_color(const Geometry* __restrict__
   }
   atomicAdd(&cnt, local);
   __syncthreads();
-  PairStats& out = st->stats[k][blockIdx.x % kStatCopies];
+  PairStats& out = st->stats[k];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) {
     for (int c = 0; c < 3; ++c) {
       const unsigned w = pk[c][i];

@@ -50,8 +50,6 @@ struct PairDesc {
 };
 
 // Per-pair integer moments of one frame (k_pair_stats -> k_pair_solve).
-constexpr int kStatCopies = 8;
-
 struct PairStats {
   unsigned int hs[3][256];   // source (view) histogram
   unsigned int hr[3][256];   // reference (partner) histogram
@@ -198,10 +196,7 @@ struct TemporalState {
 // Per-slot frame state: scratch accumulators, this frame's colour matrices,
 // LUT and report, plus pointers into the shared TemporalState.
 struct DevState {
-  // kStatCopies interleaved copies per pair (CTA b flushes into copy
-  // b % kStatCopies): fewer CTAs contend for each global counter; the
-  // pair's solve sums the copies (integers: any order)
-  PairStats stats[kMaxPairs][kStatCopies];
+  PairStats stats[kMaxPairs];
   PairWindow* windows;          // -> TemporalState::windows
   double mview[kMaxViews][9];  // colour matrix applied to each view
   unsigned int pano_hist[3][256];
