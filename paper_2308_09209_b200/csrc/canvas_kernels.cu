@@ -76,6 +76,88 @@ __global__ void __launch_bounds__(256) k_crop_warp(const __grid_constant__ Canva
                         : warp_cv<false>(P.views[view], canvas_lift<false>(P, p.x0 + dx, p.y0 + dy));
 }
 
+// Staged variant (planar canvas; STITCH_B200_WARP_STAGE=1): a CTA owns a
+// 32 x 8 tile of one crop side; thread 0 maps the tile's corner pixels
+// through the view's inverse homography, the CTA loads the bounding window
+// of their source footprint (+1 texel margin for the bilinear taps, capped at
+// kStageW x kStageH) from the RGBA frame into shared memory with coalesced
+// row loads, and every pixel samples its four taps there (sample_rgba_win,
+// bit-identical arithmetic).  Tiles whose window does not fit (or whose
+// corners leave the front of the camera) and non-interior samples use the
+// global-memory sampler.  block (32, 8)
+constexpr int kStageW = 64, kStageH = 24;
+
+__global__ void __launch_bounds__(256) k_crop_warp_staged(const __grid_constant__ CanvasParams P) {
+  __shared__ uchar4 win[kStageH * kStageW];
+  __shared__ int s_wx0, s_wy0, s_ww, s_wh;
+  const int k = blockIdx.z >> 1;
+  const int side = blockIdx.z & 1;
+  const CanvasPair& p = P.pairs[k];
+  const int bx0 = blockIdx.x * 32, by0 = blockIdx.y * 8;
+  if (bx0 >= p.w || by0 >= p.h) return;  // uniform over the CTA
+  const int view = side ? p.partner : p.view;
+  const CanvasView& v = P.views[view];
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  if (tid == 0) {
+    double mnx = 1e300, mny = 1e300, mxx = -1e300, mxy = -1e300;
+    bool ok = true;
+    const int xs[2] = {bx0, min(bx0 + 31, p.w - 1)}, ys[2] = {by0, min(by0 + 7, p.h - 1)};
+    for (int j = 0; j < 2; ++j)
+      for (int i = 0; i < 2; ++i) {
+        double sx, sy, sz;
+        warp_point<false>(v.inv, canvas_lift<false>(P, p.x0 + xs[i], p.y0 + ys[j]), sx, sy, sz);
+        if (!(sz > 1e-9)) {
+          ok = false;
+        } else {
+          const double qx = sx / sz, qy = sy / sz;
+          mnx = fmin(mnx, qx);
+          mny = fmin(mny, qy);
+          mxx = fmax(mxx, qx);
+          mxy = fmax(mxy, qy);
+        }
+      }
+    int wx0 = 0, wy0 = 0, ww = 0, wh = 0;
+    if (ok && mnx > -1e6 && mny > -1e6 && mxx < 1e6 && mxy < 1e6) {
+      // one texel of slack beyond the corner images for the rounding of the
+      // per-pixel coordinates; the window need not lie inside the frame
+      wx0 = static_cast<int>(floor(mnx)) - 1;
+      wy0 = static_cast<int>(floor(mny)) - 1;
+      ww = static_cast<int>(floor(mxx)) + 3 - wx0;
+      wh = static_cast<int>(floor(mxy)) + 3 - wy0;
+      if (ww > kStageW || wh > kStageH) ww = wh = 0;
+    }
+    s_wx0 = wx0;
+    s_wy0 = wy0;
+    s_ww = ww;
+    s_wh = wh;
+  }
+  __syncthreads();
+  const int wx0 = s_wx0, wy0 = s_wy0, ww = s_ww, wh = s_wh;
+  for (int i = tid; i < ww * wh; i += 256) {
+    const int ly = i / ww, lx = i - ly * ww;
+    const int gx = wx0 + lx, gy = wy0 + ly;
+    uchar4 t = make_uchar4(0, 0, 0, 0);
+    if (gx >= 0 && gx < v.w && gy >= 0 && gy < v.h) t = v.rgba[static_cast<size_t>(gy) * v.w + gx];
+    win[ly * kStageW + lx] = t;
+  }
+  __syncthreads();
+  const int dx = bx0 + threadIdx.x, dy = by0 + threadIdx.y;
+  if (dx >= p.w || dy >= p.h) return;
+  const Lift L = canvas_lift<false>(P, p.x0 + dx, p.y0 + dy);
+  double sx, sy, sz;
+  warp_point<false>(v.inv, L, sx, sy, sz);
+  uchar4 o = make_uchar4(0, 0, 0, 0);
+  if (!(fabs(sz) < 1e-12)) {
+    const DDivisor dz = ddivisor(sz);
+    const double qx = ddiv(sx, dz), qy = ddiv(sy, dz);
+    float r, g, b;
+    int valid = ww ? sample_rgba_win(win, kStageW, wx0, wy0, ww, wh, v.w, v.h, qx, qy, r, g, b) : -1;
+    if (valid < 0) valid = sample_rgba(v.rgba, v.w, v.h, qx, qy, r, g, b) ? 1 : 0;
+    if (valid) o = make_uchar4(quantize_f(r), quantize_f(g), quantize_f(b), 1);
+  }
+  p.crop_raw[side][dy * p.w + dx] = o;
+}
+
 // ---------------------------------------------------------------------------
 // Canvas pass: for every canvas pixel, the warped reference view, then the
 // compose_panorama fold over pairs (pipeline.cpp:326-333, flow.cpp:324-357)
@@ -553,6 +635,12 @@ void launch_expand_one(const std::uint8_t* rgb, uchar4* rgba, long long n_px, cu
 }
 
 void launch_crop_warp(const CanvasParams& P, int max_w, int max_h, cudaStream_t s) {
+  static const int stage = env_int("STITCH_B200_WARP_STAGE", 0);
+  if (stage && P.projection == 0) {
+    dim3 grid((max_w + 31) / 32, (max_h + 7) / 8, 2 * P.np);
+    k_crop_warp_staged<<<grid, dim3(32, 8), 0, s>>>(P);
+    return;
+  }
   dim3 grid((max_w + 63) / 64, (max_h + 3) / 4, 2 * P.np);
   k_crop_warp<<<grid, dim3(64, 4), 0, s>>>(P);
 }
