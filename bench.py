@@ -460,15 +460,21 @@ def run_b200(args, rank, world, local_rank):
         kernels[name] = k
     dominant = max(per_kind, key=lambda n: per_kind[n][0])
     dk = kernels[dominant]
-    traffic = None
+    # ncu DRAM bytes per launch of the dominant kernel (read + write, one
+    # frame's launches averaged: profiles/traffic.json from the committed
+    # launch list), comparable with alg_bytes_per_launch
+    traffic, traffic_src = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get(dominant)
+            t = json.load(f).get(dominant)
+        if t:
+            traffic, traffic_src = int(t["dram_bytes_per_launch"]), t["source"]
     except Exception:
         pass
     launches_dom = max(1, dk["launches_per_frame"])
     roofline = {"kernel": dominant, "bound": "hbm", "achieved": dk.get("hbm_gbs"), "peak": peak,
                 "unit": "GB/s", "frac": dk.get("hbm_frac"), "traffic": traffic,
+                "traffic_source": traffic_src,
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                 "alg_bytes_per_launch": (model[dominant]["bytes"] / launches_dom
                                          if dominant in model else None),

@@ -761,6 +761,10 @@ class SynthScene:
         cfg = _config_from_c(self.config_c())
         cfg.seed = self.spec.seed
         cfg.scene_id = f"synth-{self.spec.seed}"
+        # feature refinement (on by default, like the reference) serves the
+        # planar canvas; the 360-degree ring extension keeps its exact maps
+        if cfg.projection == "cylindrical":
+            cfg.refine.enabled = False
         return cfg
 
     def render_view(self, view: int, frame: int, threads: int = 0) -> Frame:

@@ -18,7 +18,7 @@ for r in csv.DictReader(lines):
     key = int(r["ID"])
     if key not in rows:
         order.append(key)
-    rows[key]["name"] = r["Kernel Name"].split("(")[0].replace("void ", "").split("<")[0]
+    rows[key]["name"] = r["Kernel Name"].split("(")[0].replace("void ", "").split("<")[0].split("::")[-1].split("<")[0]
     v = float(r["Metric Value"].replace(",", ""))
     unit = r["Metric Unit"]
     scale = {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "msecond": 1e-3, "byte": 1, "Kbyte": 1e3,

@@ -10,7 +10,7 @@ with open(sys.argv[1]) as f:
     lines = [ln for ln in f if ln.startswith('"')]
 for r in csv.DictReader(lines):
     if r["Metric Name"] == "gpu__time_duration.sum":
-        rows.append((r["Kernel Name"].split("(")[0].replace("void ", ""), r["Grid Size"],
+        rows.append((r["Kernel Name"].split("(")[0].replace("void ", "").split("<")[0].split("::")[-1], r["Grid Size"],
                      float(r["Metric Value"]) / 1e3))
 idx = [i for i, r in enumerate(rows) if r[0].startswith("k_expand")]
 frame = rows[idx[-2]:idx[-1]]
