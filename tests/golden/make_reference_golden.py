@@ -70,6 +70,27 @@ CASES = [
     ("star3_perturbed_flow", dict(views=3, width=320, height=240, frames=3, focal_scale=1.03,
                                   principal_px=4.0, obj=OBJ),
      dict(refine_enabled=0, levels=3, iterations=20, smoothness=10.0), 3),
+    # sweeps = iterations / 5 by integer division (flow.cpp:79-80): 23 -> 4 sweeps per
+    # warp iteration; two pyramid levels, a smaller smoothness
+    ("flow_iter23_levels2", dict(views=2, width=320, height=240, frames=3, obj=OBJ,
+                                 casts=[(1, 1, 1), (0.9, 1.05, 1.0)]),
+     dict(refine_enabled=0, levels=2, iterations=23, smoothness=7.5), 3),
+    # narrow and wide overlaps (geometry, bounds, chamfer weights), seed 7
+    ("narrow_overlap", dict(seed=7, views=2, width=320, height=240, frames=3, overlap=0.12,
+                            obj=OBJ, casts=[(1, 1, 1), (1.1, 0.95, 0.9)]),
+     dict(refine_enabled=1), 3),
+    ("wide_overlap", dict(seed=7, views=3, width=320, height=240, frames=3, overlap=0.6,
+                          obj=OBJ, casts=[(0.95, 1, 1), (1, 1, 1), (1, 1.05, 0.92)]),
+     dict(refine_enabled=1, window_capacity=1, fuse_weighting=1), 3),
+    # small frames: the pyramid stop rule checks the previous level (flow.cpp:153)
+    ("small_frames", dict(seed=3, views=2, width=96, height=72, frames=4, obj=dict(
+        enabled=True, half_size=12.0, velocity=(2.0, 1.0)), casts=[(1, 1, 1), (0.8, 1, 1.2)]),
+     dict(refine_enabled=0), 4),
+    # perturbed principal point refined away, 5 frames
+    ("principal_refine", dict(seed=5, views=3, width=320, height=240, frames=5,
+                              focal_scale=1.02, principal_px=6.0, obj=OBJ,
+                              casts=[(1, 1, 1), (0.9, 1, 1.05), (1.05, 0.97, 1)]),
+     dict(refine_enabled=1, lam=0.08), 5),
 ]
 
 
