@@ -55,6 +55,17 @@ __global__ void __launch_bounds__(256) k_expand_one(const std::uint8_t* __restri
 // ---------------------------------------------------------------------------
 template <bool CYL>
 __device__ __forceinline__ uchar4 warp_cv(const CanvasView& v, Lift L) {
+  if (v.f32) {  // experiment: FP32 interior weights (not bit-exact)
+    double sx, sy, sz;
+    warp_point<CYL>(v.inv, L, sx, sy, sz);
+    uchar4 o = make_uchar4(0, 0, 0, 0);
+    if (fabs(sz) < 1e-12) return o;
+    if (CYL && !(sz > 0.0)) return o;
+    float r, g, b;
+    const DDivisor dz = ddivisor(sz);
+    if (!sample_rgba_f32(v.rgba, v.w, v.h, ddiv(sx, dz), ddiv(sy, dz), r, g, b)) return o;
+    return make_uchar4(quantize_f(r), quantize_f(g), quantize_f(b), 1);
+  }
   ViewDesc d;
   d.width = v.w;
   d.height = v.h;

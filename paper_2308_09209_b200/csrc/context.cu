@@ -825,6 +825,8 @@ int build_context(const stitch_b200_init* in, int device,
         for (int i = 0; i < 4; ++i) P.views[v].bbox[i] = g.views[v].bbox[i];
         P.views[v].gap[0] = g.views[v].gap[0];
         P.views[v].gap[1] = g.views[v].gap[1];
+        static const int warp_f32 = env_int("STITCH_B200_WARP_F32", 0);
+        P.views[v].f32 = warp_f32;
       }
       for (int k = 0; k < g.n_pairs; ++k) {
         const PairDesc& p = g.pairs[k];

@@ -132,6 +132,7 @@ struct CanvasView {
   int w, h;
   int bbox[4];
   int gap[2];
+  int f32;  // experiment (STITCH_B200_WARP_F32): FP32 interior weights and sums
 };
 
 struct CanvasPair {

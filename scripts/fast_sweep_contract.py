@@ -9,6 +9,10 @@ as one RESULT JSON line; profiles/r02_fast_sweep_contract.json records the
 outcome (the variant breaks the contract, so the bit-exact sweep stays).
 
     python -m pytest scripts/fast_sweep_contract.py -q -s
+    CONTRACT_ENV=STITCH_B200_WARP_F32=1 python -m pytest scripts/fast_sweep_contract.py -q -s
+
+CONTRACT_ENV (comma-separated NAME=VALUE, default STITCH_B200_HS_FAST=1) picks the
+contract-tolerant variant under test.
 """
 import json
 import os
@@ -38,7 +42,8 @@ print("RESULT " + json.dumps(worst))
 @pytest.mark.gpu
 @pytest.mark.parametrize("key", ["c1", "c2", "c3", "c4"])
 def test_fast_sweep_within_contract(key):
-    env = dict(os.environ, STITCH_B200_HS_FAST="1")
+    spec = os.environ.get("CONTRACT_ENV", "STITCH_B200_HS_FAST=1")
+    env = dict(os.environ, **dict(kv.split("=", 1) for kv in spec.split(",") if kv))
     r = subprocess.run([sys.executable, "-c", CODE, key], cwd=ROOT, env=env, capture_output=True,
                        text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
