@@ -495,7 +495,8 @@ def run_b200(args, rank, world, local_rank):
         "p50_ms_per_frame": round(p50, 4), "higher_is_better": True,
         "scaling": "strong" if fixed_total else "weak",
         "vs_baseline": None, "dtype": "u8 (fp64 warp, fp32 flow)",
-        "data": "synthetic (procedural plane scene, SynthScene restatement; seed 1+rank)",
+        "data": ("synthetic (procedural plane scene: the repo's SynthScene, byte-identical to "
+                 "the reference's renderer on <= 3 views; seed 1+rank)"),
         "config": {"workload": wl["desc"], "config_key": args.config, "cameras": nv,
                    "camera_size": [wl["width"], wl["height"]],
                    "canvas": [state.canvas_width, state.canvas_height],
