@@ -421,6 +421,16 @@ def run_b200(args, rank, world, local_rank):
                                                   None))
     e2e_sync_s = sharding.max_over_ranks(time.perf_counter() - t0)
     e2e_sync = world * min(e2e_steps, 50) / e2e_sync_s
+    # ... and with pageable buffers: the drop-in binding's call (INTEGRATION.md:
+    # process_frame_b200 hands the reference's std::vector frames to
+    # stitch_b200_process)
+    t0 = time.perf_counter()
+    for i in range(min(e2e_steps, 50)):
+        pb.pipeline.check(lib.stitch_b200_process(hs_[0], pg_in_ptrs[i % F],
+                                                  pg_out[0][0].ctypes.data,
+                                                  pg_out[0][1].ctypes.data, None))
+    e2e_sync_pg_s = sharding.max_over_ranks(time.perf_counter() - t0)
+    e2e_sync_pg = world * min(e2e_steps, 50) / e2e_sync_pg_s
 
     # ---- per-kernel profile (eager plan, CUDA events around each launch) ----
     n_ops = 4096
@@ -513,6 +523,7 @@ def run_b200(args, rank, world, local_rank):
                 "steps": e2e_steps, "streams": 1,
                 "api": f"stitch_b200_submit/stitch_b200_wait ({depth} frames in flight, pinned host)",
                 "sync_process_value": round(e2e_sync, 2),
+                "sync_pageable_value": round(e2e_sync_pg, 2),
                 "pageable_value": round(e2e_pageable, 2),
                 "pageable_api": "same calls with pageable (numpy) frames and outputs, staged "
                                 "through the context's pinned ring"},

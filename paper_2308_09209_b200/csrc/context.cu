@@ -243,6 +243,16 @@ struct Ctx {
   std::uint8_t* h_stage_mask[kMaxSlots] = {};
   std::uint8_t* user_rgb[kMaxSlots] = {};
   std::uint8_t* user_mask[kMaxSlots] = {};
+  // staged outputs leave the device in chunks, each followed by an event, so
+  // the copy of chunk c into the caller's buffer overlaps the DMA of c + 1
+  static constexpr int kOutChunks = 16;
+  struct OutChunk {
+    std::uint8_t* dst;
+    const std::uint8_t* src;
+    size_t n;
+  };
+  std::vector<OutChunk> out_chunks[kMaxSlots];
+  cudaEvent_t out_ev[kMaxSlots][kOutChunks] = {};
   std::unique_ptr<CopyPool> copier;
   std::vector<int> pair_levels;
   float2* d_zero = nullptr;
@@ -284,6 +294,8 @@ struct Ctx {
       for (auto* q : h_stage_in[s])
         if (q) cudaFreeHost(q);
       if (h_stage_rgb[s]) cudaFreeHost(h_stage_rgb[s]);
+      for (cudaEvent_t e : out_ev[s])
+        if (e) cudaEventDestroy(e);
       if (h_stage_mask[s]) cudaFreeHost(h_stage_mask[s]);
     }
     if (stream) cudaStreamDestroy(stream);
@@ -990,16 +1002,15 @@ void fill_report(Ctx* ctx, int slot, stitch_b200_report* r) {
 // its report for a later stitch_b200_wait().
 int retire_slot(Ctx* ctx, int slot) {
   if (!ctx->slot_pending[slot]) return STITCH_B200_OK;
-  CUDA_TRY(cudaEventSynchronize(ctx->d2h_done[slot]));
-  if (ctx->user_rgb[slot] || ctx->user_mask[slot]) {  // pageable outputs: ring -> caller
-    std::vector<CopyPool::Job> jobs;
-    if (ctx->user_rgb[slot])
-      jobs.push_back({ctx->user_rgb[slot], ctx->h_stage_rgb[slot], static_cast<size_t>(ctx->n_px) * 3});
-    if (ctx->user_mask[slot])
-      jobs.push_back({ctx->user_mask[slot], ctx->h_stage_mask[slot], static_cast<size_t>(ctx->n_px)});
-    ctx->copier->run(jobs);
-    ctx->user_rgb[slot] = ctx->user_mask[slot] = nullptr;
+  // pageable outputs: ring -> caller, chunk by chunk as the download lands
+  std::vector<Ctx::OutChunk>& oc = ctx->out_chunks[slot];
+  for (size_t c = 0; c < oc.size(); ++c) {
+    CUDA_TRY(cudaEventSynchronize(ctx->out_ev[slot][c]));
+    ctx->copier->run({{oc[c].dst, oc[c].src, oc[c].n}});
   }
+  oc.clear();
+  CUDA_TRY(cudaEventSynchronize(ctx->d2h_done[slot]));
+  ctx->user_rgb[slot] = ctx->user_mask[slot] = nullptr;
   stitch_b200_report r;
   fill_report(ctx, slot, &r);
   ctx->done_reports.emplace_back(ctx->slot_ticket[slot], r);
@@ -1082,6 +1093,8 @@ int ensure_staging(Ctx* ctx, int slot) {
   if (!ctx->h_stage_mask[slot])
     CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_stage_mask[slot]),
                            static_cast<size_t>(ctx->n_px), cudaHostAllocDefault));
+  for (cudaEvent_t& e : ctx->out_ev[slot])
+    if (!e) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   return STITCH_B200_OK;
 }
 
@@ -1108,15 +1121,12 @@ int submit_host(Ctx* ctx, const std::uint8_t* const* frames, std::uint8_t* pano_
   // the slot's inputs were last read by its previous frame (retired above,
   // so its staging buffers are free as well)
   CUDA_TRY(cudaStreamWaitEvent(ctx->h2d, ctx->comp_done[slot], 0));
-  if (any_stage) {
-    std::vector<CopyPool::Job> jobs;
-    for (int v = 0; v < ctx->hg.n_views; ++v)
-      if (stage_in[v]) jobs.push_back({ctx->h_stage_in[slot][v], frames[v], ctx->frame_bytes[v]});
-    ctx->copier->run(jobs);
-  }
-  for (int v = 0; v < ctx->hg.n_views; ++v)
+  // view by view: the DMA of a staged view runs while the next one is copied
+  for (int v = 0; v < ctx->hg.n_views; ++v) {
+    if (stage_in[v]) ctx->copier->run({{ctx->h_stage_in[slot][v], frames[v], ctx->frame_bytes[v]}});
     CUDA_TRY(cudaMemcpyAsync(ctx->d_in[slot][v], stage_in[v] ? ctx->h_stage_in[slot][v] : frames[v],
                              ctx->frame_bytes[v], cudaMemcpyHostToDevice, ctx->h2d));
+  }
   CUDA_TRY(cudaEventRecord(ctx->h2d_done[slot], ctx->h2d));
   CUDA_TRY(cudaStreamWaitEvent(ctx->slot[slot].cs, ctx->h2d_done[slot], 0));
   const std::uint8_t* in[kMaxViews];
@@ -1124,12 +1134,35 @@ int submit_host(Ctx* ctx, const std::uint8_t* const* frames, std::uint8_t* pano_
   rc = enqueue_frame(ctx, slot, in);
   if (rc) return rc;
   CUDA_TRY(cudaStreamWaitEvent(ctx->d2h, ctx->comp_done[slot], 0));
-  if (pano_rgb)
-    CUDA_TRY(cudaMemcpyAsync(stage_rgb ? ctx->h_stage_rgb[slot] : pano_rgb, ctx->d_out_rgb[slot],
-                             static_cast<size_t>(ctx->n_px) * 3, cudaMemcpyDeviceToHost, ctx->d2h));
-  if (pano_mask)
-    CUDA_TRY(cudaMemcpyAsync(stage_mask ? ctx->h_stage_mask[slot] : pano_mask, ctx->d_out_mask[slot],
-                             static_cast<size_t>(ctx->n_px), cudaMemcpyDeviceToHost, ctx->d2h));
+  const size_t rgb_bytes = static_cast<size_t>(ctx->n_px) * 3, mask_bytes = static_cast<size_t>(ctx->n_px);
+  if (pano_rgb && !stage_rgb)
+    CUDA_TRY(cudaMemcpyAsync(pano_rgb, ctx->d_out_rgb[slot], rgb_bytes, cudaMemcpyDeviceToHost,
+                             ctx->d2h));
+  if (pano_mask && !stage_mask)
+    CUDA_TRY(cudaMemcpyAsync(pano_mask, ctx->d_out_mask[slot], mask_bytes, cudaMemcpyDeviceToHost,
+                             ctx->d2h));
+  if (stage_rgb || stage_mask) {
+    // chunks of >= 4 MiB, at most kOutChunks in all
+    const size_t total = (stage_rgb ? rgb_bytes : 0) + (stage_mask ? mask_bytes : 0);
+    const size_t chunk = std::max<size_t>(size_t(4) << 20, (total + Ctx::kOutChunks - 3) / (Ctx::kOutChunks - 2));
+    std::vector<Ctx::OutChunk>& oc = ctx->out_chunks[slot];
+    oc.clear();
+    auto split = [&](std::uint8_t* dst, std::uint8_t* stage, size_t n) {
+      for (size_t o = 0; o < n; o += chunk) oc.push_back({dst + o, stage + o, std::min(chunk, n - o)});
+    };
+    if (stage_rgb) split(pano_rgb, ctx->h_stage_rgb[slot], rgb_bytes);
+    const size_t n_rgb_chunks = oc.size();
+    if (stage_mask) split(pano_mask, ctx->h_stage_mask[slot], mask_bytes);
+    for (size_t c = 0; c < oc.size(); ++c) {
+      const bool is_rgb = c < n_rgb_chunks;
+      const std::uint8_t* stage0 = is_rgb ? ctx->h_stage_rgb[slot] : ctx->h_stage_mask[slot];
+      const std::uint8_t* dev0 = is_rgb ? ctx->d_out_rgb[slot] : ctx->d_out_mask[slot];
+      const size_t off = static_cast<size_t>(oc[c].src - stage0);
+      CUDA_TRY(cudaMemcpyAsync(const_cast<std::uint8_t*>(oc[c].src), dev0 + off, oc[c].n,
+                               cudaMemcpyDeviceToHost, ctx->d2h));
+      CUDA_TRY(cudaEventRecord(ctx->out_ev[slot][c], ctx->d2h));
+    }
+  }
   CUDA_TRY(cudaEventRecord(ctx->d2h_done[slot], ctx->d2h));
   ctx->user_rgb[slot] = stage_rgb ? pano_rgb : nullptr;
   ctx->user_mask[slot] = stage_mask ? pano_mask : nullptr;
