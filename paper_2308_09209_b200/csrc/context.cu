@@ -1002,13 +1002,23 @@ void fill_report(Ctx* ctx, int slot, stitch_b200_report* r) {
 // its report for a later stitch_b200_wait().
 int retire_slot(Ctx* ctx, int slot) {
   if (!ctx->slot_pending[slot]) return STITCH_B200_OK;
-  // pageable outputs: ring -> caller, chunk by chunk as the download lands
+  // pageable outputs: ring -> caller.  A download still in flight (a caller
+  // waiting right after its submit) is copied chunk by chunk as it lands; a
+  // finished one (frames kept in flight) in one batch.
   std::vector<Ctx::OutChunk>& oc = ctx->out_chunks[slot];
-  for (size_t c = 0; c < oc.size(); ++c) {
-    CUDA_TRY(cudaEventSynchronize(ctx->out_ev[slot][c]));
-    ctx->copier->run({{oc[c].dst, oc[c].src, oc[c].n}});
+  if (!oc.empty()) {
+    if (cudaEventQuery(ctx->d2h_done[slot]) == cudaSuccess) {
+      std::vector<CopyPool::Job> jobs;
+      for (const auto& c : oc) jobs.push_back({c.dst, c.src, c.n});
+      ctx->copier->run(jobs);
+    } else {
+      for (size_t c = 0; c < oc.size(); ++c) {
+        CUDA_TRY(cudaEventSynchronize(ctx->out_ev[slot][c]));
+        ctx->copier->run({{oc[c].dst, oc[c].src, oc[c].n}});
+      }
+    }
+    oc.clear();
   }
-  oc.clear();
   CUDA_TRY(cudaEventSynchronize(ctx->d2h_done[slot]));
   ctx->user_rgb[slot] = ctx->user_mask[slot] = nullptr;
   stitch_b200_report r;
@@ -1121,9 +1131,20 @@ int submit_host(Ctx* ctx, const std::uint8_t* const* frames, std::uint8_t* pano_
   // the slot's inputs were last read by its previous frame (retired above,
   // so its staging buffers are free as well)
   CUDA_TRY(cudaStreamWaitEvent(ctx->h2d, ctx->comp_done[slot], 0));
-  // view by view: the DMA of a staged view runs while the next one is copied
+  // An idle pipeline (the synchronous pattern: submit, then wait) stages view
+  // by view so each view's DMA runs while the next one is copied; with frames
+  // in flight the copy engine is busy anyway and one batch costs the least.
+  bool idle = true;
+  for (int sl = 0; sl < ctx->n_slots; ++sl) idle = idle && !ctx->slot_pending[sl];
+  if (any_stage && !idle) {
+    std::vector<CopyPool::Job> jobs;
+    for (int v = 0; v < ctx->hg.n_views; ++v)
+      if (stage_in[v]) jobs.push_back({ctx->h_stage_in[slot][v], frames[v], ctx->frame_bytes[v]});
+    ctx->copier->run(jobs);
+  }
   for (int v = 0; v < ctx->hg.n_views; ++v) {
-    if (stage_in[v]) ctx->copier->run({{ctx->h_stage_in[slot][v], frames[v], ctx->frame_bytes[v]}});
+    if (stage_in[v] && idle)
+      ctx->copier->run({{ctx->h_stage_in[slot][v], frames[v], ctx->frame_bytes[v]}});
     CUDA_TRY(cudaMemcpyAsync(ctx->d_in[slot][v], stage_in[v] ? ctx->h_stage_in[slot][v] : frames[v],
                              ctx->frame_bytes[v], cudaMemcpyHostToDevice, ctx->h2d));
   }
