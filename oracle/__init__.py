@@ -471,11 +471,12 @@ def make_config(n_views, reference, sizes, cams, *, lam=0.05, gamma_dark=1.5, ga
 class OracleState:
     """so_state: the oracle's PipelineState (initialize + process_frame)."""
 
-    def __init__(self, cfg: SoConfig, first_frames=None):
+    def __init__(self, cfg: SoConfig, first_frames=None, first_masks=None):
         self.cfg = cfg
         err = C.c_int(SO_OK)
         if first_frames is not None:
-            refs = [FrameRef(f) for f in first_frames]
+            fm = first_masks or [None] * len(first_frames)
+            refs = [FrameRef(f, m) for f, m in zip(first_frames, fm)]
             arr = (SoFrame * len(refs))(*[r.c for r in refs])
             self._h = lib().so_initialize_frames(C.byref(cfg), arr, C.byref(err))
         else:
@@ -514,8 +515,10 @@ class OracleState:
         lib().so_state_map(self._h, v, h, inv)
         return np.array(h[:]).reshape(3, 3), np.array(inv[:]).reshape(3, 3)
 
-    def process(self, frames):
-        refs = [FrameRef(f) for f in frames]
+    def process(self, frames, masks=None):
+        """frames: RGB8 arrays; masks: per frame None or an (H, W) 0/1 array
+        (Frame::mask, frame.hpp:44-47)."""
+        refs = [FrameRef(f, m) for f, m in zip(frames, masks or [None] * len(frames))]
         arr = (SoFrame * len(refs))(*[r.c for r in refs])
         out = SoFrame()
         rep = SoReport()

@@ -201,12 +201,15 @@ static stitch::StitchConfig make_config(const Scene* sc, const ref_opts* o) {
   return c;
 }
 
+// masks: NULL, or per view NULL (no mask) or width*height 0/1 bytes
 static std::vector<stitch::Frame> wrap(const std::vector<std::pair<int, int>>& sizes,
-                                       const uint8_t* const* rgb) {
+                                       const uint8_t* const* rgb,
+                                       const uint8_t* const* masks = nullptr) {
   std::vector<stitch::Frame> out;
   for (std::size_t v = 0; v < sizes.size(); ++v) {
     stitch::Frame f(sizes[v].first, sizes[v].second);
     std::memcpy(f.data.data(), rgb[v], f.data.size());
+    if (masks && masks[v]) f.mask.assign(masks[v], masks[v] + f.pixel_count());
     out.push_back(std::move(f));
   }
   return out;
@@ -219,11 +222,12 @@ static std::vector<std::pair<int, int>> scene_sizes(const Scene* sc) {
 }
 
 // stitch::initialize (pipeline.cpp:209-257) on caller-supplied first frames.
-void* ref_state_new(void* scene, const ref_opts* o, const uint8_t* const* first, int* err) {
+void* ref_state_new(void* scene, const ref_opts* o, const uint8_t* const* first,
+                    const uint8_t* const* first_masks, int* err) {
   try {
     const auto* sc = static_cast<Scene*>(scene);
     auto* st = new State;
-    st->st = stitch::initialize(make_config(sc, o), wrap(scene_sizes(sc), first));
+    st->st = stitch::initialize(make_config(sc, o), wrap(scene_sizes(sc), first, first_masks));
     *err = -1;
     return st;
   } catch (const std::exception& e) {
@@ -279,13 +283,13 @@ void ref_state_pair_weights(void* p, int k, float* theta_i, float* theta_j) {
 // pano_rgb: canvas W*H*3; pano_mask: canvas W*H (all ones when the reference
 // returns no mask).
 int ref_process_sized(void* p, int n, const int* widths, const int* heights,
-                      const uint8_t* const* frames, uint8_t* pano_rgb, uint8_t* pano_mask,
-                      ref_report* rep) {
+                      const uint8_t* const* frames, const uint8_t* const* masks,
+                      uint8_t* pano_rgb, uint8_t* pano_mask, ref_report* rep) {
   try {
     auto* st = static_cast<State*>(p);
     std::vector<std::pair<int, int>> sizes;
     for (int v = 0; v < n; ++v) sizes.emplace_back(widths[v], heights[v]);
-    stitch::ProcessResult r = stitch::process_frame(st->st, wrap(sizes, frames));
+    stitch::ProcessResult r = stitch::process_frame(st->st, wrap(sizes, frames, masks));
     const stitch::Frame& pano = r.panorama;
     std::memcpy(pano_rgb, pano.data.data(), pano.data.size());
     if (pano.has_mask())

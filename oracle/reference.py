@@ -87,7 +87,8 @@ def lib() -> C.CDLL:
         "ref_scene_reference": (C.c_int, [C.c_void_p]),
         "ref_scene_render": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
         "ref_scene_cameras": (C.c_int, [C.c_void_p, P(C.c_double)]),
-        "ref_state_new": (C.c_void_p, [C.c_void_p, P(RefOpts), P(C.c_void_p), P(C.c_int)]),
+        "ref_state_new": (C.c_void_p, [C.c_void_p, P(RefOpts), P(C.c_void_p), P(C.c_void_p),
+                                        P(C.c_int)]),
         "ref_state_free": (None, [C.c_void_p]),
         "ref_state_canvas": (None, [C.c_void_p, P(C.c_int), P(C.c_int), P(C.c_double),
                                     P(C.c_double)]),
@@ -96,7 +97,8 @@ def lib() -> C.CDLL:
         "ref_state_pair": (None, [C.c_void_p, C.c_int, P(C.c_int), P(C.c_int), P(C.c_int)]),
         "ref_state_pair_weights": (None, [C.c_void_p, C.c_int, P(C.c_float), P(C.c_float)]),
         "ref_process_sized": (C.c_int, [C.c_void_p, C.c_int, P(C.c_int), P(C.c_int),
-                                        P(C.c_void_p), C.c_void_p, C.c_void_p, P(RefReport)]),
+                                        P(C.c_void_p), P(C.c_void_p), C.c_void_p, C.c_void_p,
+                                        P(RefReport)]),
         "ref_dense_flow": (C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
                                      C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_int,
                                      P(C.c_float), P(C.c_float)]),
@@ -127,6 +129,14 @@ def default_opts(**kw) -> RefOpts:
     for k, v in kw.items():
         setattr(o, "lambda_" if k == "lam" else k, v)
     return o
+
+
+def _mask_ptrs(masks, n):
+    """NULL for no masks, else a per-view pointer table (NULL = unmasked view)."""
+    if masks is None or all(m is None for m in masks):
+        return None, []
+    keep = [None if m is None else np.ascontiguousarray(m, np.uint8) for m in masks]
+    return (C.c_void_p * n)(*[None if m is None else m.ctypes.data for m in keep]), keep
 
 
 class Scene:
@@ -194,11 +204,12 @@ class Scene:
 class State:
     """stitch::PipelineState from stitch::initialize (pipeline.cpp:209-257)."""
 
-    def __init__(self, scene: Scene, opts: RefOpts, first_frames):
+    def __init__(self, scene: Scene, opts: RefOpts, first_frames, first_masks=None):
         self._keep = [np.ascontiguousarray(f, np.uint8) for f in first_frames]
         ptrs = (C.c_void_p * len(self._keep))(*[f.ctypes.data for f in self._keep])
+        mptrs, self._keep_m = _mask_ptrs(first_masks, len(self._keep))
         err = C.c_int(OK)
-        self._h = lib().ref_state_new(scene._h, C.byref(opts), ptrs, C.byref(err))
+        self._h = lib().ref_state_new(scene._h, C.byref(opts), ptrs, mptrs, C.byref(err))
         if not self._h:
             raise RefError(err.value)
         w, h, ox, oy = C.c_int(), C.c_int(), C.c_double(), C.c_double()
@@ -227,18 +238,20 @@ class State:
         lib().ref_state_map(self._h, v, h, inv)
         return np.array(h[:]).reshape(3, 3), np.array(inv[:]).reshape(3, 3)
 
-    def process(self, frames):
+    def process(self, frames, masks=None):
+        """frames: RGB8 arrays; masks: None or per frame None / (H, W) 0/1."""
         fs = [np.ascontiguousarray(f, np.uint8) for f in frames]
         n = len(fs)
         ws = (C.c_int * n)(*[f.shape[1] for f in fs])
         hs = (C.c_int * n)(*[f.shape[0] for f in fs])
         ptrs = (C.c_void_p * n)(*[f.ctypes.data for f in fs])
+        mptrs, keep_m = _mask_ptrs(masks, n)
         w, h = self.canvas[0], self.canvas[1]
         rgb = np.zeros((h, w, 3), np.uint8)
         mask = np.zeros((h, w), np.uint8)
         rep = RefReport()
-        rc = lib().ref_process_sized(self._h, n, ws, hs, ptrs, rgb.ctypes.data, mask.ctypes.data,
-                                     C.byref(rep))
+        rc = lib().ref_process_sized(self._h, n, ws, hs, ptrs, mptrs, rgb.ctypes.data,
+                                     mask.ctypes.data, C.byref(rep))
         if rc != OK:
             raise RefError(rc)
         return rgb, mask, rep

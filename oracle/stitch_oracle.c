@@ -1239,7 +1239,11 @@ static void build_pairs(so_state* s) {
 /* rebuild_pair_geometry (pipeline.cpp:181-205): warp masks (geometry only:
  * the warped pixel values are not needed), view footprints, overlap bounds
  * and blend weights of every pair. */
-static int rebuild_pair_geometry(so_state* s) {
+/* With first frames that carry masks (frame.hpp:44-47), the pair bounds and
+ * blend weights come from the warps of those frames, as the reference's
+ * rebuild_pair_geometry warps first_frames; the view footprints stay the
+ * geometry-only ones (a superset of any frame's warp). */
+static int rebuild_pair_geometry_frames(so_state* s, const so_frame* first) {
   const so_config* cfg = &s->cfg;
   so_frame warped[SO_MAX_VIEWS];
   for (int v = 0; v < cfg->n_views; ++v) {
@@ -1248,11 +1252,16 @@ static int rebuild_pair_geometry(so_state* s) {
     int e = so_warp_frame_lift(&zero, s->inv[v], s->canvas_w, s->canvas_h, s->offx,
                                s->offy, s->lsin, s->lcos, s->lh, cfg->threads, &warped[v]);
     so_free_frame(&zero);
+    if (e == SO_OK) mask_bbox(&warped[v], &s->view_bbox[v]);
+    if (e == SO_OK && first && first[v].mask) {
+      so_free_frame(&warped[v]);
+      e = so_warp_frame_lift(&first[v], s->inv[v], s->canvas_w, s->canvas_h, s->offx,
+                             s->offy, s->lsin, s->lcos, s->lh, cfg->threads, &warped[v]);
+    }
     if (e != SO_OK) {
       for (int u = 0; u < v; ++u) so_free_frame(&warped[u]);
       return e;
     }
-    mask_bbox(&warped[v], &s->view_bbox[v]);
   }
   for (int k = 0; k < s->n_pairs; ++k) {
     so_pair* p = &s->pairs[k];
@@ -1275,6 +1284,15 @@ static int rebuild_pair_geometry(so_state* s) {
   }
   for (int v = 0; v < cfg->n_views; ++v) so_free_frame(&warped[v]);
   return SO_OK;
+}
+
+static int rebuild_pair_geometry(so_state* s) { return rebuild_pair_geometry_frames(s, NULL); }
+
+static int any_mask(const so_frame* first, int n) {
+  if (!first) return 0;
+  for (int v = 0; v < n; ++v)
+    if (first[v].mask) return 1;
+  return 0;
 }
 
 so_state* so_initialize(const so_config* cfg, int* err) {
@@ -1491,9 +1509,28 @@ static int refine_pair(so_state* s, const so_frame* warped, int k) {
   return SO_OK;
 }
 
+static void free_pair_weights(so_state* s) {
+  for (int k = 0; k < s->n_pairs; ++k) {
+    free(s->pairs[k].theta_i);
+    free(s->pairs[k].theta_j);
+    s->pairs[k].theta_i = s->pairs[k].theta_j = NULL;
+  }
+}
+
 so_state* so_initialize_frames(const so_config* cfg, const so_frame* first, int* err) {
   so_state* s = so_initialize(cfg, err);
-  if (!s || !cfg->refine_enabled || !first) return s;
+  if (!s || !first) return s;
+  if (any_mask(first, cfg->n_views)) {
+    /* masked first frames: the pair geometry of their warps (pipeline.cpp:246) */
+    free_pair_weights(s);
+    const int e = rebuild_pair_geometry_frames(s, first);
+    if (e != SO_OK) {
+      so_destroy(s);
+      *err = e;
+      return NULL;
+    }
+  }
+  if (!cfg->refine_enabled) return s;
   if (cfg->projection == 1) return s; /* refinement serves the planar canvas */
   so_frame warped[SO_MAX_VIEWS];
   for (int v = 0; v < cfg->n_views; ++v) {
@@ -1515,12 +1552,8 @@ so_state* so_initialize_frames(const so_config* cfg, const so_frame* first, int*
     return NULL;
   }
   /* refinement moved the maps: bounds and weights shift (pipeline.cpp:254) */
-  for (int k = 0; k < s->n_pairs; ++k) {
-    free(s->pairs[k].theta_i);
-    free(s->pairs[k].theta_j);
-    s->pairs[k].theta_i = s->pairs[k].theta_j = NULL;
-  }
-  const int e = rebuild_pair_geometry(s);
+  free_pair_weights(s);
+  const int e = rebuild_pair_geometry_frames(s, first);
   if (e != SO_OK) {
     so_destroy(s);
     *err = e;

@@ -32,6 +32,8 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
+from tests.golden.masks import case_masks  # noqa: E402
+
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "reference_small.json")
 
 OBJ = dict(enabled=True, half_size=40.0, velocity=(3.0, 1.0))
@@ -86,6 +88,18 @@ CASES = [
     ("small_frames", dict(seed=3, views=2, width=96, height=72, frames=4, obj=dict(
         enabled=True, half_size=12.0, velocity=(2.0, 1.0)), casts=[(1, 1, 1), (0.8, 1, 1.2)]),
      dict(refine_enabled=0), 4),
+    # MASKED INPUTS (Frame::mask, e.g. PNG alpha): the sampler skips masked taps
+    # (frame.cpp:95-104) and the pair geometry follows the masked first
+    # frames (pipeline.cpp:181-205); C1 with refinement, masks on both views
+    ("c1_masked", dict(views=2, width=640, height=480, frames=6, obj=OBJ, flicker=FLICKER,
+                       casts=[(1, 1, 1), (0.85, 1.0, 1.1)],
+                       masks=dict(seed=11, views=[0, 1])),
+     dict(refine_enabled=1), 6),
+    # 3-view star, masks on two views, one frame unmasked (mixed inputs)
+    ("star3_masked_mixed", dict(views=3, width=320, height=240, frames=4, obj=OBJ,
+                                casts=[(0.9, 1, 1), (1, 1, 1), (1, 0.95, 1.1)],
+                                masks=dict(seed=12, views=[0, 2], skip_frames=[2])),
+     dict(refine_enabled=0), 4),
     # perturbed principal point refined away, 5 frames
     ("principal_refine", dict(seed=5, views=3, width=320, height=240, frames=5,
                               focal_scale=1.02, principal_px=6.0, obj=OBJ,
@@ -98,12 +112,25 @@ def sha(a) -> str:
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
 
+def frame_masks(skw, t):
+    spec = skw.get("masks")
+    if spec is None:
+        return None
+    return [case_masks(spec, v, t, skw["width"], skw["height"]) for v in range(skw["views"])]
+
+
 def run_case(R, skw, okw, frames, threads=8):
+    skw = dict(skw)
+    mspec = skw.pop("masks", None)
     sc = R.Scene(**skw)
+    skw["masks"] = mspec
     first = [sc.render(v, 0) for v in range(sc.views)]
-    st = R.State(sc, R.default_opts(threads=threads, **okw), first)
+    st = R.State(sc, R.default_opts(threads=threads, **okw), first, frame_masks(skw, 0))
     out = {"canvas": list(st.canvas), "reference_view": sc.reference,
            "input_digest": [sha(f) for f in first], "pairs": []}
+    if mspec is not None:
+        out["mask_digest"] = [[None if m is None else sha(m) for m in frame_masks(skw, t)]
+                              for t in range(frames)]
     for k in range(st.n_pairs()):
         v, b, warn = st.pair(k)
         ti, tj = st.pair_weights(k)
@@ -114,7 +141,7 @@ def run_case(R, skw, okw, frames, threads=8):
     out["frames"] = []
     for t in range(frames):
         fr = [sc.render(v, t) for v in range(sc.views)]
-        rgb, mask, rep = st.process(fr)
+        rgb, mask, rep = st.process(fr, frame_masks(skw, t))
         out["frames"].append({
             "pano_rgb": sha(rgb), "pano_mask": sha(mask),
             "m": [sha(np.array(rep.m[k][:], np.float64)) for k in range(rep.n_pairs)],
