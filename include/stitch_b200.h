@@ -183,6 +183,15 @@ int stitch_b200_initialize(const stitch_b200_config* cfg, int device,
 int stitch_b200_initialize_frames(const stitch_b200_config* cfg,
                                   const uint8_t* const* frames, int device,
                                   stitch_b200_ctx** out);
+/* initialize_frames with masked first frames (masks: NULL, or per view NULL /
+ * width*height bytes, 0 = invalid): the pair bounds and blend weights follow
+ * the masked warps of the first frames, as the reference's
+ * rebuild_pair_geometry warps first_frames (pipeline.cpp:181-205); the
+ * feature refinement warps them with the masked sampler too. */
+int stitch_b200_initialize_frames_masked(const stitch_b200_config* cfg,
+                                         const uint8_t* const* frames,
+                                         const uint8_t* const* masks, int device,
+                                         stitch_b200_ctx** out);
 
 /* run_sequence's re-refinement branch (pipeline.cpp:395-406): a fresh
  * initialize(config, current frames) (with refinement when enabled) replaces
@@ -289,6 +298,20 @@ int stitch_b200_submit(stitch_b200_ctx* ctx, const uint8_t* const* frames,
 int stitch_b200_wait(stitch_b200_ctx* ctx, long long ticket,
                      stitch_b200_report* report);
 
+/* Masked input frames (Frame::mask, frame.hpp:44-47, e.g. PNG alpha,
+ * image_io.cpp:120-127): masks[v] is NULL (view unmasked) or width*height
+ * bytes, 0 = invalid pixel.  The warp skips masked taps exactly like
+ * sample_bilinear (frame.cpp:95-104), and the canvas evaluates the
+ * compose fold for every pixel of such a frame; results equal the
+ * reference's process_frame on the same masked frames.  masks == NULL is
+ * stitch_b200_process / stitch_b200_submit. */
+int stitch_b200_process_masked(stitch_b200_ctx* ctx, const uint8_t* const* frames,
+                               const uint8_t* const* masks, uint8_t* pano_rgb,
+                               uint8_t* pano_mask, stitch_b200_report* report);
+int stitch_b200_submit_masked(stitch_b200_ctx* ctx, const uint8_t* const* frames,
+                              const uint8_t* const* masks, uint8_t* pano_rgb,
+                              uint8_t* pano_mask, long long* ticket);
+
 /* Device-resident variant: frames[v] are device pointers; outputs stay in
  * the context (see stitch_b200_device_pano).  Ordered on the context's API
  * stream (stitch_b200_stream): inputs written there before the call are
@@ -389,12 +412,10 @@ int stitch_b200_n_views(const stitch_b200_ctx* ctx);
 int stitch_b200_slots(const stitch_b200_ctx* ctx);
 int stitch_b200_view_size(const stitch_b200_ctx* ctx, int view, int* width, int* height);
 /* Validates one frame set before process/submit: n must equal the configured
- * views, every frame must have the size its view was initialized with
- * (InputMismatch otherwise), and masks (may be NULL, or hold NULL entries for
- * unmasked frames) must be all-nonzero: the reference's masked sampler
- * (frame.cpp:95-104) is not part of the B200 path, so a frame with any
- * masked pixel is rejected with InputMismatch instead of being treated as
- * unmasked.  The C++ and Python mirrors call it on every frame set. */
+ * views and every frame must have the size its view was initialized with
+ * (InputMismatch otherwise).  masks (may be NULL) are accepted: frames that
+ * carry masks go through stitch_b200_process_masked / submit_masked.  The
+ * C++ and Python mirrors call it on every frame set. */
 int stitch_b200_check_frames(const stitch_b200_ctx* ctx, int n, const int* widths,
                              const int* heights, const uint8_t* const* masks);
 /* Set the calling thread's last error; returns code. */

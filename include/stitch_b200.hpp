@@ -284,18 +284,24 @@ inline PipelineState initialize(const StitchConfig& config, const std::vector<Fr
     throw StitchError(ErrorCode::ConfigurationError, "pipeline supports 2 to 16 views");
   if (first_frames.size() != config.views.size())
     throw StitchError(ErrorCode::ConfigurationError, "frame count does not match configured views");
+  bool any_mask = false;
   for (const Frame& f : first_frames) {
     if (f.data.size() != f.pixel_count() * 3)
       throw StitchError(ErrorCode::InputMismatch, "frame data must be width*height*3 bytes");
-    for (std::uint8_t m : f.mask)
-      if (m == 0)
-        throw StitchError(ErrorCode::InputMismatch,
-                          "masked input frames (frame.cpp:95-104) are not supported by the "
-                          "B200 path");
+    if (f.has_mask() && f.mask.size() != f.pixel_count())
+      throw StitchError(ErrorCode::InputMismatch, "frame mask must be width*height bytes");
+    any_mask = any_mask || f.has_mask();
   }
   stitch_b200_config c = to_c(config, first_frames);
   stitch_b200_ctx* ctx = nullptr;
-  if (config.refine.enabled) {
+  if (any_mask) {  // masked first frames decide the pair geometry (pipeline.cpp:181-205)
+    std::vector<const std::uint8_t*> ptrs, masks;
+    for (const Frame& f : first_frames) {
+      ptrs.push_back(f.data.data());
+      masks.push_back(f.has_mask() ? f.mask.data() : nullptr);
+    }
+    check(stitch_b200_initialize_frames_masked(&c, ptrs.data(), masks.data(), config.device, &ctx));
+  } else if (config.refine.enabled) {
     std::vector<const std::uint8_t*> ptrs;
     for (const Frame& f : first_frames) ptrs.push_back(f.data.data());
     check(stitch_b200_initialize_frames(&c, ptrs.data(), config.device, &ctx));
@@ -332,7 +338,13 @@ inline ProcessResult process_frame(PipelineState& state, const std::vector<Frame
   pano.data.resize(pano.pixel_count() * 3);
   pano.mask.resize(pano.pixel_count());
   stitch_b200_report r;
-  check(stitch_b200_process(state.handle(), ptrs.data(), pano.data.data(), pano.mask.data(), &r));
+  bool any_mask = false;
+  for (const std::uint8_t* m : masks) any_mask = any_mask || m != nullptr;
+  if (any_mask)  // Frame::mask: masked taps drop out (frame.cpp:95-104)
+    check(stitch_b200_process_masked(state.handle(), ptrs.data(), masks.data(), pano.data.data(),
+                                     pano.mask.data(), &r));
+  else
+    check(stitch_b200_process(state.handle(), ptrs.data(), pano.data.data(), pano.mask.data(), &r));
   FrameReport& rep = result.report;
   rep.frame_index = static_cast<long>(r.frame_index);
   for (int i = 0; i < kStageCount; ++i) rep.times.seconds[i] = r.stage_ms[i] * 1e-3;

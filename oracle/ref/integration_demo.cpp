@@ -7,7 +7,12 @@
 // byte: panorama RGB and mask, colour matrices (bitwise), rank flags,
 // thresholds, frame index.  Prints one JSON line; exit 0 iff identical.
 //
-//   integration_demo <views> <width> <height> <frames> [refine 0|1] [device]
+//   integration_demo <views> <width> <height> <frames> [refine 0|1] [device] [masked 0|1]
+//
+// masked = 1 gives every view a per-frame Frame::mask (a moving hole, a cut
+// border strip, scattered pixels), first frames included, as a PNG source
+// with alpha would (image_io.cpp:120-127).
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -36,6 +41,21 @@ int main(int argc, char** argv) {
   spec.frames = std::atoi(argv[4]);
   const bool refine = argc > 5 ? std::atoi(argv[5]) != 0 : true;
   const int device = argc > 6 ? std::atoi(argv[6]) : 0;
+  const bool masked = argc > 7 ? std::atoi(argv[7]) != 0 : false;
+  auto add_mask = [&](stitch::Frame& f, int view, int t) {
+    if (!masked) return;
+    f.mask.assign(f.pixel_count(), 1);
+    const int cx = (f.width / 3 + 9 * t + 31 * view) % f.width;
+    const int cy = (f.height / 2 + 5 * t) % f.height;
+    const int r = std::max(3, f.height / 9);
+    for (int y = 0; y < f.height; ++y)
+      for (int x = 0; x < f.width; ++x) {
+        const bool hole = (x - cx) * (x - cx) + (y - cy) * (y - cy) <= r * r;
+        const bool strip = view % 2 ? x >= f.width - 4 : x < 4;
+        const bool dot = ((x * 7 + y * 13 + t * 3 + view) % 89) == 0;
+        if (hole || strip || dot) f.mask[f.index(x, y)] = 0;
+      }
+  };
   spec.overlap_fraction = 0.3;
   for (int v = 0; v < spec.views; ++v)
     spec.color_casts.push_back(v == 0 ? std::array<double, 3>{1, 1, 1}
@@ -50,14 +70,20 @@ int main(int argc, char** argv) {
   cfg.threads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
   cfg.flow.threads = cfg.threads;
   std::vector<stitch::Frame> first;
-  for (int v = 0; v < spec.views; ++v) first.push_back(scene.render_view(v, 0));
+  for (int v = 0; v < spec.views; ++v) {
+    first.push_back(scene.render_view(v, 0));
+    add_mask(first.back(), v, 0);
+  }
   stitch::PipelineState cpu = stitch::initialize(cfg, first);
   stitch::PipelineState gpu = cpu;  // the same initialized state, driven by the binding
   int differing = 0, max_diff = 0;
   bool masks = true, reports = true;
   for (int t = 0; t < spec.frames; ++t) {
     std::vector<stitch::Frame> frames;
-    for (int v = 0; v < spec.views; ++v) frames.push_back(scene.render_view(v, t));
+    for (int v = 0; v < spec.views; ++v) {
+      frames.push_back(scene.render_view(v, t));
+      add_mask(frames.back(), v, t);
+    }
     const stitch::ProcessResult a = stitch::process_frame(cpu, frames);
     stitch::ProcessResult b;
     try {
@@ -89,9 +115,11 @@ int main(int argc, char** argv) {
   stitch::release_b200(gpu);
   const bool ok = differing == 0 && masks && reports;
   std::printf("{\"views\": %d, \"width\": %d, \"height\": %d, \"frames\": %d, \"refine\": %d, "
+              "\"masked\": %d, "
               "\"canvas\": [%d, %d], \"frames_differing\": %d, \"max_abs_diff\": %d, "
               "\"masks_equal\": %s, \"reports_equal\": %s, \"identical\": %s}\n",
-              spec.views, spec.width, spec.height, spec.frames, refine ? 1 : 0, cpu.canvas.width,
+              spec.views, spec.width, spec.height, spec.frames, refine ? 1 : 0, masked ? 1 : 0,
+              cpu.canvas.width,
               cpu.canvas.height, differing, max_diff, masks ? "true" : "false",
               reports ? "true" : "false", ok ? "true" : "false");
   return ok ? 0 : 1;

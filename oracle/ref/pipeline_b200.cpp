@@ -139,16 +139,23 @@ ProcessResult process_frame_b200(PipelineState& state, const std::vector<Frame>&
     ws.push_back(f.width);
     hs.push_back(f.height);
   }
-  // sizes as the twin was built for; masked input frames are rejected
+  // sizes as the twin was built for
   throw_b200(stitch_b200_check_frames(twin->ctx, static_cast<int>(frames.size()), ws.data(),
                                       hs.data(), masks.data()));
+  bool any_mask = false;
+  for (const uint8_t* m : masks) any_mask = any_mask || m != nullptr;
   int cw = 0, ch = 0;
   throw_b200(stitch_b200_canvas(twin->ctx, &cw, &ch, nullptr, nullptr));
   ProcessResult result;
   result.panorama = Frame::with_mask(cw, ch, 0, 0);
   stitch_b200_report r;
-  throw_b200(stitch_b200_process(twin->ctx, ptrs.data(), result.panorama.data.data(),
-                                 result.panorama.mask.data(), &r));
+  if (any_mask)  // Frame::mask (frame.hpp:44-47): masked taps drop out (frame.cpp:95-104)
+    throw_b200(stitch_b200_process_masked(twin->ctx, ptrs.data(), masks.data(),
+                                          result.panorama.data.data(),
+                                          result.panorama.mask.data(), &r));
+  else
+    throw_b200(stitch_b200_process(twin->ctx, ptrs.data(), result.panorama.data.data(),
+                                   result.panorama.mask.data(), &r));
   result.report.frame_index = state.frame_counter++;
   for (int k = 0; k < r.n_pairs; ++k) {
     Eigen::Matrix3d m;

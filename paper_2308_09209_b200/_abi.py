@@ -87,6 +87,9 @@ SYMBOLS = [
     ("stitch_b200_initialize", C.c_int, [C.POINTER(Config), C.c_int, C.POINTER(C.c_void_p)]),
     ("stitch_b200_update_geometry", C.c_int, [C.c_void_p, C.POINTER(Init)]),
     ("stitch_b200_update_maps", C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
+    ("stitch_b200_initialize_frames_masked", C.c_int, [C.POINTER(Config), C.POINTER(C.c_void_p),
+                                                       C.POINTER(C.c_void_p), C.c_int,
+                                                       C.POINTER(C.c_void_p)]),
     ("stitch_b200_initialize_frames", C.c_int, [C.POINTER(Config), C.c_void_p, C.c_int,
                                                 C.POINTER(C.c_void_p)]),
     ("stitch_b200_refine_warning", C.c_int, [C.c_void_p, C.c_int]),
@@ -141,6 +144,12 @@ SYMBOLS = [
                                        C.POINTER(C.c_int)]),
     ("stitch_b200_write_png", C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
     ("stitch_b200_n_views", C.c_int, [C.c_void_p]),
+    ("stitch_b200_process_masked", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p),
+                                             C.POINTER(C.c_void_p), C.c_void_p, C.c_void_p,
+                                             C.c_void_p]),
+    ("stitch_b200_submit_masked", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p),
+                                            C.POINTER(C.c_void_p), C.c_void_p, C.c_void_p,
+                                            C.POINTER(C.c_longlong)]),
     ("stitch_b200_slots", C.c_int, [C.c_void_p]),
     ("stitch_b200_check_frames", C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int),
                                            C.POINTER(C.c_int), C.c_void_p]),

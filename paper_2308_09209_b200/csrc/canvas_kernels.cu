@@ -16,36 +16,51 @@ namespace stitch_b200_dev {
 // bilinear neighbour downstream).  4 pixels per thread: three aligned 32-bit
 // loads, one 16-byte store.  grid: (x blocks, views)
 // ---------------------------------------------------------------------------
+// alpha: the frame's mask byte normalised to 0/1 (Frame::mask, frame.hpp:44-47),
+// 1 for an unmasked frame; only the masked samplers read it.
 __device__ __forceinline__ void expand_span(const std::uint8_t* __restrict__ src,
+                                            const std::uint8_t* __restrict__ mask,
                                             uchar4* __restrict__ dst, long long n) {
   const long long n4 = n / 4;
   const unsigned int* s4 = reinterpret_cast<const unsigned int*>(src);
+  const unsigned int* m4 = reinterpret_cast<const unsigned int*>(mask);
   uint4* d4 = reinterpret_cast<uint4*>(dst);
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const unsigned int w0 = __ldg(s4 + 3 * i), w1 = __ldg(s4 + 3 * i + 1),
                        w2 = __ldg(s4 + 3 * i + 2);
+    unsigned int a0 = 1u, a1 = 1u, a2 = 1u, a3 = 1u;
+    if (mask) {
+      const unsigned int m = __ldg(m4 + i);
+      a0 = (m & 0xffu) != 0u;
+      a1 = (m & 0xff00u) != 0u;
+      a2 = (m & 0xff0000u) != 0u;
+      a3 = (m & 0xff000000u) != 0u;
+    }
     uint4 o;
-    o.x = w0 & 0x00ffffffu;
-    o.y = (w0 >> 24) | ((w1 & 0x0000ffffu) << 8);
-    o.z = (w1 >> 16) | ((w2 & 0x000000ffu) << 16);
-    o.w = w2 >> 8;
+    o.x = (w0 & 0x00ffffffu) | (a0 << 24);
+    o.y = (w0 >> 24) | ((w1 & 0x0000ffffu) << 8) | (a1 << 24);
+    o.z = (w1 >> 16) | ((w2 & 0x000000ffu) << 16) | (a2 << 24);
+    o.w = (w2 >> 8) | (a3 << 24);
     d4[i] = o;
   }
   if (blockIdx.x == 0)
     for (long long i = n4 * 4 + threadIdx.x; i < n; i += blockDim.x)
-      dst[i] = make_uchar4(src[3 * i], src[3 * i + 1], src[3 * i + 2], 0);
+      dst[i] = make_uchar4(src[3 * i], src[3 * i + 1], src[3 * i + 2],
+                           mask ? (mask[i] != 0) : 1);
 }
 
 __global__ void __launch_bounds__(256) k_expand(const Geometry* __restrict__ g) {
   const int v = blockIdx.y;
   const ViewDesc& vd = g->views[v];
-  expand_span(g->frames[v], g->rgba[v], static_cast<long long>(vd.width) * vd.height);
+  expand_span(g->in.frames[v], g->in.masked ? g->in.masks[v] : nullptr, g->rgba[v],
+              static_cast<long long>(vd.width) * vd.height);
 }
 
 __global__ void __launch_bounds__(256) k_expand_one(const std::uint8_t* __restrict__ src,
+                                                    const std::uint8_t* __restrict__ mask,
                                                     uchar4* __restrict__ dst, long long n) {
-  expand_span(src, dst, n);
+  expand_span(src, mask, dst, n);
 }
 
 // ---------------------------------------------------------------------------
@@ -54,7 +69,15 @@ __global__ void __launch_bounds__(256) k_expand_one(const std::uint8_t* __restri
 // grid: (ceil(max_w/64), ceil(max_h/4), 2*n_pairs), block (64, 4)
 // ---------------------------------------------------------------------------
 template <bool CYL>
-__device__ __forceinline__ uchar4 warp_cv(const CanvasView& v, Lift L) {
+__device__ __forceinline__ uchar4 warp_cv(const CanvasView& v, Lift L, bool masked) {
+  if (masked) {  // a masked frame: masked taps drop out (frame.cpp:95-104)
+    ViewDesc d;
+    d.width = v.w;
+    d.height = v.h;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) d.inv[i] = v.inv[i];
+    return warp_sample<CYL, true>(d, v.rgba, L);
+  }
   if (v.f32) {  // experiment: FP32 interior weights (not bit-exact)
     double sx, sy, sz;
     warp_point<CYL>(v.inv, L, sx, sy, sz);
@@ -82,9 +105,11 @@ __global__ void __launch_bounds__(256) k_crop_warp(const __grid_constant__ Canva
   const int dy = blockIdx.y * 4 + threadIdx.y;
   if (dx >= p.w || dy >= p.h) return;
   const int view = side ? p.partner : p.view;
+  const bool masked = *P.masked;
   p.crop_raw[side][dy * p.w + dx] =
-      P.projection == 1 ? warp_cv<true>(P.views[view], canvas_lift<true>(P, p.x0 + dx, p.y0 + dy))
-                        : warp_cv<false>(P.views[view], canvas_lift<false>(P, p.x0 + dx, p.y0 + dy));
+      P.projection == 1
+          ? warp_cv<true>(P.views[view], canvas_lift<true>(P, p.x0 + dx, p.y0 + dy), masked)
+          : warp_cv<false>(P.views[view], canvas_lift<false>(P, p.x0 + dx, p.y0 + dy), masked);
 }
 
 // Staged variant (planar canvas; STITCH_B200_WARP_STAGE=1): a CTA owns a
@@ -109,9 +134,10 @@ __global__ void __launch_bounds__(256) k_crop_warp_staged(const __grid_constant_
   const int view = side ? p.partner : p.view;
   const CanvasView& v = P.views[view];
   const int tid = threadIdx.y * 32 + threadIdx.x;
+  const bool masked = *P.masked;
   if (tid == 0) {
     double mnx = 1e300, mny = 1e300, mxx = -1e300, mxy = -1e300;
-    bool ok = true;
+    bool ok = !masked;  // masked frames take the masked global sampler
     const int xs[2] = {bx0, min(bx0 + 31, p.w - 1)}, ys[2] = {by0, min(by0 + 7, p.h - 1)};
     for (int j = 0; j < 2; ++j)
       for (int i = 0; i < 2; ++i) {
@@ -163,7 +189,9 @@ __global__ void __launch_bounds__(256) k_crop_warp_staged(const __grid_constant_
     const double qx = ddiv(sx, dz), qy = ddiv(sy, dz);
     float r, g, b;
     int valid = ww ? sample_rgba_win(win, kStageW, wx0, wy0, ww, wh, v.w, v.h, qx, qy, r, g, b) : -1;
-    if (valid < 0) valid = sample_rgba(v.rgba, v.w, v.h, qx, qy, r, g, b) ? 1 : 0;
+    if (valid < 0)
+      valid = (masked ? sample_crop(v.rgba, v.w, v.h, qx, qy, r, g, b)
+                      : sample_rgba(v.rgba, v.w, v.h, qx, qy, r, g, b)) ? 1 : 0;
     if (valid) o = make_uchar4(quantize_f(r), quantize_f(g), quantize_f(b), 1);
   }
   p.crop_raw[side][dy * p.w + dx] = o;
@@ -377,7 +405,8 @@ __device__ __forceinline__ bool in_rect(const CanvasPair& p, int x, int y) {
 // fold over pairs (pipeline.cpp:326-333, flow.cpp:324-357).
 template <bool CYL>
 __device__ __forceinline__ uchar4 canvas_pixel(const CanvasParams& P,
-                                               const double (*mview)[9], int x, int y) {
+                                               const double (*mview)[9], int x, int y,
+                                               bool masked) {
   const int ref = P.ref;
   const CanvasView& vr = P.views[ref];
   const int np = P.np;
@@ -397,7 +426,7 @@ __device__ __forceinline__ uchar4 canvas_pixel(const CanvasParams& P,
       const CanvasPair& p = P.pairs[kc];
       pv = p.crop_raw[1][(y - p.y0) * p.w + (x - p.x0)];
     } else {
-      pv = warp_cv<CYL>(vr, L);
+      pv = warp_cv<CYL>(vr, L, masked);
     }
   }
   for (int k = 0; k < np; ++k) {
@@ -406,7 +435,7 @@ __device__ __forceinline__ uchar4 canvas_pixel(const CanvasParams& P,
     if (!may_cover(vv, x, y)) continue;
     const int dx = x - p.x0, dy = y - p.y0;
     const bool inb = dx >= 0 && dy >= 0 && dx < p.w && dy < p.h;
-    const uchar4 q = inb ? p.crop_raw[0][dy * p.w + dx] : warp_cv<CYL>(vv, L);
+    const uchar4 q = inb ? p.crop_raw[0][dy * p.w + dx] : warp_cv<CYL>(vv, L, masked);
     if (!q.w) continue;
     if (pv.w) {
       if (inb) {
@@ -439,6 +468,8 @@ __global__ void __launch_bounds__(256, kCanvasCtasPerSm) k_canvas(const __grid_c
   for (int i = threadIdx.x; i < kMaxViews * 9; i += blockDim.x) mview[i / 9][i % 9] = st->mview[i / 9][i % 9];
   __syncthreads();
   const int cw = P.cw, ch = P.ch;
+  // a masked frame's coverage is not the geometry's: every pixel runs the fold
+  const bool masked = *P.masked;
   const int tiles_x = (cw + 63) / 64;
   const int ntiles = tiles_x * ((ch + 3) / 4);
   // tile -> (column, row) kept incrementally: the grid stride advances by
@@ -459,16 +490,16 @@ __global__ void __launch_bounds__(256, kCanvasCtasPerSm) k_canvas(const __grid_c
     if (x >= cw || y >= ch) continue;
     const long long idx = static_cast<long long>(y) * cw + x;
     uchar4 pv;
-    const std::uint8_t c = P.cls ? P.cls[idx] : kClassFold;
+    const std::uint8_t c = (P.cls && !masked) ? P.cls[idx] : kClassFold;
     if (c == kClassFold) {
-      pv = canvas_pixel<CYL>(P, mview, x, y);
+      pv = canvas_pixel<CYL>(P, mview, x, y, masked);
     } else if (c == kClassNone) {
       pv = make_uchar4(0, 0, 0, 0);
     } else {
       // a single view provides the pixel: its warp, colour-corrected unless
       // it is the reference (the fold's result, without evaluating the
       // views that do not cover the pixel)
-      pv = warp_cv<CYL>(P.views[c], canvas_lift<CYL>(P, x, y));
+      pv = warp_cv<CYL>(P.views[c], canvas_lift<CYL>(P, x, y), false);
       if (c != P.ref) pv = apply_matrix(mview[c], pv);
     }
     pano[idx] = pv;
@@ -539,6 +570,7 @@ __global__ void __launch_bounds__(256) k_tone(const DevState* __restrict__ st,
 }
 
 // Full-canvas warp of one view (init masks and debug readback).
+template <bool MASKED>
 __global__ void __launch_bounds__(256) k_warp_view(const Geometry* __restrict__ g, int view,
                                                    const uchar4* __restrict__ frame,
                                                    std::uint8_t* __restrict__ rgb,
@@ -549,8 +581,9 @@ __global__ void __launch_bounds__(256) k_warp_view(const Geometry* __restrict__ 
        idx += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int y = static_cast<int>(idx / g->canvas_w);
     const int x = static_cast<int>(idx - static_cast<long long>(y) * g->canvas_w);
-    const uchar4 o = g->projection == 1 ? warp_sample<true>(v, frame, canvas_lift<true>(*g, x, y))
-                                        : warp_sample<false>(v, frame, canvas_lift<false>(*g, x, y));
+    const uchar4 o = g->projection == 1
+                         ? warp_sample<true, MASKED>(v, frame, canvas_lift<true>(*g, x, y))
+                         : warp_sample<false, MASKED>(v, frame, canvas_lift<false>(*g, x, y));
     if (rgb) {
       rgb[3 * idx + 0] = o.x;
       rgb[3 * idx + 1] = o.y;
@@ -641,8 +674,9 @@ void launch_expand(const Geometry* g, int n_views, long long max_px, cudaStream_
   k_expand<<<grid, 256, 0, s>>>(g);
 }
 
-void launch_expand_one(const std::uint8_t* rgb, uchar4* rgba, long long n_px, cudaStream_t s) {
-  k_expand_one<<<blocks_for(n_px / 4 + 1, 256, 148 * 4), 256, 0, s>>>(rgb, rgba, n_px);
+void launch_expand_one(const std::uint8_t* rgb, uchar4* rgba, long long n_px, cudaStream_t s,
+                       const std::uint8_t* mask) {
+  k_expand_one<<<blocks_for(n_px / 4 + 1, 256, 148 * 4), 256, 0, s>>>(rgb, mask, rgba, n_px);
 }
 
 void launch_crop_warp(const CanvasParams& P, int max_w, int max_h, cudaStream_t s) {
@@ -674,8 +708,11 @@ void launch_tone(const DevState* st, const uchar4* pano, long long n_px, std::ui
 }
 
 void launch_warp_view(const Geometry* g, int view, const uchar4* frame, std::uint8_t* rgb,
-                      std::uint8_t* mask, cudaStream_t s) {
-  k_warp_view<<<148 * 8, 256, 0, s>>>(g, view, frame, rgb, mask);
+                      std::uint8_t* mask, cudaStream_t s, bool masked) {
+  if (masked)
+    k_warp_view<true><<<148 * 8, 256, 0, s>>>(g, view, frame, rgb, mask);
+  else
+    k_warp_view<false><<<148 * 8, 256, 0, s>>>(g, view, frame, rgb, mask);
 }
 
 void launch_warp_mask(const Geometry* g, int view, std::uint8_t* mask, cudaStream_t s) {

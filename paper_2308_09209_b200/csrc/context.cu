@@ -234,7 +234,7 @@ struct Ctx {
   std::vector<std::pair<long long, stitch_b200_report>> done_reports;
   int last_slot = 0;
   // pinned ring for device-frame pointer tables
-  const std::uint8_t** h_ptr_ring = nullptr;
+  FrameTable* h_ptr_ring = nullptr;  // pinned ring of per-frame tables
   cudaEvent_t ring_ev[16] = {};
   int ring_pos = 0;
   DevReport* h_report = nullptr;  // one per slot (pinned)
@@ -242,6 +242,10 @@ struct Ctx {
   // use), the caller's output pointers to fill when the slot retires, and
   // the copy workers
   std::uint8_t* h_stage_in[kMaxSlots][kMaxViews] = {};
+  // input masks (Frame::mask) of host-path frames: device buffers per slot
+  // (allocated on the first masked frame) and their pinned staging
+  std::uint8_t* d_mask[kMaxSlots][kMaxViews] = {};
+  std::uint8_t* h_stage_min[kMaxSlots][kMaxViews] = {};
   std::uint8_t* h_stage_rgb[kMaxSlots] = {};
   std::uint8_t* h_stage_mask[kMaxSlots] = {};
   std::uint8_t* user_rgb[kMaxSlots] = {};
@@ -295,6 +299,8 @@ struct Ctx {
     if (h_report) cudaFreeHost(h_report);
     for (int s = 0; s < kMaxSlots; ++s) {
       for (auto* q : h_stage_in[s])
+        if (q) cudaFreeHost(q);
+      for (auto* q : h_stage_min[s])
         if (q) cudaFreeHost(q);
       if (h_stage_rgb[s]) cudaFreeHost(h_stage_rgb[s]);
       for (cudaEvent_t e : out_ev[s])
@@ -383,11 +389,12 @@ LiftTables make_lift(const stitch_b200_init* in) {
 // for the given pairs, overlap bounds + blend weights.
 int init_geometry(int device, const Geometry& geom, const LiftTables& lt, int n_views,
                   const std::vector<std::pair<int, int>>& pairs, std::vector<ViewFootprint>& views,
-                  std::vector<PairGeometry>& pair_geo) {
+                  std::vector<PairGeometry>& pair_geo,
+                  const std::vector<const uchar4*>* first_rgba = nullptr) {
   CUDA_TRY(cudaSetDevice(device));
   CUDA_TRY(gpu_init_geometry(geom, lt.s.data(), lt.c.data(), lt.h.data(),
                              static_cast<int>(lt.s.size()), static_cast<int>(lt.h.size()), n_views,
-                             pairs, views, pair_geo));
+                             pairs, views, pair_geo, first_rgba));
   return STITCH_B200_OK;
 }
 
@@ -536,7 +543,7 @@ int build_context(const stitch_b200_init* in, int device,
         for (int s2 = 1; s2 < ctx->n_slots; ++s2)
           CUDA_TRY(ctx->alloc(&ctx->d_in[s2][v], ctx->frame_bytes[v]));
       }
-      g.frames[v] = ctx->d_in[sl][v];
+      g.in.frames[v] = ctx->d_in[sl][v];
       const long long vpx = static_cast<long long>(in->view_width[v]) * in->view_height[v];
       CUDA_TRY(ctx->alloc(&g.rgba[v], vpx));
       ctx->max_view_px = std::max(ctx->max_view_px, vpx);
@@ -821,6 +828,9 @@ int build_context(const stitch_b200_init* in, int device,
     }
     {
       CanvasParams& P = S.cparams;
+      // device address of this slot's FrameTable::masked (no dereference)
+      P.masked = reinterpret_cast<const int*>(reinterpret_cast<const char*>(S.dg) +
+                                              offsetof(Geometry, in) + offsetof(FrameTable, masked));
       P.cw = g.canvas_w;
       P.ch = g.canvas_h;
       P.ref = g.reference;
@@ -907,8 +917,8 @@ int build_context(const stitch_b200_init* in, int device,
   CUDA_TRY(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
   CUDA_TRY(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
   for (auto& e : ctx->ring_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_ptr_ring),
-                         sizeof(void*) * kMaxViews * 16, cudaHostAllocDefault));
+  CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_ptr_ring), sizeof(FrameTable) * 16,
+                         cudaHostAllocDefault));
   CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_report),
                          sizeof(DevReport) * ctx->n_slots, cudaHostAllocDefault));
 
@@ -961,15 +971,24 @@ int build_context(const stitch_b200_init* in, int device,
 
 // Point the slot's frame table at this frame's device inputs (pinned ring
 // of pointer tables, copied on the slot's stream).
-int set_frame_pointers(Ctx* ctx, int slot, const std::uint8_t* const* ptrs) {
+// The slot's per-frame table (inputs, masks, masked flag) from a pinned ring
+// entry, stream-ordered before the frame's kernels.  masks: nullptr or per
+// view nullptr (unmasked) / device W*H bytes.
+int set_frame_pointers(Ctx* ctx, int slot, const std::uint8_t* const* ptrs,
+                       const std::uint8_t* const* masks = nullptr) {
   const int r = ctx->ring_pos;
   ctx->ring_pos = (ctx->ring_pos + 1) % 16;
   CUDA_TRY(cudaEventSynchronize(ctx->ring_ev[r]));
-  const std::uint8_t** h = ctx->h_ptr_ring + r * kMaxViews;
-  for (int v = 0; v < ctx->hg.n_views; ++v) h[v] = ptrs[v];
+  FrameTable* h = ctx->h_ptr_ring + r;
+  std::memset(h, 0, sizeof(FrameTable));
+  for (int v = 0; v < ctx->hg.n_views; ++v) {
+    h->frames[v] = ptrs[v];
+    h->masks[v] = masks ? masks[v] : nullptr;
+    h->masked |= h->masks[v] != nullptr;
+  }
   cudaStream_t cs = ctx->slot[slot].cs;
-  CUDA_TRY(cudaMemcpyAsync(ctx->slot[slot].dg->frames, h, sizeof(void*) * ctx->hg.n_views,
-                           cudaMemcpyHostToDevice, cs));
+  CUDA_TRY(cudaMemcpyAsync(&ctx->slot[slot].dg->in, h, sizeof(FrameTable), cudaMemcpyHostToDevice,
+                           cs));
   CUDA_TRY(cudaEventRecord(ctx->ring_ev[r], cs));
   return STITCH_B200_OK;
 }
@@ -1038,11 +1057,12 @@ int retire_slot(Ctx* ctx, int slot) {
 // between slots: the colour solves (3D-M windows) wait for the previous
 // frame's, the canvas (threshold history, frame counter) for the previous
 // frame's canvas.  Everything else of consecutive frames overlaps.
-int enqueue_frame(Ctx* ctx, int slot, const std::uint8_t* const* dev_in) {
+int enqueue_frame(Ctx* ctx, int slot, const std::uint8_t* const* dev_in,
+                  const std::uint8_t* const* dev_masks = nullptr) {
   SlotRes& S = ctx->slot[slot];
   const int prev = (slot + ctx->n_slots - 1) % ctx->n_slots;
   CUDA_TRY(cudaStreamWaitEvent(S.cs, ctx->d2h_done[slot], 0));
-  int rc = set_frame_pointers(ctx, slot, dev_in);
+  int rc = set_frame_pointers(ctx, slot, dev_in, dev_masks);
   if (rc) return rc;
   if (S.exec[0]) CUDA_TRY(cudaGraphLaunch(S.exec[0], S.cs));
   CUDA_TRY(cudaStreamWaitEvent(S.cs, ctx->color_done[prev], 0));
@@ -1115,7 +1135,8 @@ int ensure_staging(Ctx* ctx, int slot) {
 // stream; returns the frame's ticket.  Pinned caller buffers are copied
 // directly; pageable ones through the slot's pinned staging ring.
 int submit_host(Ctx* ctx, const std::uint8_t* const* frames, std::uint8_t* pano_rgb,
-                std::uint8_t* pano_mask, long long* ticket) {
+                std::uint8_t* pano_mask, long long* ticket,
+                const std::uint8_t* const* masks = nullptr) {
   const int slot = static_cast<int>(ctx->seq % ctx->n_slots);
   int rc = retire_slot(ctx, slot);
   if (rc) return rc;
@@ -1155,9 +1176,36 @@ int submit_host(Ctx* ctx, const std::uint8_t* const* frames, std::uint8_t* pano_
   }
   CUDA_TRY(cudaEventRecord(ctx->h2d_done[slot], ctx->h2d));
   CUDA_TRY(cudaStreamWaitEvent(ctx->slot[slot].cs, ctx->h2d_done[slot], 0));
+  // input masks (Frame::mask) travel with the frame to the slot's mask buffers
+  const std::uint8_t* dmask[kMaxViews] = {};
+  bool any_mask = false;
+  for (int v = 0; masks && v < ctx->hg.n_views; ++v) {
+    if (!masks[v]) continue;
+    any_mask = true;
+    const size_t mb = ctx->frame_bytes[v] / 3;
+    if (!ctx->d_mask[slot][v]) CUDA_TRY(ctx->alloc(&ctx->d_mask[slot][v], mb));
+    const std::uint8_t* src = masks[v];
+    if (!is_pinned(src)) {
+      if (!ctx->h_stage_min[slot][v])
+        CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_stage_min[slot][v]), mb,
+                               cudaHostAllocDefault));
+      if (!ctx->copier) {
+        rc = ensure_staging(ctx, slot);
+        if (rc) return rc;
+      }
+      ctx->copier->run({{ctx->h_stage_min[slot][v], src, mb}});
+      src = ctx->h_stage_min[slot][v];
+    }
+    CUDA_TRY(cudaMemcpyAsync(ctx->d_mask[slot][v], src, mb, cudaMemcpyHostToDevice, ctx->h2d));
+    dmask[v] = ctx->d_mask[slot][v];
+  }
+  if (any_mask) {
+    CUDA_TRY(cudaEventRecord(ctx->h2d_done[slot], ctx->h2d));
+    CUDA_TRY(cudaStreamWaitEvent(ctx->slot[slot].cs, ctx->h2d_done[slot], 0));
+  }
   const std::uint8_t* in[kMaxViews];
   for (int v = 0; v < ctx->hg.n_views; ++v) in[v] = ctx->d_in[slot][v];
-  rc = enqueue_frame(ctx, slot, in);
+  rc = enqueue_frame(ctx, slot, in, any_mask ? dmask : nullptr);
   if (rc) return rc;
   CUDA_TRY(cudaStreamWaitEvent(ctx->d2h, ctx->comp_done[slot], 0));
   const size_t rgb_bytes = static_cast<size_t>(ctx->n_px) * 3, mask_bytes = static_cast<size_t>(ctx->n_px);
@@ -1267,6 +1315,7 @@ int stitch_b200_create(const stitch_b200_init* init, int device, stitch_b200_ctx
 // transport and refine_homography on the host.  maps / invs of refined views
 // are replaced; warn[k] = PairState::refine_warning.
 static int refine_maps(int device, const stitch_b200_config* cfg, const uint8_t* const* frames,
+                       const uint8_t* const* masks,
                        const Geometry& geom, const std::vector<PairGeometry>& pgeo,
                        const std::vector<hg_ns::PairSpec>& pairs, std::vector<hg_ns::Mat3>& maps,
                        std::vector<hg_ns::Mat3>& invs, std::vector<int>& warn) {
@@ -1307,10 +1356,16 @@ static int refine_maps(int device, const stitch_b200_config* cfg, const uint8_t*
       CUDA_TRY(dalloc(&src, 3 * npx));
       CUDA_TRY(dalloc(&rgba, 4 * npx));
       CUDA_TRY(cudaMemcpyAsync(src, frames[v], 3 * npx, cudaMemcpyHostToDevice, s));
+      void* dm = nullptr;  // the first frame's mask (Frame::mask) as the RGBA alpha
+      if (masks && masks[v]) {
+        CUDA_TRY(dalloc(&dm, npx));
+        CUDA_TRY(cudaMemcpyAsync(dm, masks[v], npx, cudaMemcpyHostToDevice, s));
+      }
       launch_expand_one(static_cast<const std::uint8_t*>(src), static_cast<uchar4*>(rgba),
-                        static_cast<long long>(npx), s);
+                        static_cast<long long>(npx), s, static_cast<const std::uint8_t*>(dm));
       launch_warp_view(static_cast<const Geometry*>(dg), v, static_cast<const uchar4*>(rgba),
-                       static_cast<std::uint8_t*>(wrgb), static_cast<std::uint8_t*>(wmask), s);
+                       static_cast<std::uint8_t*>(wrgb), static_cast<std::uint8_t*>(wmask), s,
+                       dm != nullptr);
       CUDA_TRY(cudaGetLastError());
       fv[v].reset(new FeatView());
       CUDA_TRY(fv[v]->build(static_cast<const std::uint8_t*>(wrgb), cw, ch, s));
@@ -1383,8 +1438,44 @@ static int refine_maps(int device, const stitch_b200_config* cfg, const uint8_t*
   return STITCH_B200_OK;
 }
 
+// The first frames expanded to RGBA with their masks as alpha, on the device
+// (masked views only), for the pair geometry of masked first frames.
+struct FirstFrames {
+  std::vector<void*> bufs;
+  std::vector<const uchar4*> rgba;
+  ~FirstFrames() {
+    for (void* p : bufs) cudaFree(p);
+  }
+};
+
+static int upload_masked_first(int device, const stitch_b200_config* cfg,
+                               const uint8_t* const* frames, const uint8_t* const* masks,
+                               FirstFrames& ff) {
+  CUDA_TRY(cudaSetDevice(device));
+  ff.rgba.assign(static_cast<size_t>(cfg->n_views), nullptr);
+  for (int v = 0; v < cfg->n_views; ++v) {
+    if (!masks[v]) continue;
+    const size_t npx = static_cast<size_t>(cfg->width[v]) * cfg->height[v];
+    void *src = nullptr, *dm = nullptr, *rgba = nullptr;
+    CUDA_TRY(cudaMalloc(&src, 3 * npx + 16));
+    ff.bufs.push_back(src);
+    CUDA_TRY(cudaMalloc(&dm, npx + 16));
+    ff.bufs.push_back(dm);
+    CUDA_TRY(cudaMalloc(&rgba, 4 * npx + 16));
+    ff.bufs.push_back(rgba);
+    CUDA_TRY(cudaMemcpy(src, frames[v], 3 * npx, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(dm, masks[v], npx, cudaMemcpyHostToDevice));
+    launch_expand_one(static_cast<const std::uint8_t*>(src), static_cast<uchar4*>(rgba),
+                      static_cast<long long>(npx), 0, static_cast<const std::uint8_t*>(dm));
+    CUDA_TRY(cudaGetLastError());
+    ff.rgba[v] = static_cast<const uchar4*>(rgba);
+  }
+  CUDA_TRY(cudaDeviceSynchronize());
+  return STITCH_B200_OK;
+}
+
 static int initialize_impl(const stitch_b200_config* cfg, const uint8_t* const* frames, int device,
-                           stitch_b200_ctx** out) {
+                           stitch_b200_ctx** out, const uint8_t* const* masks = nullptr) {
   *out = nullptr;
   if (cfg->refine_enabled && !frames)
     return fail(STITCH_B200_ConfigurationError,
@@ -1458,20 +1549,31 @@ static int initialize_impl(const stitch_b200_config* cfg, const uint8_t* const* 
   for (const auto& pr : pairs) vp.emplace_back(pr.view, pr.partner);
   std::vector<ViewFootprint> views;
   std::vector<PairGeometry> pgeo;
-  int rc = init_geometry(device, g, make_lift(&in), cfg->n_views, vp, views, pgeo);
+  // masked first frames decide the pair geometry (rebuild_pair_geometry warps
+  // first_frames, pipeline.cpp:181-205)
+  bool any_mask = false;
+  for (int v = 0; frames && masks && v < cfg->n_views; ++v) any_mask |= masks[v] != nullptr;
+  FirstFrames ff;
+  if (any_mask) {
+    int rc0 = upload_masked_first(device, cfg, frames, masks, ff);
+    if (rc0) return rc0;
+  }
+  const std::vector<const uchar4*>* first_rgba = any_mask ? &ff.rgba : nullptr;
+  int rc = init_geometry(device, g, make_lift(&in), cfg->n_views, vp, views, pgeo, first_rgba);
   if (rc) return rc;
   std::vector<int> warn(pairs.size(), 0);
   if (cfg->refine_enabled) {
     for (size_t k = 0; k < pairs.size(); ++k)
       if (!pgeo[k].ok) return fail(STITCH_B200_ConfigurationError, "adjacent views do not overlap");
-    rc = refine_maps(device, cfg, frames, g, pgeo, pairs, maps, invs, warn);
+    rc = refine_maps(device, cfg, frames, any_mask ? masks : nullptr, g, pgeo, pairs, maps, invs,
+                     warn);
     if (rc) return rc;
     // refinement moved the maps: bounds and weights shift (pipeline.cpp:254);
     // the canvas is kept (the reference computes it before refining)
     for (int v = 0; v < cfg->n_views; ++v)
       for (int i = 0; i < 9; ++i) in.inv_maps[v][i] = invs[v][i];
     fill_views(g, &in);
-    rc = init_geometry(device, g, make_lift(&in), cfg->n_views, vp, views, pgeo);
+    rc = init_geometry(device, g, make_lift(&in), cfg->n_views, vp, views, pgeo, first_rgba);
     if (rc) return rc;
   }
   in.n_pairs = static_cast<int>(pairs.size());
@@ -1502,6 +1604,13 @@ int stitch_b200_initialize_frames(const stitch_b200_config* cfg, const uint8_t* 
                                   int device, stitch_b200_ctx** out) {
   if (!frames) return fail(STITCH_B200_ConfigurationError, "frames must not be NULL");
   return initialize_impl(cfg, frames, device, out);
+}
+
+int stitch_b200_initialize_frames_masked(const stitch_b200_config* cfg,
+                                         const uint8_t* const* frames, const uint8_t* const* masks,
+                                         int device, stitch_b200_ctx** out) {
+  if (!frames) return fail(STITCH_B200_ConfigurationError, "frames must not be NULL");
+  return initialize_impl(cfg, frames, device, out, masks);
 }
 
 static int carry_into(stitch_b200_ctx* h, std::unique_ptr<Ctx>& fresh);
@@ -1661,14 +1770,8 @@ int stitch_b200_check_frames(const stitch_b200_ctx* h, int n, const int* widths,
                     v, widths[v], heights[v], w, ht);
       return fail(STITCH_B200_InputMismatch, msg);
     }
-    if (masks && masks[v]) {
-      const size_t px = static_cast<size_t>(w) * static_cast<size_t>(ht);
-      if (std::memchr(masks[v], 0, px) != nullptr)
-        return fail(STITCH_B200_InputMismatch,
-                    "masked input frames (a 0 in Frame::mask, frame.cpp:95-104) are not "
-                    "supported by the B200 path");
-    }
   }
+  (void)masks;  // masked frames are supported (stitch_b200_process_masked / submit_masked)
   return STITCH_B200_OK;
 }
 
@@ -1714,6 +1817,26 @@ int stitch_b200_submit(stitch_b200_ctx* h, const uint8_t* const* frames, uint8_t
   Ctx* ctx = h->c.get();
   CUDA_TRY(cudaSetDevice(ctx->device));
   return submit_host(ctx, frames, pano_rgb, pano_mask, ticket);
+}
+
+int stitch_b200_process_masked(stitch_b200_ctx* h, const uint8_t* const* frames,
+                               const uint8_t* const* masks, uint8_t* pano_rgb, uint8_t* pano_mask,
+                               stitch_b200_report* report) {
+  Ctx* ctx = h->c.get();
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  long long ticket = -1;
+  int rc = submit_host(ctx, frames, pano_rgb, pano_mask, &ticket, masks);
+  if (rc) return rc;
+  stitch_b200_report tmp;
+  return wait_ticket(ctx, ticket, report ? report : &tmp);
+}
+
+int stitch_b200_submit_masked(stitch_b200_ctx* h, const uint8_t* const* frames,
+                              const uint8_t* const* masks, uint8_t* pano_rgb, uint8_t* pano_mask,
+                              long long* ticket) {
+  Ctx* ctx = h->c.get();
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  return submit_host(ctx, frames, pano_rgb, pano_mask, ticket, masks);
 }
 
 int stitch_b200_wait(stitch_b200_ctx* h, long long ticket, stitch_b200_report* report) {

@@ -225,7 +225,8 @@ struct DevBuf {
 cudaError_t gpu_init_geometry(const Geometry& geom_in, const double* lift_s, const double* lift_c,
                               const double* lift_h, int n_lift_x, int n_lift_y, int n_views,
                               const std::vector<std::pair<int, int>>& pairs,
-                              std::vector<ViewFootprint>& views, std::vector<PairGeometry>& out) {
+                              std::vector<ViewFootprint>& views, std::vector<PairGeometry>& out,
+                              const std::vector<const uchar4*>* first_rgba) {
   Geometry geom = geom_in;
   const int w = geom.canvas_w, h = geom.canvas_h;
   const long long P = static_cast<long long>(w) * h;
@@ -279,6 +280,13 @@ cudaError_t gpu_init_geometry(const Geometry& geom_in, const double* lift_s, con
   k_mask_extent<<<dim3(296, n_views), 256, 0, s>>>(masks, P, w, h, static_cast<int2*>(djobs.p),
                                                   static_cast<int*>(dext.p),
                                                   static_cast<std::uint8_t*>(docc.p));
+  // masked first frames: from here on (pair bounds, chamfer weights) the masks
+  // are the warps of those frames (warp_frame with the masked sampler)
+  if (first_rgba)
+    for (int v = 0; v < n_views && v < static_cast<int>(first_rgba->size()); ++v)
+      if ((*first_rgba)[v])
+        launch_warp_view(static_cast<const Geometry*>(dgeom.p), v, (*first_rgba)[v], nullptr,
+                         masks + v * P, s, true);
   if (!pairs.empty())
     k_mask_extent<<<dim3(296, static_cast<unsigned>(pairs.size())), 256, 0, s>>>(
         masks, P, w, h, static_cast<int2*>(djobs.p) + n_views,

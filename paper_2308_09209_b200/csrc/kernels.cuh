@@ -84,9 +84,20 @@ struct BalanceState {
   int m1[3][3], m2[3][3];
 };
 
+// The per-frame part of the geometry, rewritten for every frame: the device
+// RGB8 inputs, their masks (Frame::mask, frame.hpp:44-47: W*H bytes, 0 =
+// invalid; nullptr = unmasked view) and whether this frame carries any mask.
+// A masked frame's samplers skip masked taps (frame.cpp:95-104) and the
+// canvas evaluates every pixel's fold instead of the geometry-only class map.
+struct FrameTable {
+  const std::uint8_t* frames[kMaxViews];
+  const std::uint8_t* masks[kMaxViews];
+  int masked;
+};
+
 struct Geometry {
-  const std::uint8_t* frames[kMaxViews];  // device RGB8 inputs (per frame)
-  uchar4* rgba[kMaxViews];                // the inputs expanded to RGBA8
+  FrameTable in;                          // per frame
+  uchar4* rgba[kMaxViews];                // the inputs expanded to RGBA8 (.w = valid)
   // canvas lift (extension): 0 planar (x+offx, y+offy, 1); 1 cylindrical
   // (sin t[x], h[y], cos t[x]) from host-computed tables
   int projection;
@@ -144,6 +155,7 @@ struct CanvasPair {
 };
 
 struct CanvasParams {
+  const int* masked;  // -> the slot's FrameTable::masked (device, per frame)
   int cw, ch, ref, np, weighting;
   double offx, offy;
   int projection;
@@ -257,8 +269,9 @@ void launch_canvas(const CanvasParams& P, const Geometry* g, DevState* st, uchar
 void launch_tone(const DevState* st, const uchar4* pano, long long n_px,
                  std::uint8_t* out_rgb, std::uint8_t* out_mask, cudaStream_t s);
 void launch_warp_view(const Geometry* g, int view, const uchar4* frame, std::uint8_t* rgb,
-                      std::uint8_t* mask, cudaStream_t s);
-void launch_expand_one(const std::uint8_t* rgb, uchar4* rgba, long long n_px, cudaStream_t s);
+                      std::uint8_t* mask, cudaStream_t s, bool masked = false);
+void launch_expand_one(const std::uint8_t* rgb, uchar4* rgba, long long n_px, cudaStream_t s,
+                       const std::uint8_t* mask = nullptr);
 void launch_warp_mask(const Geometry* g, int view, std::uint8_t* mask, cudaStream_t s);
 // the canvas class map of CanvasParams::cls (init time, geometry only)
 void launch_canvas_class(const CanvasParams& P, std::uint8_t* cls, cudaStream_t s);
@@ -331,10 +344,15 @@ struct PairGeometry {
 };
 // Warp masks of every view (launch_warp_mask), view footprints, and for each
 // (view, partner) pair its overlap bounds and chamfer blend weights.
+// first_rgba: the first frames expanded to RGBA with their masks as alpha
+// (per view, nullptr = unmasked): the pairs' bounds and weights then follow
+// those frames' masked warps, as rebuild_pair_geometry warps first_frames
+// (pipeline.cpp:181-205); the view footprints stay the geometry's.
 // lift_*: the cylindrical lift tables (projection 1), else unused.
 cudaError_t gpu_init_geometry(const Geometry& geom, const double* lift_s, const double* lift_c,
                               const double* lift_h, int n_lift_x, int n_lift_y, int n_views,
                               const std::vector<std::pair<int, int>>& pairs,
-                              std::vector<ViewFootprint>& views, std::vector<PairGeometry>& out);
+                              std::vector<ViewFootprint>& views, std::vector<PairGeometry>& out,
+                              const std::vector<const uchar4*>* first_rgba = nullptr);
 
 }  // namespace stitch_b200_dev

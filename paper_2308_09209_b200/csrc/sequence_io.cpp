@@ -94,11 +94,13 @@ std::vector<fs::path> list_images(const std::string& dir, int* rc) {
   return files;
 }
 
-// read_image (image_io.cpp:167-172) of one unmasked camera frame straight
-// into rgb (capacity bytes): the PPM raster is read in place, a PNG decoded
-// then copied.  A PNG with transparent pixels is a masked frame, which the
-// device path does not take (its inputs are unmasked).
-int read_frame(const fs::path& path, uint8_t* rgb, size_t capacity, int* w, int* h) {
+// read_image (image_io.cpp:167-172) of one camera frame straight into rgb
+// (capacity bytes): the PPM raster is read in place, a PNG decoded then
+// copied.  A PNG with transparent pixels is a masked frame (image_io.cpp:
+// 120-127): its mask goes to `mask` (capacity / 3 bytes) and *masked is set.
+int read_frame(const fs::path& path, uint8_t* rgb, size_t capacity, uint8_t* mask, bool* masked,
+               int* w, int* h) {
+  *masked = false;
   const std::string ext = path.extension().string();
   if (ext == ".ppm") return stitch_b200_read_ppm(path.string().c_str(), rgb, capacity, w, h);
   if (ext != ".png") return io_fail(path.string(), "unsupported image extension");
@@ -107,12 +109,13 @@ int read_frame(const fs::path& path, uint8_t* rgb, size_t capacity, int* w, int*
   if (rc) return rc;
   *w = img.width;
   *h = img.height;
-  if (!img.mask.empty())
-    return stitch_b200_set_error(STITCH_B200_InputMismatch,
-                                 (path.string() + ": masked (transparent) input frame").c_str());
   if (img.rgb.size() > capacity)
     return stitch_b200_set_error(STITCH_B200_InputMismatch, "frame size differs from the view size");
   std::memcpy(rgb, img.rgb.data(), img.rgb.size());
+  if (!img.mask.empty()) {
+    std::memcpy(mask, img.mask.data(), img.mask.size());
+    *masked = true;
+  }
   return STITCH_B200_OK;
 }
 
@@ -240,6 +243,8 @@ int stitch_b200_run_files(stitch_b200_ctx* ctx, const char* const* view_dirs,
   constexpr int kRing = 8, kInFlight = 4, kWriters = 4;
   struct Slot {
     std::vector<uint8_t*> in;
+    std::vector<uint8_t*> in_mask;   // the views' input masks (transparent PNG sources)
+    std::vector<char> masked;        // per view: this frame's view carries a mask
     uint8_t* rgb = nullptr;
     uint8_t* mask = nullptr;
   };
@@ -247,16 +252,22 @@ int stitch_b200_run_files(stitch_b200_ctx* ctx, const char* const* view_dirs,
   auto free_ring = [&]() {
     for (auto& s : ring) {
       for (auto* p : s.in) stitch_b200_host_free(p);
+      for (auto* p : s.in_mask) stitch_b200_host_free(p);
       stitch_b200_host_free(s.rgb);
       stitch_b200_host_free(s.mask);
     }
   };
   for (auto& s : ring) {
-    for (int v = 0; v < nv; ++v) s.in.push_back(static_cast<uint8_t*>(stitch_b200_host_alloc(vbytes[v])));
+    for (int v = 0; v < nv; ++v) {
+      s.in.push_back(static_cast<uint8_t*>(stitch_b200_host_alloc(vbytes[v])));
+      s.in_mask.push_back(static_cast<uint8_t*>(stitch_b200_host_alloc(vbytes[v] / 3)));
+    }
+    s.masked.assign(static_cast<size_t>(nv), 0);
     s.rgb = static_cast<uint8_t*>(stitch_b200_host_alloc(pano_bytes * 3));
     s.mask = static_cast<uint8_t*>(stitch_b200_host_alloc(pano_bytes));
     bool ok = s.rgb && s.mask;
     for (auto* p : s.in) ok = ok && p;
+    for (auto* p : s.in_mask) ok = ok && p;
     if (!ok) {
       free_ring();
       return stitch_b200_set_error(STITCH_B200_CudaError, "pinned allocation failed");
@@ -296,7 +307,10 @@ int stitch_b200_run_files(stitch_b200_ctx* ctx, const char* const* view_dirs,
         }
         const auto t0 = now();
         int w = 0, h = 0;
-        const int r = read_frame(lists[v][t], ring[t % kRing].in[v], vbytes[v], &w, &h);
+        bool vm = false;
+        const int r = read_frame(lists[v][t], ring[t % kRing].in[v], vbytes[v],
+                                 ring[t % kRing].in_mask[v], &vm, &w, &h);
+        ring[t % kRing].masked[v] = vm ? 1 : 0;
         if (r == STITCH_B200_OK && static_cast<size_t>(w) * h * 3 != vbytes[v]) {
           stitch_b200_set_error(STITCH_B200_InputMismatch, "frame size differs from the view size");
           set_err(STITCH_B200_InputMismatch);
@@ -382,7 +396,16 @@ int stitch_b200_run_files(stitch_b200_ctx* ctx, const char* const* view_dirs,
     }
     Slot& s = ring[t % kRing];
     long long tk = -1;
-    int r = stitch_b200_submit(ctx, s.in.data(), s.rgb, s.mask, &tk);
+    // masked PNG views go with their masks (stitch_b200_submit_masked)
+    std::vector<const uint8_t*> mptr(static_cast<size_t>(nv), nullptr);
+    bool any_mask = false;
+    for (int v = 0; v < nv; ++v)
+      if (s.masked[v]) {
+        mptr[v] = s.in_mask[v];
+        any_mask = true;
+      }
+    int r = any_mask ? stitch_b200_submit_masked(ctx, s.in.data(), mptr.data(), s.rgb, s.mask, &tk)
+                     : stitch_b200_submit(ctx, s.in.data(), s.rgb, s.mask, &tk);
     if (r) {
       set_err(r);
       break;

@@ -358,19 +358,21 @@ class ProcessResult:  # pipeline.hpp:65-68
 
 def initialize(config: StitchConfig, first_frames: Sequence[Frame]) -> PipelineState:
     """pipeline.hpp:73-74; with refine.enabled (the default, as in the
-    reference) the first frames feed the feature refinement."""
+    reference) the first frames feed the feature refinement, and masked first
+    frames (Frame.mask) the pair geometry."""
     if len(first_frames) != len(config.views):
         raise StitchError(ErrorCode.ConfigurationError + 1,
                           "frame count does not match configured views")
-    for f in first_frames:
-        if f.mask is not None and not np.asarray(f.mask).all():
-            raise StitchError(ErrorCode.InputMismatch + 1,
-                              "masked input frames (frame.cpp:95-104) are not supported by "
-                              "the B200 path")
     sizes = [(f.width, f.height) for f in first_frames]
     c = _config_to_c(config, sizes)
     h = C.c_void_p()
-    if config.refine.enabled:
+    if any(f.mask is not None for f in first_frames):
+        # masked first frames decide the pair geometry (pipeline.cpp:181-205)
+        arrs, ptrs = _frame_ptrs(first_frames, len(config.views))
+        keep, mptrs = _mask_ptrs(first_frames)
+        check(_lib().stitch_b200_initialize_frames_masked(C.byref(c), ptrs, mptrs, config.device,
+                                                          C.byref(h)))
+    elif config.refine.enabled:
         arrs, ptrs = _frame_ptrs(first_frames, len(config.views))
         check(_lib().stitch_b200_initialize_frames(C.byref(c), ptrs, config.device, C.byref(h)))
     else:
@@ -484,9 +486,8 @@ def _mask_ptrs(frames: Sequence[Frame]):
 
 
 def check_frames(state: PipelineState, frames: Sequence[Frame]) -> None:
-    """stitch_b200_check_frames: frame count, per-view size as initialized, and
-    no masked pixel (the reference's masked sampler, frame.cpp:95-104, is not
-    on the B200 path) -- InputMismatch instead of a silent misread."""
+    """stitch_b200_check_frames: frame count and per-view size as initialized
+    -- InputMismatch instead of a silent misread."""
     n = len(frames)
     ws = (C.c_int * max(1, n))(*[f.width for f in frames])
     hs = (C.c_int * max(1, n))(*[f.height for f in frames])
@@ -504,8 +505,15 @@ def process_frame(state: PipelineState, frames: Sequence[Frame]) -> ProcessResul
     rgb = np.empty((h, w, 3), dtype=np.uint8)
     mask = np.empty((h, w), dtype=np.uint8)
     rep = _abi.Report()
-    check(_lib().stitch_b200_process(state.handle, ptrs, rgb.ctypes.data_as(C.c_void_p),
-                                     mask.ctypes.data_as(C.c_void_p), C.byref(rep)))
+    if any(f.mask is not None for f in frames):
+        # masked inputs (Frame::mask): the sampler skips masked taps (frame.cpp:95-104)
+        keep, mptrs = _mask_ptrs(frames)
+        check(_lib().stitch_b200_process_masked(state.handle, ptrs, mptrs,
+                                                rgb.ctypes.data_as(C.c_void_p),
+                                                mask.ctypes.data_as(C.c_void_p), C.byref(rep)))
+    else:
+        check(_lib().stitch_b200_process(state.handle, ptrs, rgb.ctypes.data_as(C.c_void_p),
+                                         mask.ctypes.data_as(C.c_void_p), C.byref(rep)))
     state.frame_counter += 1
     return ProcessResult(Frame(rgb, mask), _report_from_c(rep))
 

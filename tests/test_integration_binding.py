@@ -33,11 +33,16 @@ def test_binding_links_the_in_tree_library():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("views,w,h,frames,refine", [(2, 640, 480, 12, 1), (3, 320, 240, 6, 1),
-                                                     (2, 320, 240, 5, 0)])
-def test_binding_reproduces_reference_process_frame(views, w, h, frames, refine):
+@pytest.mark.parametrize("views,w,h,frames,refine,masked", [(2, 640, 480, 12, 1, 0),
+                                                            (3, 320, 240, 6, 1, 0),
+                                                            (2, 320, 240, 5, 0, 0),
+                                                            (2, 640, 480, 6, 1, 1),
+                                                            (3, 320, 240, 4, 0, 1)])
+def test_binding_reproduces_reference_process_frame(views, w, h, frames, refine, masked):
+    """masked: every frame (the first ones included) carries a Frame::mask."""
     _need_demo()
-    r = subprocess.run([DEMO, str(views), str(w), str(h), str(frames), str(refine)],
+    r = subprocess.run([DEMO, str(views), str(w), str(h), str(frames), str(refine), "0",
+                        str(masked)],
                        capture_output=True, text=True, timeout=900)
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
     assert lines, r.stdout[-2000:] + r.stderr[-2000:]
