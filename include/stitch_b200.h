@@ -199,6 +199,10 @@ int stitch_b200_initialize_frames_masked(const stitch_b200_config* cfg,
  * counter are carried over.  The pair set must not change. */
 int stitch_b200_rerefine(stitch_b200_ctx* ctx, const stitch_b200_config* cfg,
                          const uint8_t* const* frames);
+/* rerefine with the current frames' masks (NULL, or per view NULL / W*H
+ * bytes): run_sequence's re-initialize on masked frames. */
+int stitch_b200_rerefine_masked(stitch_b200_ctx* ctx, const stitch_b200_config* cfg,
+                                const uint8_t* const* frames, const uint8_t* const* masks);
 
 /* 1 when pair k's refinement fell back to the unrefined map
  * (PairState::refine_warning: too few keypoints / matches, no consensus). */

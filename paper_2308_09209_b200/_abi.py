@@ -92,6 +92,8 @@ SYMBOLS = [
                                                        C.POINTER(C.c_void_p)]),
     ("stitch_b200_initialize_frames", C.c_int, [C.POINTER(Config), C.c_void_p, C.c_int,
                                                 C.POINTER(C.c_void_p)]),
+    ("stitch_b200_rerefine_masked", C.c_int, [C.c_void_p, C.POINTER(Config),
+                                              C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
     ("stitch_b200_refine_warning", C.c_int, [C.c_void_p, C.c_int]),
     ("stitch_b200_rerefine", C.c_int, [C.c_void_p, C.POINTER(Config), C.c_void_p]),
     ("stitch_b200_process_device_async", C.c_int, [C.c_void_p, C.c_void_p]),

@@ -828,9 +828,6 @@ int build_context(const stitch_b200_init* in, int device,
     }
     {
       CanvasParams& P = S.cparams;
-      // device address of this slot's FrameTable::masked (no dereference)
-      P.masked = reinterpret_cast<const int*>(reinterpret_cast<const char*>(S.dg) +
-                                              offsetof(Geometry, in) + offsetof(FrameTable, masked));
       P.cw = g.canvas_w;
       P.ch = g.canvas_h;
       P.ref = g.reference;
@@ -872,6 +869,9 @@ int build_context(const stitch_b200_init* in, int device,
     }
     CUDA_TRY(ctx->alloc(&S.dg, 1));
     CUDA_TRY(cudaMemcpy(S.dg, &g, sizeof(Geometry), cudaMemcpyHostToDevice));
+    // device address of this slot's FrameTable::masked (no dereference)
+    S.cparams.masked = reinterpret_cast<const int*>(
+        reinterpret_cast<const char*>(S.dg) + offsetof(Geometry, in) + offsetof(FrameTable, masked));
     CUDA_TRY(ctx->alloc(&S.dst, 1));
     {
       // identity matrices for every view; the temporal state lives in the
@@ -1615,17 +1615,22 @@ int stitch_b200_initialize_frames_masked(const stitch_b200_config* cfg,
 
 static int carry_into(stitch_b200_ctx* h, std::unique_ptr<Ctx>& fresh);
 
-int stitch_b200_rerefine(stitch_b200_ctx* h, const stitch_b200_config* cfg,
-                         const uint8_t* const* frames) {
+int stitch_b200_rerefine_masked(stitch_b200_ctx* h, const stitch_b200_config* cfg,
+                                const uint8_t* const* frames, const uint8_t* const* masks) {
   if (!frames) return fail(STITCH_B200_ConfigurationError, "frames must not be NULL");
   stitch_b200_ctx* fresh = nullptr;
-  int rc = initialize_impl(cfg, frames, h->c->device, &fresh);
+  int rc = initialize_impl(cfg, frames, h->c->device, &fresh, masks);
   if (rc) return rc;
   std::unique_ptr<stitch_b200_ctx> guard(fresh);
   if (fresh->c->hg.n_pairs != h->c->hg.n_pairs)
     return fail(STITCH_B200_ConfigurationError, "re-refinement must keep the pair set");
   std::unique_ptr<Ctx> f = std::move(fresh->c);
   return carry_into(h, f);
+}
+
+int stitch_b200_rerefine(stitch_b200_ctx* h, const stitch_b200_config* cfg,
+                         const uint8_t* const* frames) {
+  return stitch_b200_rerefine_masked(h, cfg, frames, nullptr);
 }
 
 int stitch_b200_refine_warning(const stitch_b200_ctx* h, int k) {

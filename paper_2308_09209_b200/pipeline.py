@@ -299,7 +299,11 @@ class PipelineState:
         initialize() on `frames` with the temporal state carried over."""
         c = _config_to_c(config, [(f.width, f.height) for f in frames])
         arrs, ptrs = _frame_ptrs(frames, len(config.views))
-        check(_lib().stitch_b200_rerefine(self._h, C.byref(c), ptrs))
+        if any(f.mask is not None for f in frames):
+            keep, mptrs = _mask_ptrs(frames)
+            check(_lib().stitch_b200_rerefine_masked(self._h, C.byref(c), ptrs, mptrs))
+        else:
+            check(_lib().stitch_b200_rerefine(self._h, C.byref(c), ptrs))
         self._refresh()
         for k, p in enumerate(self.pairs):
             p.refine_warning = bool(_lib().stitch_b200_refine_warning(self._h, k))
