@@ -397,7 +397,8 @@ typedef struct {
 /* run_sequence (pipeline.hpp:90-92, pipeline.cpp:364-412) with file sources
  * and sink: view_dirs[v] holds view v's numbered image sequence
  * (list_sequence, image_io.cpp:181-192: the .ppm / .png files sorted by name;
- * inputs must be unmasked, a transparent PNG pixel is an InputMismatch);
+ * a PNG with transparent pixels is a masked frame and runs with its mask,
+ * stitch_b200_submit_masked);
  * frame t of every view is stitched in order and the panorama written to
  * out_dir/<stem>_%06d<ext> (ext ".ppm" (NULL) or ".png" with the mask as
  * alpha; out_dir NULL: not written).  One reader thread per
