@@ -703,7 +703,26 @@ def spawn_ranks(n):
                    LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:],
                                       env=env, stdout=None if r == 0 else subprocess.DEVNULL))
-    rcs = [p.wait() for p in procs]
+    # a rank that fails would leave the others waiting at the barrier: stop
+    # them as soon as one exits non-zero
+    rcs = [None] * n
+    while any(rc is None for rc in rcs):
+        for i, p in enumerate(procs):
+            if rcs[i] is None:
+                rcs[i] = p.poll()
+        if any(rc not in (None, 0) for rc in rcs):
+            for i, p in enumerate(procs):
+                if rcs[i] is None:
+                    p.terminate()
+            for i, p in enumerate(procs):
+                if rcs[i] is None:
+                    try:
+                        rcs[i] = p.wait(timeout=30)
+                    except subprocess.TimeoutExpired:
+                        p.kill()
+                        rcs[i] = p.wait()
+            break
+        time.sleep(0.2)
     return max(rcs, key=abs)
 
 
@@ -740,8 +759,11 @@ def main():
     if world > 1:
         import torch
 
+        import datetime
+
         # gloo: only the barrier and the timing reductions cross ranks
-        torch.distributed.init_process_group("gloo", rank=rank, world_size=world)
+        torch.distributed.init_process_group("gloo", rank=rank, world_size=world,
+                                             timeout=datetime.timedelta(minutes=15))
     res = run_b200(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(res), flush=True)
