@@ -9,6 +9,7 @@ MAX_PAIRS = 16
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libstitch_b200.so")
+SYNTH_LIB_PATH = os.path.join(_HERE, "libstitch_synth.so")
 
 
 class Camera(C.Structure):
@@ -173,6 +174,13 @@ SYMBOLS = [
     ("stitch_b200_debug_prebalance", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     ("stitch_b200_debug_warp_view", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
                                               C.c_void_p]),
+
+]
+
+OP_KIND_NAMES = ["expand_rgba", "crop_warp", "pair_color", "pair_solve", "flow_prepare", "pyr_down", "hs_linearize",
+                 "hs_sweeps", "canvas_balance", "balance", "tone", "event"]
+
+SYNTH_SYMBOLS = [
     ("stitch_b200_synth_defaults", None, [C.POINTER(SynthSpec)]),
     ("stitch_b200_synth_create", C.c_int, [C.POINTER(SynthSpec), C.POINTER(C.c_void_p)]),
     ("stitch_b200_synth_destroy", None, [C.c_void_p]),
@@ -181,10 +189,8 @@ SYMBOLS = [
     ("stitch_b200_synth_render", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int]),
 ]
 
-OP_KIND_NAMES = ["expand_rgba", "crop_warp", "pair_color", "pair_solve", "flow_prepare", "pyr_down", "hs_linearize",
-                 "hs_sweeps", "canvas_balance", "balance", "tone", "event"]
-
 _lib = None
+_synth = None
 
 
 def load(path: str = LIB_PATH) -> C.CDLL:
@@ -202,4 +208,21 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         fn.restype = restype
         fn.argtypes = argtypes
     _lib = lib
+    return lib
+
+
+def load_synth(path: str = SYNTH_LIB_PATH) -> C.CDLL:
+    """Load libstitch_synth.so (the synthetic scene generator: test and bench
+    inputs, include/stitch_synth.h) -- without the B200 product library."""
+    global _synth
+    if _synth is not None:
+        return _synth
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: build it with `make -C paper_2308_09209_b200`")
+    lib = C.CDLL(path)
+    for name, restype, argtypes in SYNTH_SYMBOLS:
+        fn = getattr(lib, name)
+        fn.restype = restype
+        fn.argtypes = argtypes
+    _synth = lib
     return lib

@@ -1270,35 +1270,7 @@ const char* stitch_b200_last_error(void) { return g_last_error.c_str(); }
 
 const char* stitch_b200_version(void) { return "stitch_b200 0.1 (sm_100a)"; }
 
-void stitch_b200_config_defaults(stitch_b200_config* c) {
-  std::memset(c, 0, sizeof(*c));
-  c->n_views = 2;
-  c->reference = 0;
-  c->lambda = 0.05;
-  c->gamma_dark = 1.5;
-  c->gamma_bright = 1.5;
-  c->target_black = 0;
-  c->target_white = 255;
-  c->flow_levels = 4;
-  c->flow_iterations = 50;
-  c->smoothness = 15.0;
-  c->window_capacity = 3;
-  c->fuse_weighting = 0;
-  c->topology = 0;
-  c->refine_enabled = 1;  // RefineOptions::enabled (pipeline.hpp:24)
-  c->projection = 0;
-  c->cyl_focal = 0.0;
-  c->refine_margin = 0.15;  // RefineOptions defaults (pipeline.hpp:23-31)
-  c->ransac_iters = 500;
-  c->inlier_px = 2.0;
-  c->detect_threshold = 2e-4;
-  c->match_ratio = 0.8;
-  c->seed = 0;
-  for (int v = 0; v < STITCH_B200_MAX_VIEWS; ++v) {
-    c->cams[v].fx = c->cams[v].fy = 1.0;
-    c->cams[v].rotation[0] = c->cams[v].rotation[4] = c->cams[v].rotation[8] = 1.0;
-  }
-}
+void stitch_b200_config_defaults(stitch_b200_config* c) { hg_ns::config_defaults(c); }
 
 int stitch_b200_create(const stitch_b200_init* init, int device, stitch_b200_ctx** out) {
   *out = nullptr;

@@ -8,11 +8,46 @@
 
 #include <array>
 #include <cstdint>
+#include <cstring>
 #include <vector>
 
 #include "stitch_b200.h"
 
 namespace stitch_b200_host {
+
+// StitchConfig defaults of the reference (pipeline.hpp:23-44,
+// color_balance.hpp:19-25, flow.hpp:29-34): stitch_b200_config_defaults and
+// the synthetic scenes' configs (libstitch_synth.so) share this one copy.
+inline void config_defaults(stitch_b200_config* c) {
+  std::memset(c, 0, sizeof(*c));
+  c->n_views = 2;
+  c->reference = 0;
+  c->lambda = 0.05;
+  c->gamma_dark = 1.5;
+  c->gamma_bright = 1.5;
+  c->target_black = 0;
+  c->target_white = 255;
+  c->flow_levels = 4;
+  c->flow_iterations = 50;
+  c->smoothness = 15.0;
+  c->window_capacity = 3;
+  c->fuse_weighting = 0;
+  c->topology = 0;
+  c->refine_enabled = 1;  // RefineOptions::enabled (pipeline.hpp:24)
+  c->projection = 0;
+  c->cyl_focal = 0.0;
+  c->refine_margin = 0.15;  // RefineOptions defaults (pipeline.hpp:23-31)
+  c->ransac_iters = 500;
+  c->inlier_px = 2.0;
+  c->detect_threshold = 2e-4;
+  c->match_ratio = 0.8;
+  c->seed = 0;
+  for (int v = 0; v < STITCH_B200_MAX_VIEWS; ++v) {
+    c->cams[v].fx = c->cams[v].fy = 1.0;
+    c->cams[v].rotation[0] = c->cams[v].rotation[4] = c->cams[v].rotation[8] = 1.0;
+  }
+}
+
 
 using Mat3 = std::array<double, 9>;  // row-major
 

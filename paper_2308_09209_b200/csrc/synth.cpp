@@ -19,7 +19,7 @@
 #include <vector>
 
 #include "host_geometry.hpp"
-#include "stitch_b200.h"
+#include "stitch_synth.h"
 
 namespace {
 
@@ -294,7 +294,7 @@ int stitch_b200_synth_reference(const stitch_b200_synth* s) { return s->referenc
 
 // SynthScene::config, synth.cpp:149-168
 int stitch_b200_synth_config(const stitch_b200_synth* s, stitch_b200_config* cfg) {
-  stitch_b200_config_defaults(cfg);
+  stitch_b200_host::config_defaults(cfg);
   cfg->n_views = s->spec.views;
   cfg->reference = s->reference;
   if (s->rig == 3) {

@@ -56,6 +56,17 @@ def _lib():
     return _abi.load()
 
 
+def _synth_lib():
+    return _abi.load_synth()
+
+
+def _check_synth(status: int) -> None:
+    """status of a synthetic-scene call (libstitch_synth.so: codes only)."""
+    if status != 0:
+        raise StitchError(status, f"synthetic scene: status {status} "
+                                  f"({ErrorCode(status - 1).name if 1 <= status <= 17 else '?'})")
+
+
 def check(status: int) -> None:
     if status != 0:
         msg = _lib().stitch_b200_last_error().decode(errors="replace")
@@ -723,7 +734,7 @@ class SynthSpec:
 
     def to_c(self) -> _abi.SynthSpec:
         s = _abi.SynthSpec()
-        _lib().stitch_b200_synth_defaults(C.byref(s))
+        _synth_lib().stitch_b200_synth_defaults(C.byref(s))
         s.seed = self.seed
         s.views = self.views
         s.frames = self.frames
@@ -759,14 +770,14 @@ class SynthScene:
         self.spec = spec
         self._c = spec.to_c()
         self._h = C.c_void_p()
-        check(_lib().stitch_b200_synth_create(C.byref(self._c), C.byref(self._h)))
+        _check_synth(_synth_lib().stitch_b200_synth_create(C.byref(self._c), C.byref(self._h)))
 
     def reference_view(self) -> int:
-        return _lib().stitch_b200_synth_reference(self._h)
+        return _synth_lib().stitch_b200_synth_reference(self._h)
 
     def config_c(self) -> _abi.Config:
         c = _abi.Config()
-        check(_lib().stitch_b200_synth_config(self._h, C.byref(c)))
+        _check_synth(_synth_lib().stitch_b200_synth_config(self._h, C.byref(c)))
         return c
 
     def config(self) -> StitchConfig:
@@ -781,7 +792,7 @@ class SynthScene:
 
     def render_view(self, view: int, frame: int, threads: int = 0) -> Frame:
         out = np.empty((self.spec.height, self.spec.width, 3), dtype=np.uint8)
-        check(_lib().stitch_b200_synth_render(self._h, view, frame,
+        _check_synth(_synth_lib().stitch_b200_synth_render(self._h, view, frame,
                                               out.ctypes.data_as(C.c_void_p), threads))
         return Frame(out, None)
 
@@ -791,7 +802,7 @@ class SynthScene:
 
     def close(self):
         if self._h:
-            _lib().stitch_b200_synth_destroy(self._h)
+            _synth_lib().stitch_b200_synth_destroy(self._h)
             self._h = None
 
     def __del__(self):

@@ -11,6 +11,7 @@
 
 #include "../../oracle/stitch_oracle.h"
 #include "stitch_b200.hpp"
+#include "stitch_synth.h"
 
 static int g_failures = 0, g_checks = 0;
 #define CHECK(cond)                                                      \

@@ -31,6 +31,24 @@ def test_library_loads_and_exports_every_declared_symbol():
     assert sorted(n for n, _, _ in _abi.SYMBOLS) == names
 
 
+SYNTH_HEADER = os.path.join(ROOT, "include", "stitch_synth.h")
+
+
+def test_synth_library_is_separate():
+    """the input generator (stitch_synth.h) lives in libstitch_synth.so, which
+    exports exactly its C API; the product library exports none of it."""
+    src = re.sub(r"/\*.*?\*/", "", open(SYNTH_HEADER).read(), flags=re.S)
+    names = sorted(set(re.findall(r"\b(stitch_b200_synth_\w+)\s*\(", src)))
+    assert names and sorted(n for n, _, _ in _abi.SYNTH_SYMBOLS) == names
+    synth = subprocess.run(["nm", "-D", "--defined-only", _abi.SYNTH_LIB_PATH],
+                           capture_output=True, text=True, check=True).stdout
+    assert sorted(set(re.findall(r" T (\w+)", synth))) == names
+    prod = subprocess.run(["nm", "-D", "--defined-only", _abi.LIB_PATH], capture_output=True,
+                          text=True, check=True).stdout
+    assert "stitch_b200_synth_" not in prod
+    _abi.load_synth()
+
+
 def test_exported_dynamic_symbols():
     out = subprocess.run(["nm", "-D", "--defined-only", _abi.LIB_PATH], capture_output=True,
                          text=True, check=True).stdout
@@ -43,7 +61,7 @@ def test_struct_layouts_match_header():
     prog = r"""
 #include <stdio.h>
 #include <stddef.h>
-#include "stitch_b200.h"
+#include "stitch_synth.h"
 int main(void){
  printf("%zu %zu %zu %zu %zu %zu %zu\n", sizeof(stitch_b200_camera), sizeof(stitch_b200_config),
    sizeof(stitch_b200_pair), sizeof(stitch_b200_init), sizeof(stitch_b200_report),
