@@ -965,6 +965,9 @@ int build_context(const stitch_b200_init* in, int device,
     }
   }
   ctx->launches = launches;
+  // the zero fills of ctx->alloc run on the legacy stream, which the context's
+  // non-blocking streams do not wait for: settle them before the first frame
+  CUDA_TRY(cudaDeviceSynchronize());
   out = std::move(ctx);
   return STITCH_B200_OK;
 }
@@ -1183,7 +1186,14 @@ int submit_host(Ctx* ctx, const std::uint8_t* const* frames, std::uint8_t* pano_
     if (!masks[v]) continue;
     any_mask = true;
     const size_t mb = ctx->frame_bytes[v] / 3;
-    if (!ctx->d_mask[slot][v]) CUDA_TRY(ctx->alloc(&ctx->d_mask[slot][v], mb));
+    if (!ctx->d_mask[slot][v]) {
+      // no zero fill: a cudaMemset on the legacy stream would not be ordered
+      // before the copy below on the (non-blocking) upload stream
+      void* q = nullptr;
+      CUDA_TRY(cudaMalloc(&q, std::max<size_t>(mb, 16)));
+      ctx->allocs.push_back(q);
+      ctx->d_mask[slot][v] = static_cast<std::uint8_t*>(q);
+    }
     const std::uint8_t* src = masks[v];
     if (!is_pinned(src)) {
       if (!ctx->h_stage_min[slot][v])
