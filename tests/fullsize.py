@@ -78,16 +78,22 @@ def frame_diffs(state, ost, frames):
     }
 
 
-def run_config(key: str, frames: int | None = None, seed: int = 1):
+def run_config(key: str, frames: int | None = None, seed: int = 1, refine: bool | None = None):
     """Initialise both paths on the bench's inputs for `key` and compare
-    `frames` frames; returns (geometry_equal, per-frame diff dicts, info)."""
+    `frames` frames; returns (geometry_equal, per-frame diff dicts, info).
+    refine (default: as bench.py, i.e. on for the planar rigs, off for the
+    360-degree ring) runs the feature refinement at initialize on both paths."""
     wl = bench.WORKLOADS[key]
     sc = bench.build_scene(wl, seed)
     n = frames or FRAMES[key]
     threads = host_threads()
+    if refine is None:
+        refine = wl.get("rig", "auto") != "ring"
     t0 = time.perf_counter()
-    state = pb.initialize(product_config(sc), frames_at(sc, 0))
-    ost = O.OracleState(oracle_config(sc, threads=threads))
+    first = frames_at(sc, 0)
+    state = pb.initialize(product_config(sc, refine=refine, seed=sc.spec.seed), first)
+    ost = O.OracleState(oracle_config(sc, threads=threads, refine=refine, seed=sc.spec.seed),
+                        first_frames=[f.data for f in first] if refine else None)
     geom = state.canvas == ost.canvas and len(state.pairs) == ost.n_pairs()
     for v in range(sc.spec.views):
         _, inv = ost.maps(v)
@@ -101,7 +107,7 @@ def run_config(key: str, frames: int | None = None, seed: int = 1):
         for t in range(n):
             per_frame.append(frame_diffs(state, ost, frames_at(sc, t)))
     finally:
-        info = {"config": key, "workload": wl["desc"], "cameras": wl["views"],
+        info = {"config": key, "workload": wl["desc"], "cameras": wl["views"], "refine": refine,
                 "camera_size": [wl["width"], wl["height"]], "canvas": list(state.canvas[:2]),
                 "pairs": len(state.pairs), "frames": n, "oracle_threads": threads,
                 "seconds": round(time.perf_counter() - t0, 1)}
