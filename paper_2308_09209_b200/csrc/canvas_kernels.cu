@@ -68,9 +68,11 @@ __global__ void __launch_bounds__(256) k_expand_one(const std::uint8_t* __restri
 // (pipeline.cpp:310-311) evaluated directly on the bounds.
 // grid: (ceil(max_w/64), ceil(max_h/4), 2*n_pairs), block (64, 4)
 // ---------------------------------------------------------------------------
-template <bool CYL>
-__device__ __forceinline__ uchar4 warp_cv(const CanvasView& v, Lift L, bool masked) {
-  if (masked) {  // a masked frame: masked taps drop out (frame.cpp:95-104)
+// MASKED (a compile-time choice, dispatched once per kernel from the frame's
+// flag): a masked frame's masked taps drop out (frame.cpp:95-104)
+template <bool CYL, bool MASKED = false>
+__device__ __forceinline__ uchar4 warp_cv(const CanvasView& v, Lift L) {
+  if (MASKED) {
     ViewDesc d;
     d.width = v.w;
     d.height = v.h;
@@ -105,11 +107,16 @@ __global__ void __launch_bounds__(256) k_crop_warp(const __grid_constant__ Canva
   const int dy = blockIdx.y * 4 + threadIdx.y;
   if (dx >= p.w || dy >= p.h) return;
   const int view = side ? p.partner : p.view;
-  const bool masked = *P.masked;
-  p.crop_raw[side][dy * p.w + dx] =
-      P.projection == 1
-          ? warp_cv<true>(P.views[view], canvas_lift<true>(P, p.x0 + dx, p.y0 + dy), masked)
-          : warp_cv<false>(P.views[view], canvas_lift<false>(P, p.x0 + dx, p.y0 + dy), masked);
+  uchar4 o;
+  if (*P.masked)
+    o = P.projection == 1
+            ? warp_cv<true, true>(P.views[view], canvas_lift<true>(P, p.x0 + dx, p.y0 + dy))
+            : warp_cv<false, true>(P.views[view], canvas_lift<false>(P, p.x0 + dx, p.y0 + dy));
+  else
+    o = P.projection == 1
+            ? warp_cv<true>(P.views[view], canvas_lift<true>(P, p.x0 + dx, p.y0 + dy))
+            : warp_cv<false>(P.views[view], canvas_lift<false>(P, p.x0 + dx, p.y0 + dy));
+  p.crop_raw[side][dy * p.w + dx] = o;
 }
 
 // Staged variant (planar canvas; STITCH_B200_WARP_STAGE=1): a CTA owns a
@@ -403,10 +410,9 @@ __device__ __forceinline__ bool in_rect(const CanvasPair& p, int x, int y) {
 
 // One canvas pixel: the warped reference view, then the compose_panorama
 // fold over pairs (pipeline.cpp:326-333, flow.cpp:324-357).
-template <bool CYL>
+template <bool CYL, bool MASKED>
 __device__ __forceinline__ uchar4 canvas_pixel(const CanvasParams& P,
-                                               const double (*mview)[9], int x, int y,
-                                               bool masked) {
+                                               const double (*mview)[9], int x, int y) {
   const int ref = P.ref;
   const CanvasView& vr = P.views[ref];
   const int np = P.np;
@@ -426,7 +432,7 @@ __device__ __forceinline__ uchar4 canvas_pixel(const CanvasParams& P,
       const CanvasPair& p = P.pairs[kc];
       pv = p.crop_raw[1][(y - p.y0) * p.w + (x - p.x0)];
     } else {
-      pv = warp_cv<CYL>(vr, L, masked);
+      pv = warp_cv<CYL, MASKED>(vr, L);
     }
   }
   for (int k = 0; k < np; ++k) {
@@ -435,7 +441,7 @@ __device__ __forceinline__ uchar4 canvas_pixel(const CanvasParams& P,
     if (!may_cover(vv, x, y)) continue;
     const int dx = x - p.x0, dy = y - p.y0;
     const bool inb = dx >= 0 && dy >= 0 && dx < p.w && dy < p.h;
-    const uchar4 q = inb ? p.crop_raw[0][dy * p.w + dx] : warp_cv<CYL>(vv, L, masked);
+    const uchar4 q = inb ? p.crop_raw[0][dy * p.w + dx] : warp_cv<CYL, MASKED>(vv, L);
     if (!q.w) continue;
     if (pv.w) {
       if (inb) {
@@ -449,27 +455,13 @@ __device__ __forceinline__ uchar4 canvas_pixel(const CanvasParams& P,
   return pv;
 }
 
-constexpr int kCanvasCtasPerSm = 4;  // resident CTAs per SM (register budget; 5 spills)
-
-// Every canvas pixel once (64 x 4 tiles, grid-stride), per-CTA histogram
-// flushed to the frame histogram; the last CTA builds the balance LUT.
-template <bool CYL>
-__global__ void __launch_bounds__(256, kCanvasCtasPerSm) k_canvas(const __grid_constant__ CanvasParams P,
-                                                   const Geometry* __restrict__ g,
-                                                   DevState* __restrict__ st,
-                                                   uchar4* __restrict__ pano) {
-  __shared__ unsigned int hist[3][256];
-  __shared__ double mview[kMaxViews][9];
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-    hist[0][i] = 0;
-    hist[1][i] = 0;
-    hist[2][i] = 0;
-  }
-  for (int i = threadIdx.x; i < kMaxViews * 9; i += blockDim.x) mview[i / 9][i % 9] = st->mview[i / 9][i % 9];
-  __syncthreads();
+// Every canvas pixel of this CTA's grid-stride tiles (64 x 4), into pano and
+// the CTA's histogram.
+template <bool CYL, bool MASKED>
+__device__ __forceinline__ void canvas_tiles(const CanvasParams& P, const double (*mview)[9],
+                                             uchar4* __restrict__ pano,
+                                             unsigned int (*hist)[256]) {
   const int cw = P.cw, ch = P.ch;
-  // a masked frame's coverage is not the geometry's: every pixel runs the fold
-  const bool masked = *P.masked;
   const int tiles_x = (cw + 63) / 64;
   const int ntiles = tiles_x * ((ch + 3) / 4);
   // tile -> (column, row) kept incrementally: the grid stride advances by
@@ -490,16 +482,17 @@ __global__ void __launch_bounds__(256, kCanvasCtasPerSm) k_canvas(const __grid_c
     if (x >= cw || y >= ch) continue;
     const long long idx = static_cast<long long>(y) * cw + x;
     uchar4 pv;
-    const std::uint8_t c = (P.cls && !masked) ? P.cls[idx] : kClassFold;
+    // a masked frame's coverage is not the geometry's: every pixel runs the fold
+    const std::uint8_t c = (P.cls && !MASKED) ? P.cls[idx] : kClassFold;
     if (c == kClassFold) {
-      pv = canvas_pixel<CYL>(P, mview, x, y, masked);
+      pv = canvas_pixel<CYL, MASKED>(P, mview, x, y);
     } else if (c == kClassNone) {
       pv = make_uchar4(0, 0, 0, 0);
     } else {
       // a single view provides the pixel: its warp, colour-corrected unless
       // it is the reference (the fold's result, without evaluating the
       // views that do not cover the pixel)
-      pv = warp_cv<CYL>(P.views[c], canvas_lift<CYL>(P, x, y), false);
+      pv = warp_cv<CYL>(P.views[c], canvas_lift<CYL>(P, x, y));
       if (c != P.ref) pv = apply_matrix(mview[c], pv);
     }
     pano[idx] = pv;
@@ -509,6 +502,30 @@ __global__ void __launch_bounds__(256, kCanvasCtasPerSm) k_canvas(const __grid_c
       atomicAdd(&hist[2][pv.z], 1u);
     }
   }
+}
+
+constexpr int kCanvasCtasPerSm = 4;  // resident CTAs per SM (register budget; 5 spills)
+
+// Every canvas pixel once (64 x 4 tiles, grid-stride), per-CTA histogram
+// flushed to the frame histogram; the last CTA builds the balance LUT.
+template <bool CYL>
+__global__ void __launch_bounds__(256, kCanvasCtasPerSm) k_canvas(const __grid_constant__ CanvasParams P,
+                                                   const Geometry* __restrict__ g,
+                                                   DevState* __restrict__ st,
+                                                   uchar4* __restrict__ pano) {
+  __shared__ unsigned int hist[3][256];
+  __shared__ double mview[kMaxViews][9];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    hist[0][i] = 0;
+    hist[1][i] = 0;
+    hist[2][i] = 0;
+  }
+  for (int i = threadIdx.x; i < kMaxViews * 9; i += blockDim.x) mview[i / 9][i % 9] = st->mview[i / 9][i % 9];
+  __syncthreads();
+  if (*P.masked)
+    canvas_tiles<CYL, true>(P, mview, pano, hist);
+  else
+    canvas_tiles<CYL, false>(P, mview, pano, hist);
   __syncthreads();
   for (int i = threadIdx.x; i < 256; i += blockDim.x)
     for (int c = 0; c < 3; ++c)
