@@ -100,6 +100,14 @@ CASES = [
                                 casts=[(0.9, 1, 1), (1, 1, 1), (1, 0.95, 1.1)],
                                 masks=dict(seed=12, views=[0, 2], skip_frames=[2])),
      dict(refine_enabled=0), 4),
+    # full HD: the reference's own 3 x 1080p star rig (canvas
+    # 7082 x 2111, overlaps 713 x 1080), refinement on, flicker -- the sizes
+    # the bench runs at, pinned to the reference itself
+    ("star3_1080p", dict(views=3, width=1920, height=1080, frames=3, obj=dict(
+        enabled=True, half_size=120.0, velocity=(9.0, 3.0)),
+                         casts=[(0.9, 1, 1), (1, 1, 1), (1, 0.95, 1.1)],
+                         flicker=[dict(frame=1, view=0, gains=(1.2, 1.1, 0.9))]),
+     dict(refine_enabled=1), 3),
     # perturbed principal point refined away, 5 frames
     ("principal_refine", dict(seed=5, views=3, width=320, height=240, frames=5,
                               focal_scale=1.02, principal_px=6.0, obj=OBJ,
@@ -177,7 +185,7 @@ def main():
     for name, skw, okw, frames in CASES:
         t0 = time.time()
         sc, st, out = run_case(R, skw, okw, frames)
-        if name in ("c1_defaults", "star3_refine"):
+        if name in ("c1_defaults", "star3_refine", "star3_1080p"):
             out["ops"] = op_digests(R, sc, st)
         doc["cases"][name] = {"scene": skw, "opts": okw, "n_frames": frames, **out}
         print(f"{name}: {frames} frames in {time.time() - t0:.1f} s", flush=True)
