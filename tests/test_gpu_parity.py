@@ -335,7 +335,9 @@ def test_create_from_snapshot_matches_initialize():
                                  {"STITCH_B200_HS_TALL_MIN": "1", "STITCH_B200_HS_ELIN_TALL": "2"},
                                  {"STITCH_B200_HS_SPLIT": "0"},
                                  {"STITCH_B200_PYR_FUSE": "0"},
-                                 {"STITCH_B200_WARP_STAGE": "1"}])
+                                 {"STITCH_B200_WARP_STAGE": "1"},
+                                 {"STITCH_B200_HS_PAIR": "1"},
+                                 {"STITCH_B200_HS_PAIR": "1", "STITCH_B200_HS_FORCE_EXACT": "1"}])
 def test_flow_kernel_variants_bit_exact(env):
     """The register-blocked Jacobi kernel's region variants, sweep
     segmentations and its exact IEEE-division fallback path (forced) all
