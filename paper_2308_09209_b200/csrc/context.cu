@@ -1162,17 +1162,34 @@ int submit_host(Ctx* ctx, const std::uint8_t* const* frames, std::uint8_t* pano_
   // the slot's inputs were last read by its previous frame (retired above,
   // so its staging buffers are free as well)
   CUDA_TRY(cudaStreamWaitEvent(ctx->h2d, ctx->comp_done[slot], 0));
-  // An idle pipeline (the synchronous pattern) stages view by view so each
-  // view's DMA runs while the next one is copied; with frames in flight the
-  // copy engine is busy anyway and one batch costs the least.
-  if (any_stage && !idle) {
+  // An idle pipeline (the synchronous pattern) stages in 4 MiB pieces, each
+  // piece's DMA queued as soon as it is copied so it runs while the next one
+  // is copied; with frames in flight the copy engine is busy anyway and one
+  // batch costs the least.  Measured at C2, synchronous call, pageable input
+  // (scripts/sync_stage_modes.py, median ms per call, 14 / 6 / 2 copy
+  // workers): 4 MiB pieces 3.05 / 3.01 / 3.19, whole views (the former
+  // scheme, STITCH_B200_STAGE_MODE=0) 4.88 / 3.65 / 3.25, one batch (=1)
+  // 4.61 / 3.83 / 3.53; pinned input 2.43.
+  static const int stage_mode = env_int("STITCH_B200_STAGE_MODE", 2);
+  static const size_t stage_chunk =
+      static_cast<size_t>(std::max(1, env_int("STITCH_B200_STAGE_CHUNK_MB", 4))) << 20;
+  if (any_stage && (!idle || stage_mode == 1)) {
     std::vector<CopyPool::Job> jobs;
     for (int v = 0; v < ctx->hg.n_views; ++v)
       if (stage_in[v]) jobs.push_back({ctx->h_stage_in[slot][v], frames[v], ctx->frame_bytes[v]});
     ctx->copier->run(jobs);
   }
   for (int v = 0; v < ctx->hg.n_views; ++v) {
-    if (stage_in[v] && idle)
+    if (stage_in[v] && idle && stage_mode == 2) {
+      for (size_t o = 0; o < ctx->frame_bytes[v]; o += stage_chunk) {
+        const size_t n = std::min(stage_chunk, ctx->frame_bytes[v] - o);
+        ctx->copier->run({{ctx->h_stage_in[slot][v] + o, frames[v] + o, n}});
+        CUDA_TRY(cudaMemcpyAsync(ctx->d_in[slot][v] + o, ctx->h_stage_in[slot][v] + o, n,
+                                 cudaMemcpyHostToDevice, ctx->h2d));
+      }
+      continue;
+    }
+    if (stage_in[v] && idle && stage_mode == 0)
       ctx->copier->run({{ctx->h_stage_in[slot][v], frames[v], ctx->frame_bytes[v]}});
     CUDA_TRY(cudaMemcpyAsync(ctx->d_in[slot][v], stage_in[v] ? ctx->h_stage_in[slot][v] : frames[v],
                              ctx->frame_bytes[v], cudaMemcpyHostToDevice, ctx->h2d));
