@@ -187,7 +187,9 @@ int stitch_b200_initialize_frames(const stitch_b200_config* cfg,
  * width*height bytes, 0 = invalid): the pair bounds and blend weights follow
  * the masked warps of the first frames, as the reference's
  * rebuild_pair_geometry warps first_frames (pipeline.cpp:181-205); the
- * feature refinement warps them with the masked sampler too. */
+ * feature refinement warps them with the masked sampler too.  A masked first
+ * frame without one valid warped pixel is STITCH_B200_EmptyProjection
+ * (checked before the overlaps, as the reference warps every view first). */
 int stitch_b200_initialize_frames_masked(const stitch_b200_config* cfg,
                                          const uint8_t* const* frames,
                                          const uint8_t* const* masks, int device,
@@ -307,8 +309,12 @@ int stitch_b200_wait(stitch_b200_ctx* ctx, long long ticket,
  * bytes, 0 = invalid pixel.  The warp skips masked taps exactly like
  * sample_bilinear (frame.cpp:95-104), and the canvas evaluates the
  * compose fold for every pixel of such a frame; results equal the
- * reference's process_frame on the same masked frames.  masks == NULL is
- * stitch_b200_process / stitch_b200_submit. */
+ * reference's process_frame on the same masked frames.  A masked view
+ * without one valid warped pixel fails the frame with
+ * STITCH_B200_EmptyProjection before it is enqueued, with the temporal state
+ * untouched (warp_frame, geometry.cpp:79, throws before process_frame
+ * changes any state, pipeline.cpp:270-277); submit then issues no ticket.
+ * masks == NULL is stitch_b200_process / stitch_b200_submit. */
 int stitch_b200_process_masked(stitch_b200_ctx* ctx, const uint8_t* const* frames,
                                const uint8_t* const* masks, uint8_t* pano_rgb,
                                uint8_t* pano_mask, stitch_b200_report* report);

@@ -631,6 +631,66 @@ __device__ __forceinline__ bool warp_valid(const double* inv, int W, int H, Lift
   return false;
 }
 
+// Validity of sample_bilinear on a masked frame (frame.cpp:79-109): some
+// neighbour with a positive weight is inside the frame and unmasked -- the
+// weights of sample_crop, so exactly its `wsum > 0`.
+__device__ __forceinline__ bool masked_sample_valid(const std::uint8_t* __restrict__ m, int W,
+                                                    int H, double x, double y) {
+  const double fx0 = floor(x), fy0 = floor(y);
+  const int x0 = static_cast<int>(fx0), y0 = static_cast<int>(fy0);
+  const double ax = x - fx0, ay = y - fy0;
+  const double wx0 = 1.0 - ax, wy0 = 1.0 - ay;
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const double w = (i ? ax : wx0) * (j ? ay : wy0);
+      const unsigned xx = static_cast<unsigned>(x0) + static_cast<unsigned>(i);
+      const unsigned yy = static_cast<unsigned>(y0) + static_cast<unsigned>(j);
+      if (w > 0.0 && xx < static_cast<unsigned>(W) && yy < static_cast<unsigned>(H) &&
+          m[static_cast<size_t>(yy) * W + xx])
+        return true;
+    }
+  return false;
+}
+
+// warp_frame's `any` (geometry.cpp:64-81) for masked frames: grid (CTAs,
+// listed views); each CTA scans its share of the view's rect and stops as
+// soon as any CTA has found a valid pixel of that view.
+template <bool CYL>
+__global__ void __launch_bounds__(256) k_mask_coverage(const Geometry* __restrict__ g,
+                                                       const __grid_constant__ MaskSet ms,
+                                                       unsigned* covered) {
+  const int j = blockIdx.y;
+  const int view = ms.view[j];
+  const ViewDesc& v = g->views[view];
+  const int x0 = ms.rect[j][0], y0 = ms.rect[j][1];
+  const int rw = ms.rect[j][2] - x0, rh = ms.rect[j][3] - y0;
+  if (rw <= 0 || rh <= 0) return;
+  const long long n = static_cast<long long>(rw) * rh;
+  const unsigned bit = 1u << view;
+  const volatile unsigned* cv = covered;
+  for (long long base = blockIdx.x * 256ll; base < n; base += gridDim.x * 256ll) {
+    bool hit = false;
+    const long long idx = base + threadIdx.x;
+    if (idx < n) {
+      const int y = y0 + static_cast<int>(idx / rw);
+      const int x = x0 + static_cast<int>(idx % rw);
+      double sx, sy, sz;
+      warp_point<CYL>(v.inv, canvas_lift<CYL>(*g, x, y), sx, sy, sz);
+      if (!(fabs(sz) < 1e-12) && (!CYL || sz > 0.0)) {
+        const DDivisor dz = ddivisor(sz);
+        hit = masked_sample_valid(ms.mask[j], v.width, v.height, ddiv(sx, dz), ddiv(sy, dz));
+      }
+    }
+    const bool done = threadIdx.x == 0 && (*cv & bit);
+    if (__syncthreads_or(hit || done)) {
+      if (threadIdx.x == 0) atomicOr(covered, bit);
+      return;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_warp_mask(const Geometry* __restrict__ g, int view,
                                                    std::uint8_t* __restrict__ mask) {
   const ViewDesc& v = g->views[view];
@@ -734,6 +794,16 @@ void launch_warp_view(const Geometry* g, int view, const uchar4* frame, std::uin
 
 void launch_warp_mask(const Geometry* g, int view, std::uint8_t* mask, cudaStream_t s) {
   k_warp_mask<<<148 * 8, 256, 0, s>>>(g, view, mask);
+}
+
+void launch_mask_coverage(const Geometry* g, int projection, const MaskSet& ms, long long max_px,
+                          unsigned* covered, cudaStream_t s) {
+  if (ms.n <= 0) return;
+  const dim3 grid(blocks_for(max_px, 256, 148 * 4), ms.n);
+  if (projection == 1)
+    k_mask_coverage<true><<<grid, 256, 0, s>>>(g, ms, covered);
+  else
+    k_mask_coverage<false><<<grid, 256, 0, s>>>(g, ms, covered);
 }
 
 void launch_canvas_class(const CanvasParams& P, std::uint8_t* cls, cudaStream_t s) {

@@ -261,6 +261,9 @@ struct Ctx {
   std::vector<OutChunk> out_chunks[kMaxSlots];
   cudaEvent_t out_ev[kMaxSlots][kOutChunks] = {};
   std::unique_ptr<CopyPool> copier;
+  // coverage of masked frames (EmptyProjection): device word + pinned copy
+  unsigned* d_cover = nullptr;
+  unsigned* h_cover = nullptr;
   std::vector<int> pair_levels;
   float2* d_zero = nullptr;
 
@@ -297,6 +300,7 @@ struct Ctx {
     for (void* p : allocs) cudaFree(p);
     if (h_ptr_ring) cudaFreeHost(h_ptr_ring);
     if (h_report) cudaFreeHost(h_report);
+    if (h_cover) cudaFreeHost(h_cover);
     for (int s = 0; s < kMaxSlots; ++s) {
       for (auto* q : h_stage_in[s])
         if (q) cudaFreeHost(q);
@@ -1134,6 +1138,45 @@ int ensure_staging(Ctx* ctx, int slot) {
   return STITCH_B200_OK;
 }
 
+// EmptyProjection of masked frames: every masked view of this frame must
+// give at least one valid warped pixel (inside its geometric footprint, which
+// holds all of them).  Runs on the upload stream after the mask uploads and
+// waits for it: the error must surface before the frame is enqueued.
+int check_mask_coverage(Ctx* ctx, int slot, const std::uint8_t* const* dmask) {
+  MaskSet ms{};
+  unsigned need = 0;
+  long long max_px = 0;
+  for (int v = 0; v < ctx->hg.n_views; ++v) {
+    if (!dmask[v]) continue;
+    const int* b = ctx->hg.views[v].bbox;
+    ms.view[ms.n] = v;
+    ms.mask[ms.n] = dmask[v];
+    for (int i = 0; i < 4; ++i) ms.rect[ms.n][i] = b[i];
+    max_px = std::max(max_px, static_cast<long long>(b[2] - b[0]) * (b[3] - b[1]));
+    need |= 1u << v;
+    ++ms.n;
+  }
+  if (!ms.n) return STITCH_B200_OK;
+  if (!ctx->d_cover) {
+    void* q = nullptr;
+    CUDA_TRY(cudaMalloc(&q, 16));
+    ctx->allocs.push_back(q);
+    ctx->d_cover = static_cast<unsigned*>(q);
+  }
+  if (!ctx->h_cover)
+    CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_cover), sizeof(unsigned),
+                           cudaHostAllocDefault));
+  CUDA_TRY(cudaMemsetAsync(ctx->d_cover, 0, sizeof(unsigned), ctx->h2d));
+  launch_mask_coverage(ctx->slot[slot].dg, ctx->hg.projection, ms, max_px, ctx->d_cover, ctx->h2d);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_cover, ctx->d_cover, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                           ctx->h2d));
+  CUDA_TRY(cudaStreamSynchronize(ctx->h2d));
+  if ((*ctx->h_cover & need) != need)
+    return fail(STITCH_B200_EmptyProjection, "a masked frame projects to no canvas pixel");
+  return STITCH_B200_OK;
+}
+
 // Host-buffer frame: H2D on the upload stream, compute, D2H on the download
 // stream; returns the frame's ticket.  Pinned caller buffers are copied
 // directly; pageable ones through the slot's pinned staging ring.
@@ -1227,6 +1270,11 @@ int submit_host(Ctx* ctx, const std::uint8_t* const* frames, std::uint8_t* pano_
     dmask[v] = ctx->d_mask[slot][v];
   }
   if (any_mask) {
+    // warp_frame throws EmptyProjection for a view without one valid warped
+    // pixel (geometry.cpp:79), before process_frame touches any state
+    // (pipeline.cpp:270-277): the frame fails here, nothing is enqueued
+    rc = check_mask_coverage(ctx, slot, dmask);
+    if (rc) return rc;
     CUDA_TRY(cudaEventRecord(ctx->h2d_done[slot], ctx->h2d));
     CUDA_TRY(cudaStreamWaitEvent(ctx->slot[slot].cs, ctx->h2d_done[slot], 0));
   }
@@ -1558,7 +1606,18 @@ static int initialize_impl(const stitch_b200_config* cfg, const uint8_t* const* 
     if (rc0) return rc0;
   }
   const std::vector<const uchar4*>* first_rgba = any_mask ? &ff.rgba : nullptr;
+  // rebuild_pair_geometry warps every first frame before it looks at any
+  // overlap: a masked first frame without one valid warped pixel is
+  // EmptyProjection (geometry.cpp:79), before NoOverlap
+  auto masked_empty = [&]() {
+    for (const ViewFootprint& f : views)
+      if (f.masked_empty)
+        return fail(STITCH_B200_EmptyProjection, "a masked first frame projects to no canvas pixel");
+    return static_cast<int>(STITCH_B200_OK);
+  };
   int rc = init_geometry(device, g, make_lift(&in), cfg->n_views, vp, views, pgeo, first_rgba);
+  if (rc) return rc;
+  rc = masked_empty();
   if (rc) return rc;
   std::vector<int> warn(pairs.size(), 0);
   if (cfg->refine_enabled) {
@@ -1573,6 +1632,8 @@ static int initialize_impl(const stitch_b200_config* cfg, const uint8_t* const* 
       for (int i = 0; i < 9; ++i) in.inv_maps[v][i] = invs[v][i];
     fill_views(g, &in);
     rc = init_geometry(device, g, make_lift(&in), cfg->n_views, vp, views, pgeo, first_rgba);
+    if (rc) return rc;
+    rc = masked_empty();
     if (rc) return rc;
   }
   in.n_pairs = static_cast<int>(pairs.size());

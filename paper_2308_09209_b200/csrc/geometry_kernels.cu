@@ -36,6 +36,16 @@ __device__ __forceinline__ int cadd(int a, int c) { return a >= kChamferInf ? kC
 // extent (bbox) of the valid pixels of masks[view] (& masks[other] when
 // other >= 0), plus (views only) a per-column occupancy byte.
 // ext: [minx, miny, maxx, maxy] per job, initialised to (w, h, -1, -1).
+// *flag = 1 if any byte of the plane is nonzero
+__global__ void __launch_bounds__(256) k_plane_any(const std::uint8_t* __restrict__ plane,
+                                                   long long n, int* flag) {
+  bool on = false;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n && !on;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    on = plane[i] != 0;
+  if (__syncthreads_or(on) && threadIdx.x == 0) *flag = 1;
+}
+
 __global__ void __launch_bounds__(256) k_mask_extent(const std::uint8_t* __restrict__ masks,
                                                      long long plane, int w, int h,
                                                      const int2* __restrict__ jobs,
@@ -282,11 +292,21 @@ cudaError_t gpu_init_geometry(const Geometry& geom_in, const double* lift_s, con
                                                   static_cast<std::uint8_t*>(docc.p));
   // masked first frames: from here on (pair bounds, chamfer weights) the masks
   // are the warps of those frames (warp_frame with the masked sampler)
-  if (first_rgba)
+  DevBuf dany;
+  std::vector<int> any_masked(static_cast<size_t>(n_views), 1);
+  if (first_rgba) {
+    GEO_TRY(cudaMalloc(&dany.p, sizeof(int) * n_views));
+    GEO_TRY(cudaMemsetAsync(dany.p, 0, sizeof(int) * n_views, s));
     for (int v = 0; v < n_views && v < static_cast<int>(first_rgba->size()); ++v)
-      if ((*first_rgba)[v])
+      if ((*first_rgba)[v]) {
         launch_warp_view(static_cast<const Geometry*>(dgeom.p), v, (*first_rgba)[v], nullptr,
                          masks + v * P, s, true);
+        // warp_frame's `any` of the masked first frame (geometry.cpp:79)
+        k_plane_any<<<296, 256, 0, s>>>(masks + v * P, P, static_cast<int*>(dany.p) + v);
+      }
+    GEO_TRY(cudaMemcpyAsync(any_masked.data(), dany.p, sizeof(int) * n_views,
+                            cudaMemcpyDeviceToHost, s));
+  }
   if (!pairs.empty())
     k_mask_extent<<<dim3(296, static_cast<unsigned>(pairs.size())), 256, 0, s>>>(
         masks, P, w, h, static_cast<int2*>(djobs.p) + n_views,
@@ -299,6 +319,8 @@ cudaError_t gpu_init_geometry(const Geometry& geom_in, const double* lift_s, con
   views.assign(static_cast<size_t>(n_views), ViewFootprint{});
   for (int v = 0; v < n_views; ++v) {
     ViewFootprint& f = views[v];
+    f.masked_empty = first_rgba && v < static_cast<int>(first_rgba->size()) &&
+                     (*first_rgba)[v] && any_masked[v] == 0;
     f.empty = ext[4 * v + 2] < 0;
     if (f.empty) continue;
     f.bbox[0] = ext[4 * v + 0];

@@ -273,6 +273,17 @@ void launch_warp_view(const Geometry* g, int view, const uchar4* frame, std::uin
 void launch_expand_one(const std::uint8_t* rgb, uchar4* rgba, long long n_px, cudaStream_t s,
                        const std::uint8_t* mask = nullptr);
 void launch_warp_mask(const Geometry* g, int view, std::uint8_t* mask, cudaStream_t s);
+// Coverage of masked frames (warp_frame's EmptyProjection, geometry.cpp:79):
+// for each listed view, does its masked frame give at least one valid warped
+// pixel inside rect?  Sets bit view of *covered (zeroed by the caller).
+struct MaskSet {
+  int n;
+  int view[kMaxViews];
+  const std::uint8_t* mask[kMaxViews];  // W x H bytes, nonzero = valid
+  int rect[kMaxViews][4];               // canvas x0, y0, x1, y1 to scan
+};
+void launch_mask_coverage(const Geometry* g, int projection, const MaskSet& ms, long long max_px,
+                          unsigned* covered, cudaStream_t s);
 // the canvas class map of CanvasParams::cls (init time, geometry only)
 void launch_canvas_class(const CanvasParams& P, std::uint8_t* cls, cudaStream_t s);
 // test entry: n tone curves (build_curve) for the given (m1[i], m2[i])
@@ -336,6 +347,7 @@ struct ViewFootprint {
   int bbox[4] = {0, 0, 0, 0};  // bbox of the warp mask
   int gap[2] = {0, 0};         // widest empty column run inside it
   bool empty = true;
+  bool masked_empty = false;   // a masked first frame warps to no pixel
 };
 struct PairGeometry {
   bool ok = false;             // the pair's masks overlap

@@ -44,7 +44,11 @@ def input_mask(seed, view, frame, width, height):
 
 
 def case_masks(spec, view, frame, width, height):
-    """spec: {"seed": s, "views": [masked view ids], "skip_frames": [...]} -> mask or None"""
+    """spec: {"seed": s, "views": [masked view ids], "skip_frames": [...],
+    "empty": [[frame, view], ...]} -> mask or None; an "empty" entry is a
+    fully masked frame (a PNG whose alpha is 0 everywhere)."""
     if spec is None or view not in spec["views"] or frame in spec.get("skip_frames", []):
         return None
+    if [frame, view] in [list(e) for e in spec.get("empty", [])]:
+        return np.zeros((height, width), np.uint8)
     return input_mask(spec["seed"], view, frame, width, height)
