@@ -7,11 +7,14 @@
 // byte: panorama RGB and mask, colour matrices (bitwise), rank flags,
 // thresholds, frame index.  Prints one JSON line; exit 0 iff identical.
 //
-//   integration_demo <views> <width> <height> <frames> [refine 0|1] [device] [masked 0|1]
+//   integration_demo <views> <width> <height> <frames> [refine 0|1] [device] [masked 0|1|2]
 //
 // masked = 1 gives every view a per-frame Frame::mask (a moving hole, a cut
 // border strip, scattered pixels), first frames included, as a PNG source
-// with alpha would (image_io.cpp:120-127).
+// with alpha would (image_io.cpp:120-127).  masked = 2 also masks frame 2 of
+// the last view completely: the reference throws EmptyProjection there
+// (geometry.cpp:79) and the binding must throw the same code, with both
+// states left untouched for the frames after it.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -41,9 +44,14 @@ int main(int argc, char** argv) {
   spec.frames = std::atoi(argv[4]);
   const bool refine = argc > 5 ? std::atoi(argv[5]) != 0 : true;
   const int device = argc > 6 ? std::atoi(argv[6]) : 0;
-  const bool masked = argc > 7 ? std::atoi(argv[7]) != 0 : false;
+  const int masked_mode = argc > 7 ? std::atoi(argv[7]) : 0;
+  const bool masked = masked_mode != 0;
   auto add_mask = [&](stitch::Frame& f, int view, int t) {
     if (!masked) return;
+    if (masked_mode == 2 && t == 2 && view == spec.views - 1) {
+      f.mask.assign(f.pixel_count(), 0);  // nothing valid: EmptyProjection
+      return;
+    }
     f.mask.assign(f.pixel_count(), 1);
     const int cx = (f.width / 3 + 9 * t + 31 * view) % f.width;
     const int cy = (f.height / 2 + 5 * t) % f.height;
@@ -76,21 +84,33 @@ int main(int argc, char** argv) {
   }
   stitch::PipelineState cpu = stitch::initialize(cfg, first);
   stitch::PipelineState gpu = cpu;  // the same initialized state, driven by the binding
-  int differing = 0, max_diff = 0;
-  bool masks = true, reports = true;
+  int differing = 0, max_diff = 0, errors = 0;
+  bool masks = true, reports = true, errors_equal = true;
   for (int t = 0; t < spec.frames; ++t) {
     std::vector<stitch::Frame> frames;
     for (int v = 0; v < spec.views; ++v) {
       frames.push_back(scene.render_view(v, t));
       add_mask(frames.back(), v, t);
     }
-    const stitch::ProcessResult a = stitch::process_frame(cpu, frames);
-    stitch::ProcessResult b;
+    stitch::ProcessResult a, b;
+    int ea = -1, eb = -1;
+    try {
+      a = stitch::process_frame(cpu, frames);
+    } catch (const stitch::StitchError& e) {
+      ea = static_cast<int>(e.code());
+    }
     try {
       b = stitch::process_frame_b200(gpu, frames, device);
+    } catch (const stitch::StitchError& e) {
+      eb = static_cast<int>(e.code());
     } catch (const std::exception& e) {
       std::printf("{\"error\": \"%s\"}\n", e.what());
       return 1;
+    }
+    if (ea != eb) errors_equal = false;
+    if (ea >= 0 || eb >= 0) {  // both threw (or a mismatch, already counted)
+      errors += ea >= 0;
+      continue;
     }
     const std::vector<std::uint8_t> am =
         a.panorama.has_mask() ? a.panorama.mask
@@ -113,14 +133,16 @@ int main(int argc, char** argv) {
     reports = reports && rep;
   }
   stitch::release_b200(gpu);
-  const bool ok = differing == 0 && masks && reports;
+  const bool ok = differing == 0 && masks && reports && errors_equal;
   std::printf("{\"views\": %d, \"width\": %d, \"height\": %d, \"frames\": %d, \"refine\": %d, "
               "\"masked\": %d, "
               "\"canvas\": [%d, %d], \"frames_differing\": %d, \"max_abs_diff\": %d, "
-              "\"masks_equal\": %s, \"reports_equal\": %s, \"identical\": %s}\n",
-              spec.views, spec.width, spec.height, spec.frames, refine ? 1 : 0, masked ? 1 : 0,
+              "\"masks_equal\": %s, \"reports_equal\": %s, \"errors\": %d, "
+              "\"errors_equal\": %s, \"identical\": %s}\n",
+              spec.views, spec.width, spec.height, spec.frames, refine ? 1 : 0, masked_mode,
               cpu.canvas.width,
               cpu.canvas.height, differing, max_diff, masks ? "true" : "false",
-              reports ? "true" : "false", ok ? "true" : "false");
+              reports ? "true" : "false", errors, errors_equal ? "true" : "false",
+              ok ? "true" : "false");
   return ok ? 0 : 1;
 }

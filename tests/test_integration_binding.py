@@ -37,9 +37,13 @@ def test_binding_links_the_in_tree_library():
                                                             (3, 320, 240, 6, 1, 0),
                                                             (2, 320, 240, 5, 0, 0),
                                                             (2, 640, 480, 6, 1, 1),
-                                                            (3, 320, 240, 4, 0, 1)])
+                                                            (3, 320, 240, 4, 0, 1),
+                                                            (2, 320, 240, 5, 1, 2),
+                                                            (3, 320, 240, 5, 0, 2)])
 def test_binding_reproduces_reference_process_frame(views, w, h, frames, refine, masked):
-    """masked: every frame (the first ones included) carries a Frame::mask."""
+    """masked: every frame (the first ones included) carries a Frame::mask;
+    masked = 2 also masks frame 2 of the last view completely, where the
+    reference throws EmptyProjection and the binding must throw it too."""
     _need_demo()
     r = subprocess.run([DEMO, str(views), str(w), str(h), str(frames), str(refine), "0",
                         str(masked)],
@@ -49,3 +53,4 @@ def test_binding_reproduces_reference_process_frame(views, w, h, frames, refine,
     res = json.loads(lines[-1])
     print(lines[-1])
     assert r.returncode == 0 and res["identical"], res
+    assert res["errors"] == (1 if masked == 2 else 0), res
