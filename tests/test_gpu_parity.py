@@ -595,3 +595,81 @@ def test_pageable_submit_matches_pinned():
             assert list(reps[t].threshold_m1) == list(want[t].report.threshold_m1)
     finally:
         b.close()
+
+
+@pytest.mark.parametrize("kind", ["ring", "chain"])
+def test_masked_extension_rigs_parity(kind):
+    """Masked inputs (Frame::mask) on the extension rigs the reference cannot
+    run -- the 6-camera cylindrical 360-degree ring and a 4-view chain --
+    against the extended oracle: masked first frames set the pair geometry,
+    every frame's panorama / mask / report is identical, and a fully masked
+    frame fails with EmptyProjection on both sides with the temporal state
+    untouched (the frames after it still agree)."""
+    from tests.golden.masks import input_mask
+
+    if kind == "ring":
+        spec = pb.SynthSpec(views=6, width=256, height=144, frames=5, rig="ring",
+                            color_casts=[(1.0 - 0.04 * v, 1.0, 1.0 + 0.03 * v) for v in range(6)])
+        sc = pb.SynthScene(spec)
+        masked_views, empty = (0, 2, 3), (2, 3)
+    else:
+        sc = scene(views=4, width=200, height=150, frames=5,
+                   casts=[(1.0, 1.0, 1.0), (0.9, 1.0, 1.1), (1.1, 0.95, 0.9), (0.95, 1.05, 1.0)])
+        masked_views, empty = (1, 3), (3, 1)
+    nv = sc.spec.views
+    w, h = sc.spec.width, sc.spec.height
+
+    def masks(t):
+        out = []
+        for v in range(nv):
+            if v not in masked_views:
+                out.append(None)
+            elif (t, v) == empty:
+                out.append(np.zeros((h, w), np.uint8))
+            else:
+                out.append(input_mask(31, v, t, w, h))
+        return out
+
+    def frames(t):
+        ms = masks(t)
+        return [pb.Frame(sc.render_view(v, t).data, ms[v]) for v in range(nv)]
+
+    first = frames(0)
+    state = pb.initialize(product_config(sc), first)
+    ost = O.OracleState(oracle_config(sc), first_frames=[f.data for f in first],
+                        first_masks=masks(0))
+    try:
+        assert state.canvas == ost.canvas
+        for k, p in enumerate(state.pairs):
+            view, partner, bounds = ost.pair(k)
+            assert (p.view, p.partner, p.bounds) == (view, partner, bounds)
+            np.testing.assert_array_equal(p.theta_i, ost.pair_weights(k))
+        errors = 0
+        for t in range(sc.spec.frames):
+            fr = frames(t)
+            if t == empty[0]:
+                with pytest.raises(O.OracleError) as oe:
+                    ost.process([f.data for f in fr], masks(t))
+                with pytest.raises(pb.StitchError) as ge:
+                    pb.process_frame(state, fr)
+                assert O.ERROR_NAMES[oe.value.code] == "EmptyProjection"
+                assert ge.value.code == pb.ErrorCode.EmptyProjection
+                errors += 1
+                continue
+            res = pb.process_frame(state, fr)
+            odata, omask, orep = ost.process([f.data for f in fr], masks(t))
+            rep = res.report
+            np.testing.assert_array_equal(res.panorama.mask, omask)
+            assert maxdiff(res.panorama.data, odata) == 0, t
+            for k in range(len(state.pairs)):
+                np.testing.assert_array_equal(rep.color_matrices[k],
+                                              np.array(orep.m[k][:]).reshape(3, 3))
+                assert rep.rank_deficient[k] == bool(orep.rank_deficient[k])
+            assert rep.threshold_m1 == list(orep.threshold_m1)
+            assert rep.threshold_m2 == list(orep.threshold_m2)
+            assert rep.frame_index == orep.frame_index
+        assert errors == 1
+    finally:
+        state.close()
+        ost.close()
+        sc.close()
