@@ -429,8 +429,8 @@ int enqueue_op(Ctx* ctx, const Op& op, cudaStream_t s, int slot = 0) {
       launch_crop_warp(S.cparams, ctx->max_crop_w, ctx->max_crop_h, s);
       return 1;
     case OP_STATS:
-      launch_pair_color(S.dg, S.dst, ctx->d_lists + op.offset, op.count, ctx->max_crop_px, s);
-      return 1;
+      return launch_pair_color(S.dg, S.dst, ctx->d_lists + op.offset, op.count, ctx->max_crop_px,
+                               s);
     case OP_PREP:
       if (!g.n_pairs) return 0;
       if (op.fuse)

@@ -231,7 +231,7 @@ inline int env_int(const char* name, int dflt) {
 // ---- launchers (kernels.cu) ----
 void launch_expand(const Geometry* g, int n_views, long long max_px, cudaStream_t s);
 void launch_crop_warp(const CanvasParams& P, int max_w, int max_h, cudaStream_t s);
-void launch_pair_color(const Geometry* g, DevState* st, const int* pair_list, int n,
+int launch_pair_color(const Geometry* g, DevState* st, const int* pair_list, int n,
                        int max_crop_px, cudaStream_t s);
 void launch_flow_prepare(const Geometry* g, DevState* st, int n_pairs, int max_crop_px,
                          cudaStream_t s);
