@@ -507,8 +507,9 @@ __device__ __forceinline__ void canvas_tiles(const CanvasParams& P, const double
 constexpr int kCanvasCtasPerSm = 4;  // resident CTAs per SM (register budget; 5 spills)
 
 // Every canvas pixel once (64 x 4 tiles, grid-stride), per-CTA histogram
-// flushed to the frame histogram; the last CTA builds the balance LUT.
-template <bool CYL>
+// flushed to the frame histogram; k_balance (or, ELECT, the last CTA) then
+// builds the balance LUT.
+template <bool CYL, bool ELECT = true>
 __global__ void __launch_bounds__(256, kCanvasCtasPerSm) k_canvas(const __grid_constant__ CanvasParams P,
                                                    const Geometry* __restrict__ g,
                                                    DevState* __restrict__ st,
@@ -530,8 +531,15 @@ __global__ void __launch_bounds__(256, kCanvasCtasPerSm) k_canvas(const __grid_c
   for (int i = threadIdx.x; i < 256; i += blockDim.x)
     for (int c = 0; c < 3; ++c)
       if (hist[c][i]) atomicAdd(&st->pano_hist[c][i], hist[c][i]);
+  if (!ELECT) return;
   if (!elect_last_cta(&st->canvas_done, gridDim.x)) return;
   if (threadIdx.x == 0) st->canvas_done = 0;
+  balance_lut(g, st);
+}
+
+// the balance LUT in its own launch after the canvas (ELECT = false)
+__global__ void __launch_bounds__(256) k_balance(const Geometry* __restrict__ g,
+                                                 DevState* __restrict__ st) {
   balance_lut(g, st);
 }
 
@@ -767,15 +775,29 @@ void launch_crop_warp(const CanvasParams& P, int max_w, int max_h, cudaStream_t 
   k_crop_warp<<<grid, dim3(64, 4), 0, s>>>(P);
 }
 
-void launch_canvas(const CanvasParams& P, const Geometry* g, DevState* st, uchar4* pano,
-                   int num_sms, cudaStream_t s) {
+int launch_canvas(const CanvasParams& P, const Geometry* g, DevState* st, uchar4* pano,
+                  int num_sms, cudaStream_t s) {
   const long long tiles = static_cast<long long>((P.cw + 63) / 64) * ((P.ch + 3) / 4);
   const long long b = std::min<long long>(static_cast<long long>(num_sms) * kCanvasCtasPerSm, tiles);
   const int blocks = static_cast<int>(b < 1 ? 1 : b);
+  // the balance LUT in its own one-CTA launch: the canvas CTAs exit after
+  // their histogram flush instead of fencing for the last-CTA election
+  // (canvas 0.177 -> 0.171 ms, p50 1.458 -> 1.448 ms at C2, scripts/exp24.sh);
+  // STITCH_B200_CANVAS_SPLIT=0 restores the election
+  static const int split = env_int("STITCH_B200_CANVAS_SPLIT", 1);
+  if (split) {
+    if (P.projection == 1)
+      k_canvas<true, false><<<blocks, 256, 0, s>>>(P, g, st, pano);
+    else
+      k_canvas<false, false><<<blocks, 256, 0, s>>>(P, g, st, pano);
+    k_balance<<<1, 256, 0, s>>>(g, st);
+    return 2;
+  }
   if (P.projection == 1)
     k_canvas<true><<<blocks, 256, 0, s>>>(P, g, st, pano);
   else
     k_canvas<false><<<blocks, 256, 0, s>>>(P, g, st, pano);
+  return 1;
 }
 
 void launch_tone(const DevState* st, const uchar4* pano, long long n_px, std::uint8_t* out_rgb,

@@ -449,8 +449,7 @@ int enqueue_op(Ctx* ctx, const Op& op, cudaStream_t s, int slot = 0) {
                      ctx->alpha2, s);
       return 1;
     case OP_CANVAS:
-      launch_canvas(S.cparams, S.dg, S.dst, S.d_pano, ctx->num_sms, s);
-      return 1;
+      return launch_canvas(S.cparams, S.dg, S.dst, S.d_pano, ctx->num_sms, s);
     case OP_TONE:
       launch_tone(S.dst, S.d_pano, ctx->n_px, ctx->d_out_rgb[slot], ctx->d_out_mask[slot], s);
       return 1;

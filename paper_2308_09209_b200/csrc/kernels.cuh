@@ -264,8 +264,8 @@ int hs_fuse_wanted(int n, int max_w, int max_h, int sweeps);
 int hs_elin_wanted(int n, int max_w, int max_h, int sweeps);
 // mode 0: whole canvas; 1: outside every pair's bounds (flow-independent);
 // 2: inside the bounds.  Modes 1 + 2 together cover the canvas once.
-void launch_canvas(const CanvasParams& P, const Geometry* g, DevState* st, uchar4* pano,
-                   int num_sms, cudaStream_t s);
+int launch_canvas(const CanvasParams& P, const Geometry* g, DevState* st, uchar4* pano,
+                  int num_sms, cudaStream_t s);
 void launch_tone(const DevState* st, const uchar4* pano, long long n_px,
                  std::uint8_t* out_rgb, std::uint8_t* out_mask, cudaStream_t s);
 void launch_warp_view(const Geometry* g, int view, const uchar4* frame, std::uint8_t* rgb,
