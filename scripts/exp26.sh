@@ -1,4 +1,5 @@
 # crop warp: rows per thread 1 / 2 / 4
+# (the STITCH_B200_CROP_RPT variant was removed after this measurement: no gain)
 set -u
 O=gpurun_out
 for r in 2 4; do STITCH_B200_CROP_RPT=$r python -m pytest tests/test_ref_pin.py tests/test_gpu_parity.py -m gpu -q -x -k "not variants" > $O/e26_r${r}_tests.log 2>&1; echo "rpt=$r tests rc=$?"; done
