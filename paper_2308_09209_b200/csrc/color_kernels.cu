@@ -32,7 +32,6 @@ __device__ __forceinline__ int sidx(int a, int b) { return a * 2 + (b > a ? b - 
 __device__ void pair_solve(const PairDesc& p, int k, DevState* __restrict__ st) {
   __shared__ unsigned char lut[3][256];
   __shared__ unsigned long long cref[3][256];
-  __shared__ unsigned long long mom[18];
   PairStats& in = st->stats[k];
   const int v = threadIdx.x;  // level owned by this thread
   const unsigned long long n = in.n;
@@ -105,7 +104,7 @@ __device__ void pair_solve(const PairDesc& p, int k, DevState* __restrict__ st) 
   }
   __syncthreads();
   // exact integer moments: every thread's 18 terms, reduced per warp by
-  // shuffles, the 8 warp partials summed by thread 0 (integer: any order)
+  // shuffles, the 8 warp partials summed below (integer: any order)
   __shared__ unsigned long long wmom[8][18];
   const unsigned long long vv = static_cast<unsigned long long>(v);
 #pragma unroll
@@ -121,30 +120,44 @@ __device__ void pair_solve(const PairDesc& p, int k, DevState* __restrict__ st) 
     if (lane == 0) wmom[wid][q] = x;
   }
   __syncthreads();
-  if (threadIdx.x < 18) {
-    unsigned long long t = 0;
-    for (int i = 0; i < 8; ++i) t += wmom[i][threadIdx.x];
-    mom[threadIdx.x] = t;
+  // TransferWindow push (newest first, capacity-clamped) and the window
+  // sums, one thread per moment entry (18) plus one for the counts: the
+  // entries are independent, so the global reads and writes of the ring
+  // overlap instead of running as one thread's dependent chain
+  PairWindow& w = st->windows[k];
+  const int size = w.size < w.capacity ? w.size + 1 : w.capacity;
+  __shared__ unsigned long long wsum[19];
+  if (threadIdx.x < 19) {
+    const int q = threadIdx.x;
+    unsigned long long cur;
+    if (q < 18) {
+      cur = 0;
+      for (int i = 0; i < 8; ++i) cur += wmom[i][q];
+    } else {
+      cur = n;
+    }
+    auto slot = [&](int e) -> unsigned long long& {
+      return q < 9 ? w.e[e].xtx[q] : (q < 18 ? w.e[e].xty[q - 9] : w.e[e].n);
+    };
+    unsigned long long old[3];
+    for (int e = 0; e + 1 < size; ++e) old[e] = slot(e);
+    unsigned long long sum = cur;
+    for (int e = size - 1; e > 0; --e) {
+      slot(e) = old[e - 1];
+      sum += old[e - 1];
+    }
+    slot(0) = cur;
+    wsum[q] = sum;
   }
   __syncthreads();
   if (threadIdx.x != 0) return;
-  PairWindow& w = st->windows[k];
-  const int size = w.size < w.capacity ? w.size + 1 : w.capacity;
-  for (int i = size - 1; i > 0; --i) w.e[i] = w.e[i - 1];
-  for (int i = 0; i < 9; ++i) {
-    w.e[0].xtx[i] = mom[i];
-    w.e[0].xty[i] = mom[9 + i];
-  }
-  w.e[0].n = n;
   w.size = size;
-  unsigned long long sx[9] = {0}, sy[9] = {0}, total = 0;
-  for (int e = 0; e < size; ++e) {
-    for (int i = 0; i < 9; ++i) {
-      sx[i] += w.e[e].xtx[i];
-      sy[i] += w.e[e].xty[i];
-    }
-    total += w.e[e].n;
+  unsigned long long sx[9], sy[9];
+  for (int i = 0; i < 9; ++i) {
+    sx[i] = wsum[i];
+    sy[i] = wsum[9 + i];
   }
+  const unsigned long long total = wsum[18];
   double normal[9], xty[9], m[9], sv[3];
   for (int i = 0; i < 9; ++i) {
     normal[i] = static_cast<double>(sx[i]);
