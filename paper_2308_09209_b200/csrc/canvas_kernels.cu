@@ -265,7 +265,16 @@ __device__ void balance_lut(const Geometry* __restrict__ g, DevState* __restrict
   __shared__ int sm1[3], sm2[3], first1[3], first2[3];
   __shared__ unsigned long long wtot[8];
   __shared__ int ok;
+  // the threshold history and the frame counter, staged in shared memory by
+  // parallel loads so thread 0's update below is not a chain of dependent
+  // global round trips
+  constexpr int kBsInts = static_cast<int>(sizeof(BalanceState) / sizeof(int));
+  __shared__ int sbs[kBsInts];
+  __shared__ long long s_counter;
   const int v = threadIdx.x;
+  int* gbs = reinterpret_cast<int*>(st->balance);
+  if (v < kBsInts) sbs[v] = gbs[v];
+  if (v == kBsInts) s_counter = *st->frame_counter;
   unsigned int hist[3];
   for (int c = 0; c < 3; ++c) {
     hist[c] = st->pano_hist[c][v];
@@ -307,9 +316,9 @@ __device__ void balance_lut(const Geometry* __restrict__ g, DevState* __restrict
   __syncthreads();
   if (v == 0) {
     ok = 0;
-    st->report.frame_index = *st->frame_counter;
+    st->report.frame_index = s_counter;
     if (tot != 0) {
-      BalanceState& bs = *st->balance;
+      BalanceState& bs = *reinterpret_cast<BalanceState*>(sbs);
       if (bs.n == 3) {
         for (int i = 0; i < 2; ++i)
           for (int c = 0; c < 3; ++c) {
@@ -351,9 +360,10 @@ __device__ void balance_lut(const Geometry* __restrict__ g, DevState* __restrict
       st->report.m1[c] = ok ? sm1[c] : 0;
       st->report.m2[c] = ok ? sm2[c] : 0;
     }
-    ++*st->frame_counter;
+    *st->frame_counter = s_counter + 1;
   }
   __syncthreads();
+  if (v < kBsInts) gbs[v] = sbs[v];
   for (int c = 0; c < 3; ++c)
     st->lut[c][v] = ok ? curve_entry(v, sm1[c], sm2[c], g->gamma_dark, g->gamma_bright,
                                      g->target_black, g->target_white)
