@@ -212,8 +212,8 @@ __global__ void __launch_bounds__(256) k_crop_warp_staged(const __grid_constant_
 // (flow.cpp:282-322) evaluated on demand.  Inside a pair's bounds the raw
 // warped samples already computed for the overlap crops are reused
 // (bit-identical: same sampler).  Also the balance histogram of the composed
-// panorama (compute_histogram, histogram.cpp:5-18); the last CTA turns it
-// into the tone LUT (global balancing, pipeline.cpp:336-355).
+// panorama (compute_histogram, histogram.cpp:5-18); k_balance turns it into
+// the tone LUT (global balancing, pipeline.cpp:336-355).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ bool fused_pixel(const CanvasParams& P, const CanvasPair& p, int dx,
                                             int dy, uchar4& out) {
@@ -254,7 +254,8 @@ __device__ __forceinline__ bool fused_pixel(const CanvasParams& P, const CanvasP
   return true;
 }
 
-// Global balancing on the last CTA: find_thresholds (color_balance.cpp:8-38),
+// Global balancing, one CTA (k_balance, or the canvas's last CTA):
+// find_thresholds (color_balance.cpp:8-38),
 // history push (pipeline.cpp:340-345), smooth_thresholds
 // (color_balance.cpp:40-63), build_curve (color_balance.cpp:65-104).
 __device__ unsigned char curve_entry(int v, int m1, int m2, double gamma_dark,

@@ -24,7 +24,8 @@ namespace stitch_b200_dev {
 
 __device__ __forceinline__ int sidx(int a, int b) { return a * 2 + (b > a ? b - 1 : b); }
 
-// The per-pair solve, executed by the pair's last CTA (256 threads):
+// The per-pair solve, one 256-thread CTA per pair (k_pair_solve, or the
+// pair's last statistics CTA):
 // histogram_specification (color_transfer.cpp:28-55), revised-row moments,
 // TransferWindow push (color_transfer.cpp:16-21), solve_color_matrix with
 // the rank guard (color_transfer.cpp:73-99), and the degrade rules of
