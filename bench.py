@@ -582,6 +582,22 @@ class CpuRunner:
             self.st = O.OracleState(cfg, first_frames=self.frames[0])
             sc.close()
 
+    def geometry(self):
+        """canvas size, pair bounds and refined-pair count of the initialized
+        state: the same values the B200 arm reports for the workload."""
+        cw, ch = int(self.st.canvas[0]), int(self.st.canvas[1])
+        pairs, refined = [], 0
+        for k in range(self.st.n_pairs()):
+            pr = self.st.pair(k)
+            if self.kind == "reference":
+                _, b, warn = pr
+            else:
+                _, _, b = pr
+                warn = self.st.refine_warning(k)
+            pairs.append([int(x) for x in b])
+            refined += 0 if warn else 1
+        return [cw, ch], pairs, refined
+
     def rate(self, seconds, max_frames=None, warmup=1):
         for i in range(warmup):
             self.st.process(self.frames[i % len(self.frames)])
@@ -664,6 +680,7 @@ def run_reference(args):
         if time.perf_counter() - t0 > budget:
             break
     el = time.perf_counter() - t0
+    canvas, pairs, refined = r.geometry()
     r.close()
     v = n / el
     if kind == "reference":
@@ -677,7 +694,11 @@ def run_reference(args):
            "n_gpus": 0, "steps": n, "warmup": args.warmup, "ms_per_step": round(1e3 * el / n, 2),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
            "dtype": "u8 (fp64 warp, fp32 flow)", "data": "synthetic",
-           "config": {"workload": wl["desc"], "config_key": args.config},
+           "config": {"workload": wl["desc"], "config_key": args.config,
+                      "cameras": wl["views"], "camera_size": [wl["width"], wl["height"]],
+                      "canvas": canvas, "pairs": pairs, "streams_total": 1,
+                      "refined_pairs": refined,
+                      "parallelism": f"one stream on {threads} host threads (CPU reference arm)"},
            "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": threads, "kind": kind,
                             "sample": f"{n} of {args.steps} requested frames within a "
                                       f"{budget:.0f} s budget ({what})"},
