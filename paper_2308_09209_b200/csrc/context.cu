@@ -810,6 +810,20 @@ int build_context(const stitch_b200_init* in, int device,
     plan.push_back({OP_TONE});
     plan.push_back({OP_EVENT, 0, 0, 0, 0, 0, 5});
 
+    // TMA tensor maps of the kq planes (TMA-staged plain segments)
+    if (hs_tma_wanted() && !hs_table.empty()) {
+      struct alignas(64) Map128 {
+        unsigned char b[128];
+      };
+      std::vector<Map128> maps(hs_table.size());
+      for (size_t i = 0; i < hs_table.size(); ++i)
+        if (!encode_kq_map(&maps[i], hs_table[i].kq, hs_table[i].w, hs_table[i].h))
+          return fail(STITCH_B200_Unsupported, "cuTensorMapEncodeTiled failed");
+      Map128* dm = nullptr;
+      CUDA_TRY(ctx->alloc(&dm, maps.size()));
+      CUDA_TRY(cudaMemcpy(dm, maps.data(), maps.size() * sizeof(Map128), cudaMemcpyHostToDevice));
+      for (size_t i = 0; i < hs_table.size(); ++i) hs_table[i].kq_map = dm + i;
+    }
     // upload tables + geometry + state
     CUDA_TRY(ctx->alloc(&S.d_hs, hs_table.size() + 1));
     CUDA_TRY(ctx->alloc(&S.d_hp, hp_table.size() + 1));

@@ -188,6 +188,9 @@ struct HsTask {
   // epilogue linearisation (last segment of a warp iteration): the next warp
   // iteration's constants, from lin_a / lin_b and this segment's result
   float4* kq_next;
+  // TMA tensor map (CUtensorMap, 64-byte aligned, in device memory) of the
+  // kq plane as a 4w x h float tensor, for the TMA-staged plain segment
+  const void* kq_map;
 };
 
 struct PyrTask {
@@ -247,6 +250,10 @@ int hs_segments(int sweeps);
 // segment lengths of one warp iteration at a level (tasks n, max w x h)
 std::vector<int> hs_split(int n, int max_w, int max_h, int sweeps);
 cudaError_t prepare_hs(int sweeps);
+// TMA-staged plain segments (STITCH_B200_HS_TMA): whether they are on, and
+// the CUtensorMap (128 bytes) of a w x h float4 plane
+bool hs_tma_wanted();
+bool encode_kq_map(void* map128, const float4* kq, int w, int h);
 void launch_hs_prepare(const PrepTask* tasks, int n, int max_w, int max_h, float alpha2,
                        cudaStream_t s);
 // fuse_lin: 0 plain segment; 1 the segment first linearises the warp
