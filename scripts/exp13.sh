@@ -1,4 +1,5 @@
 # Sweep variants: where the per-pixel denominator / reciprocal come from
+# (record of a measurement: the exp_so/ builds it swapped in were local, git-ignored and are gone; rebuild with the EXTRA= flags named in DESIGN.md §4 to repeat it)
 # (HS_YSMEM 0 / 1 / 2, prebuilt under exp_so/ys*/).  Parity subset + bench.
 set -u
 O=gpurun_out

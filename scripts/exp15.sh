@@ -1,4 +1,5 @@
 # Last-CTA election fence: membar.sc (ELECT_FENCE=0), fence.acq_rel (1),
+# (record of a measurement: the exp_so/ builds it swapped in were local, git-ignored and are gone; rebuild with the EXTRA= flags named in DESIGN.md §4 to repeat it)
 # release atomic + acq_rel (2); prebuilt under exp_so/ef*/.
 set -u
 O=gpurun_out
