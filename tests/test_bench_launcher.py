@@ -61,3 +61,19 @@ def test_c5_sixty_four_streams_sharded_over_two_ranks():
     res = json.loads([ln for ln in p.stdout.splitlines() if ln.startswith("{")][0])
     assert res["scaling"] == "strong" and res["config"]["streams_total"] == 64
     assert res["config"]["streams_this_rank"] == 32
+
+
+@pytest.mark.gpu
+def test_both_arms_report_the_same_workload_geometry():
+    """The reference arm (the compiled reference on c1) and the B200 arm name
+    the same workload: same canvas, pair bounds and refined pairs, computed
+    independently by each arm's own initialize."""
+    ref = _run(["--impl", "reference", "--config", "c1", "--steps", "1", "--warmup", "0"])
+    gpu = _run(["--config", "c1", "--steps", "3", "--warmup", "3", "--e2e-steps", "3",
+                "--no-cpu-baseline"], timeout=900)
+    assert ref.returncode == 0 and gpu.returncode == 0, ref.stderr[-2000:] + gpu.stderr[-2000:]
+    rc = json.loads([ln for ln in ref.stdout.splitlines() if ln.startswith("{")][-1])["config"]
+    gc = json.loads([ln for ln in gpu.stdout.splitlines() if ln.startswith("{")][-1])["config"]
+    for key in ("workload", "config_key", "cameras", "camera_size", "canvas", "pairs",
+                "refined_pairs"):
+        assert rc[key] == gc[key], (key, rc[key], gc[key])
