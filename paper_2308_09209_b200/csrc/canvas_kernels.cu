@@ -51,6 +51,7 @@ __device__ __forceinline__ void expand_span(const std::uint8_t* __restrict__ src
 }
 
 __global__ void __launch_bounds__(256) k_expand(const Geometry* __restrict__ g) {
+  pdl_wait();
   const int v = blockIdx.y;
   const ViewDesc& vd = g->views[v];
   expand_span(g->in.frames[v], g->in.masked ? g->in.masks[v] : nullptr, g->rgba[v],
@@ -100,6 +101,7 @@ __device__ __forceinline__ uchar4 warp_cv(const CanvasView& v, Lift L) {
 }
 
 __global__ void __launch_bounds__(256) k_crop_warp(const __grid_constant__ CanvasParams P) {
+  pdl_wait();
   const int k = blockIdx.z >> 1;
   const int side = blockIdx.z & 1;
   const CanvasPair& p = P.pairs[k];
@@ -131,6 +133,7 @@ __global__ void __launch_bounds__(256) k_crop_warp(const __grid_constant__ Canva
 constexpr int kStageW = 64, kStageH = 24;
 
 __global__ void __launch_bounds__(256) k_crop_warp_staged(const __grid_constant__ CanvasParams P) {
+  pdl_wait();
   __shared__ uchar4 win[kStageH * kStageW];
   __shared__ int s_wx0, s_wy0, s_ww, s_wh;
   const int k = blockIdx.z >> 1;
@@ -525,6 +528,7 @@ __global__ void __launch_bounds__(256, kCanvasCtasPerSm) k_canvas(const __grid_c
                                                    const Geometry* __restrict__ g,
                                                    DevState* __restrict__ st,
                                                    uchar4* __restrict__ pano) {
+  pdl_wait();
   __shared__ unsigned int hist[3][256];
   __shared__ double mview[kMaxViews][9];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) {
@@ -551,6 +555,7 @@ __global__ void __launch_bounds__(256, kCanvasCtasPerSm) k_canvas(const __grid_c
 // the balance LUT in its own launch after the canvas (ELECT = false)
 __global__ void __launch_bounds__(256) k_balance(const Geometry* __restrict__ g,
                                                  DevState* __restrict__ st) {
+  pdl_wait();
   balance_lut(g, st);
 }
 
@@ -561,6 +566,7 @@ __global__ void __launch_bounds__(256) k_tone(const DevState* __restrict__ st,
                                               const uchar4* __restrict__ pano, long long n_px,
                                               std::uint8_t* __restrict__ out_rgb,
                                               std::uint8_t* __restrict__ out_mask) {
+  pdl_wait();
   __shared__ unsigned char lut[3][256];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) {
     lut[0][i] = st->lut[0][i];

@@ -250,6 +250,7 @@ template <bool ELECT, bool VEC>
 __global__ void __launch_bounds__(256) k_pair_color(const Geometry* __restrict__ g,
                                                     DevState* __restrict__ st,
                                                     const int* __restrict__ list) {
+  pdl_wait();
   __shared__ unsigned int pk[3][256];  // count << 19 | sum of x_a1, bin x_b
   __shared__ unsigned int s2[3][256];  // sum of x_a2, bin x_b
   __shared__ unsigned int hr[3][256];
@@ -332,6 +333,7 @@ __global__ void __launch_bounds__(256) k_pair_color(const Geometry* __restrict__
 __global__ void __launch_bounds__(256) k_pair_solve(const Geometry* __restrict__ g,
                                                     DevState* __restrict__ st,
                                                     const int* __restrict__ list) {
+  pdl_wait();
   const int k = list[blockIdx.x];
   pair_solve(g->pairs[k], k, st);
 }

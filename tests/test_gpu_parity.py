@@ -340,6 +340,8 @@ def test_create_from_snapshot_matches_initialize():
                                  {"STITCH_B200_COLOR_VEC": "1", "STITCH_B200_COLOR_SPLIT": "0"},
                                  {"STITCH_B200_CANVAS_SPLIT": "0"},
                                  {"STITCH_B200_HS_TMA": "1"},
+                                 {"STITCH_B200_PDL": "0"},
+                                 {"STITCH_B200_PDL": "2"},
                                  {"STITCH_B200_HS_PAIR": "1"},
                                  {"STITCH_B200_HS_PAIR": "1", "STITCH_B200_HS_FORCE_EXACT": "1"}])
 def test_flow_kernel_variants_bit_exact(env):
