@@ -543,6 +543,7 @@ __global__ void __launch_bounds__(256, kCanvasCtasPerSm) k_canvas(const __grid_c
   else
     canvas_tiles<CYL, false>(P, mview, pano, hist);
   __syncthreads();
+  if (!ELECT) pdl_trigger();  // only the histogram flush remains
   for (int i = threadIdx.x; i < 256; i += blockDim.x)
     for (int c = 0; c < 3; ++c)
       if (hist[c][i]) atomicAdd(&st->pano_hist[c][i], hist[c][i]);

@@ -309,6 +309,7 @@ __global__ void __launch_bounds__(256) k_pair_color(const Geometry* __restrict__
   }
   atomicAdd(&cnt, local);
   __syncthreads();
+  if (!ELECT) pdl_trigger();  // only the flush of the tables remains
   PairStats& out = st->stats[k];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) {
     for (int c = 0; c < 3; ++c) {
